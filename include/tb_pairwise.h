@@ -1,0 +1,182 @@
+/*
+ * tb_pairwise.h — C-ABI of the B200-native memory-safe pairwise-kernel hot
+ * path (kNN + SGPR statistics + kernel MVM).  Plain pointers and sizes only;
+ * no torch or C++ types cross this boundary.
+ *
+ * The reference ("tensorbudget", /root/reference/pkg/src/tensorbudget) is a
+ * pure-Python package whose operator API for this path is the graph builder
+ * + interpreter pair.  Each entry point below replaces the piece of that API
+ * named beside it; INTEGRATION.md shows the ctypes binding a maintainer adds.
+ *
+ * Conventions (mirroring the reference):
+ *   - row-major, C-contiguous device buffers (interpreter.py:35-38,543);
+ *   - dtype TB_F32 / TB_F64 only (ir.py:32-51);
+ *   - kNN parameters: database first, queries second (frontend.py:108-109);
+ *   - results ascending, equal distances resolve to the lower data index
+ *     (interpreter.py:379-381);
+ *   - inputs are read-only; the library never allocates device memory: the
+ *     caller passes a workspace whose size the planner returns;
+ *   - every function returns a status code; tb_last_error() gives the
+ *     thread-local message (the reference raises BudgetExceeded /
+ *     EvaluationError / ValueError / UnsplittableCandidate instead,
+ *     interpreter.py:40-54, frontend.py:103-106, split.py:31-32).
+ *   - all device work is stream-ordered on the given cudaStream_t (passed as
+ *     void*); there is no global mutable state besides the error string.
+ */
+#ifndef TB_PAIRWISE_H
+#define TB_PAIRWISE_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TB_API __attribute__((visibility("default")))
+#else
+#define TB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define TB_OK 0
+#define TB_ERR_ARG 1          /* EvaluationError / ValueError analogue      */
+#define TB_ERR_BUDGET 2       /* BudgetExceeded analogue                    */
+#define TB_ERR_UNSPLITTABLE 3 /* UnsplittableCandidate analogue             */
+#define TB_ERR_CUDA 4         /* CUDA runtime / launch failure              */
+#define TB_ERR_UNSUPPORTED 5  /* shape outside the compiled kernel set      */
+#define TB_ERR_NO_DEVICE 6    /* no sm_100 device visible                   */
+
+/* element types (ir.py:32-51) */
+#define TB_F32 0
+#define TB_F64 1
+
+/* kNN metrics (frontend.py:19) */
+#define TB_METRIC_L2 0
+#define TB_METRIC_L1 1
+#define TB_METRIC_COSINE 2
+
+/* kNN candidate engines */
+#define TB_ENGINE_AUTO 0
+#define TB_ENGINE_TC3 1   /* tcgen05 bf16x3 split cross term (fp32-class)   */
+#define TB_ENGINE_SIMT 2  /* CUDA-core fp32 cross term                      */
+#define TB_ENGINE_TC1 3   /* tcgen05 single-pass bf16 + certified re-rank   */
+
+/* SGPR kernels */
+#define TB_KERNEL_RBF 0
+#define TB_KERNEL_MATERN32 1
+
+/*
+ * kNN plan: the runtime replacement of the reference's compile-time
+ * memory tiler (PassConfig pipeline.py:18-41, plan_split split.py:285-301).
+ * Filled by tb_knn_plan_create; treat as opaque except for the documented outputs.
+ */
+typedef struct tb_knn_plan {
+  /* problem */
+  int64_t n, m, d, k;
+  int32_t metric, dtype, out_dtype, engine;
+  /* memory contract */
+  int64_t memory_limit;    /* bytes; <= 0 means unlimited                    */
+  int64_t resident_bytes;  /* caller-owned device bytes counted in the limit */
+  /* planner outputs */
+  int32_t cand;            /* K': candidates kept per (slice, query)         */
+  int32_t slices;          /* database slices per chunk (CTA columns)        */
+  int64_t chunk_rows;      /* database rows staged per chunk                 */
+  int64_t n_chunks;
+  int64_t d_pad, m_pad;    /* tensor-core padded extents                     */
+  int64_t workspace_bytes; /* caller must pass at least this much           */
+  int64_t output_bytes;    /* dist[m,k] (out_dtype) + idx[m,k] (int64)        */
+  int64_t peak_bytes;      /* resident + workspace + output: <= memory_limit */
+  int64_t off[16];         /* workspace carve-up (internal)                  */
+} tb_knn_plan;
+
+/* Replaces build_knn(n, m, d, k, metric, dtype) + run_pipeline(PassConfig)
+ * (frontend.py:98-114, pipeline.py:44-60): validates arguments exactly as
+ * build_knn does (k in [1, n], known metric) and sizes every tile so that
+ * resident_bytes + workspace + outputs <= memory_limit.  Fails with
+ * TB_ERR_BUDGET when no tiling fits (the reference would raise
+ * BudgetExceeded at run time, interpreter.py:149-151). */
+TB_API int tb_knn_plan_create(int64_t n, int64_t m, int64_t d, int64_t k, int32_t metric,
+                int32_t dtype, int32_t out_dtype, int32_t engine,
+                int64_t memory_limit, int64_t resident_bytes,
+                tb_knn_plan* plan);
+
+/* Replaces evaluate(knn_graph, [x, q], budget) (interpreter.py:522-551) for
+ * the kNN graph family: x[n,d], q[m,d] (plan dtype) -> out_dist[m,k]
+ * (plan out_dtype, squared L2 as the reference's rewritten graph computes,
+ * match_replace.py:149-155) and out_idx[m,k] (int64, + index_base so a
+ * database shard reports global indices).  Asynchronous on `stream`. */
+TB_API int tb_knn_run(const tb_knn_plan* plan, const void* x, const void* q,
+               int64_t index_base, void* out_dist, int64_t* out_idx,
+               void* workspace, int64_t workspace_bytes, void* stream);
+
+/* tb_knn_run plus timing hooks: when events != NULL it records
+ * events[2c] / events[2c+1] (cudaEvent_t) on `stream` immediately before /
+ * after the candidate-engine launch of database chunk c (c < n_events/2),
+ * so a caller can time the dominant kernel inside a larger timed region. */
+TB_API int tb_knn_run_ex(const tb_knn_plan* plan, const void* x, const void* q,
+                         int64_t index_base, void* out_dist, int64_t* out_idx,
+                         void* workspace, int64_t workspace_bytes, void* stream,
+                         void** events, int32_t n_events);
+
+/* Merge L per-shard result lists (each [m,k], ascending, dtype `dtype`) into
+ * the global top-k with ties -> lower global index.  No reference
+ * counterpart: the reference splits queries, never the database
+ * (split.py:221-222), so this is the cross-GPU merge the north star adds. */
+TB_API int tb_topk_merge(const void* dist_lists, const int64_t* idx_lists,
+                  int32_t n_lists, int64_t m, int64_t k, int32_t dtype,
+                  void* out_dist, int64_t* out_idx, void* stream);
+
+/* Number of queries the last tb_knn_run on this plan sent to the exact fp64
+ * fallback (read from the workspace; synchronises the stream). */
+TB_API int tb_knn_fallback_count(const tb_knn_plan* plan, const void* workspace,
+                          void* stream, int64_t* count);
+
+/* ---------------- SGPR sufficient statistics ----------------------------
+ * Sigma = Kuf Kuf^T (M x M, fp64, full symmetric), v = Kuf y (M, fp64),
+ * yy = y^T y, for X[N,dim], y[N], Z[M,dim] (dtype), accumulated over N in
+ * ascending order.  No reference counterpart; the nearest
+ * is the contracted-dim running add of split.py:322-324,539-547, which the
+ * reference cannot apply to Kuf Kuf^T (split.py:210-214).  accumulate != 0
+ * adds into Sigma/v/yy instead of overwriting (for N streamed in calls). */
+typedef struct tb_sgpr_plan {
+  int64_t N, M, dim;
+  int32_t kernel, dtype;
+  int64_t memory_limit, resident_bytes;
+  int64_t chunk_n;          /* training points per streamed chunk           */
+  int64_t workspace_bytes;
+  int64_t output_bytes;     /* Sigma + v + yy                               */
+  int64_t peak_bytes;
+  int64_t off[8];
+} tb_sgpr_plan;
+
+TB_API int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel,
+                 int32_t dtype, int64_t memory_limit, int64_t resident_bytes,
+                 tb_sgpr_plan* plan);
+
+TB_API int tb_sgpr_stats_run(const tb_sgpr_plan* plan, const void* X, const void* y,
+                      const void* Z, double variance,
+                      const double* lengthscales, double* Sigma, double* v,
+                      double* yy, int32_t accumulate, void* workspace,
+                      int64_t workspace_bytes, void* stream);
+
+/* ---------------- kernel MVM --------------------------------------------
+ * out[i] = sum_j k(X_i, Z_j) w_j in fp64 accumulation, X[n,dim], Z[M,dim]
+ * (dtype), w[M] fp64 -> out[n] fp64.  Replaces evaluate(build_kernel_mvm)
+ * (frontend.py:34-54: 1-D inputs, SE kernel, op order scale->exp->variance)
+ * and is the SGPR predictive mean K*u w.  Streams Z tiles; never forms K. */
+TB_API int tb_kernel_mvm(const void* X, const void* Z, const double* w, int64_t n,
+                  int64_t M, int64_t dim, int32_t kernel, int32_t dtype,
+                  double variance, const double* lengthscales, double* out,
+                  void* stream);
+
+/* ---------------- misc ---------------------------------------------------*/
+TB_API const char* tb_last_error(void);
+/* compiled-in capabilities: bit0 tcgen05 kNN, bit1 SIMT kNN, bit2 SGPR,
+ * bit3 kernel MVM; returns the library version in the high 16 bits. */
+TB_API int32_t tb_capabilities(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TB_PAIRWISE_H */

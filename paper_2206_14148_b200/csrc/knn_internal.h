@@ -1,0 +1,76 @@
+// knn_internal.h — launchers shared between the C-ABI layer and kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace tb {
+
+// workspace slots of tb_knn_plan::off
+enum KnnSlot {
+  kQn64 = 0,    // double[m]        ||q||^2 (fp64, exact)
+  kQnorm = 1,   // float[m]         ||q||   (for the error bound)
+  kStats = 2,   // u32[64]          [0] = max ||x|| bits, [1] = fallback count
+  kFbList = 3,  // int[m]           queries sent to the exact fallback
+  kXn = 4,      // float[chunk_pad] ||x||^2 of the staged chunk (fp32)
+  kCandS = 5,   // float[L][m][K']  per-(slice,query) candidate scores
+  kCandI = 6,   // int  [L][m][K']
+  kRunS = 7,    // float[2][m][K']  running merged candidates (ping-pong)
+  kRunI = 8,    // int  [2][m][K']
+  kQHi = 9,     // bf16[m_pad][d_pad]   (tensor-core engines)
+  kQLo = 10,
+  kXHi = 11,    // bf16[chunk_pad][d_pad]
+  kXLo = 12,
+  kNumSlots = 13
+};
+
+struct KnnDims {
+  int64_t n, m, d, k;
+  int cand;
+  int64_t d_pad, m_pad;
+};
+
+// prep
+int launch_query_prep(int dtype, const void* q, int64_t m, int64_t d,
+                      double* qn64, float* qnorm, __nv_bfloat16* qhi,
+                      __nv_bfloat16* qlo, int64_t m_pad, int64_t d_pad,
+                      cudaStream_t st);
+int launch_db_prep(int dtype, const void* x, int64_t rows, int64_t d,
+                   float* xn, unsigned* xmax_bits, __nv_bfloat16* xhi,
+                   __nv_bfloat16* xlo, int64_t rows_pad, int64_t d_pad,
+                   cudaStream_t st);
+// SIMT candidate engine: writes lists [2*slices][m][cand]
+int launch_knn_simt(int dtype, int cand, const void* x_chunk, const void* q,
+                    const float* xn, int64_t rows, int64_t m, int64_t d,
+                    int slices, int idx_base, float* cand_s, int* cand_i,
+                    cudaStream_t st);
+// tcgen05 candidate engine: writes lists [lists][m][cand]; returns lists
+int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi,
+                  const __nv_bfloat16* xlo, const __nv_bfloat16* qhi,
+                  const __nv_bfloat16* qlo, const float* xn, int64_t rows,
+                  int64_t rows_pad, int64_t m, int64_t m_pad, int64_t d_pad,
+                  int slices, int idx_base, float* cand_s, int* cand_i,
+                  cudaStream_t st);
+int tc_lists_per_slice();
+// merge L lists (+ optional previous running list) into out
+int launch_knn_merge(int cand, const float* in_s, const int* in_i, int lists,
+                     const float* prev_s, const int* prev_i, int64_t m,
+                     float* out_s, int* out_i, cudaStream_t st);
+// exact fp64 re-rank + certification
+int launch_knn_refine(int dtype, int out_dtype, int cand, const float* cs,
+                      const int* ci, const void* x, const void* q,
+                      const double* qn64, const float* qnorm,
+                      const unsigned* stats, int64_t n, int64_t m, int64_t d,
+                      int64_t k, double c1, double c2, void* out_dist,
+                      int64_t* out_idx, int64_t index_base, int* fb_list,
+                      cudaStream_t st);
+int launch_knn_fallback(int dtype, int out_dtype, const void* x, const void* q,
+                        int64_t n, int64_t m, int64_t d, int64_t k,
+                        const unsigned* stats, const int* fb_list,
+                        void* out_dist, int64_t* out_idx, int64_t index_base,
+                        cudaStream_t st);
+int launch_topk_merge(const void* dist_lists, const int64_t* idx_lists,
+                      int n_lists, int64_t m, int64_t k, int dtype,
+                      void* out_dist, int64_t* out_idx, cudaStream_t st);
+
+}  // namespace tb

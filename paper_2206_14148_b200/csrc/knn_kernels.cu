@@ -1,0 +1,547 @@
+// knn_kernels.cu — data prep, SIMT candidate engine, candidate merge, exact
+// fp64 re-rank + certification, and the exact fp64 fallback.
+//
+// Pipeline per shard:
+//   query_prep -> [per chunk: db_prep -> candidate engine -> merge]
+//   -> refine (exact fp64 distances of the K' candidates, ties -> lower
+//      index, certification against the engine's error bound)
+//   -> fallback (exact fp64 brute force for uncertified queries; normally 0)
+//
+// The reference computes the distances as ``norms + (-2)·dot`` in the input
+// dtype (match_replace.py:149-155) and selects with a full stable argsort
+// (interpreter.py:371-390).  Here candidates are *selected* with the fast
+// approximate score s_j = ||x_j||^2 - 2 q·x_j (||q||^2 is constant per row),
+// and the returned distances/ordering come from an exact fp64 re-rank.
+#include "tb_common.cuh"
+#include "knn_internal.h"
+
+namespace tb {
+
+// ------------------------------------------------------------------ prep --
+
+// One warp per row: ||row||^2 in fp64 and optional bf16 hi/lo split with
+// zero padding to [rows_pad, d_pad] (tensor-core operand layout, K-major).
+template <typename T>
+__global__ void rows_prep_kernel(const T* __restrict__ src, int64_t rows,
+                                 int64_t d, double* __restrict__ n64,
+                                 float* __restrict__ n32,
+                                 float* __restrict__ norm32,
+                                 unsigned* __restrict__ max_bits,
+                                 __nv_bfloat16* __restrict__ hi,
+                                 __nv_bfloat16* __restrict__ lo,
+                                 int64_t rows_pad, int64_t d_pad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t limit = hi ? rows_pad : rows;
+  if (r >= limit) return;
+  const int64_t cols = hi ? d_pad : d;
+  double acc = 0.0;
+  for (int64_t j = lane; j < cols; j += 32) {
+    const double v = (r < rows && j < d) ? (double)src[r * d + j] : 0.0;
+    acc += v * v;
+    if (hi) {
+      const __nv_bfloat16 h = __double2bfloat16(v);
+      const __nv_bfloat16 l = __double2bfloat16(v - (double)__bfloat162float(h));
+      hi[r * d_pad + j] = h;
+      lo[r * d_pad + j] = l;
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0 && r < rows) {
+    if (n64) n64[r] = acc;
+    if (n32) n32[r] = (float)acc;
+    const float nrm = (float)sqrt(acc) * (1.0f + 1e-6f);
+    if (norm32) norm32[r] = nrm;
+    if (max_bits) atomicMax(max_bits, __float_as_uint(nrm));
+  }
+}
+
+template <typename T>
+static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
+                     float* n32, float* norm32, unsigned* max_bits,
+                     __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t rows_pad,
+                     int64_t d_pad, cudaStream_t st) {
+  const int64_t limit = hi ? rows_pad : rows;
+  if (limit <= 0) return TB_OK;
+  const int warps = 8;
+  const int64_t blocks = ceil_div(limit, warps);
+  rows_prep_kernel<T><<<(unsigned)blocks, warps * 32, 0, st>>>(
+      (const T*)src, rows, d, n64, n32, norm32, max_bits, hi, lo, rows_pad, d_pad);
+  TB_LAUNCH_CHECK("rows_prep");
+  return TB_OK;
+}
+
+int launch_query_prep(int dtype, const void* q, int64_t m, int64_t d,
+                      double* qn64, float* qnorm, __nv_bfloat16* qhi,
+                      __nv_bfloat16* qlo, int64_t m_pad, int64_t d_pad,
+                      cudaStream_t st) {
+  if (dtype == TB_F32)
+    return rows_prep<float>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st);
+  return rows_prep<double>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st);
+}
+
+int launch_db_prep(int dtype, const void* x, int64_t rows, int64_t d,
+                   float* xn, unsigned* xmax_bits, __nv_bfloat16* xhi,
+                   __nv_bfloat16* xlo, int64_t rows_pad, int64_t d_pad,
+                   cudaStream_t st) {
+  if (dtype == TB_F32)
+    return rows_prep<float>(x, rows, d, nullptr, xn, nullptr, xmax_bits, xhi, xlo, rows_pad, d_pad, st);
+  return rows_prep<double>(x, rows, d, nullptr, xn, nullptr, xmax_bits, xhi, xlo, rows_pad, d_pad, st);
+}
+
+// ------------------------------------------------- SIMT candidate engine --
+// CTA = 128 queries x one database slice; 256 threads, 8x8 fp32 micro-tile
+// per thread over 128x128 score tiles; the score tile is staged in shared
+// memory and scanned by 256 threads (query row tid&127, column half tid>>7)
+// that each keep a register top-K' list.  Output: 2 lists per slice.
+constexpr int kSimtTile = 128;
+constexpr int kSimtLd = 132;   // padded k-major operand rows
+constexpr int kSimtSt = 129;   // padded score rows
+constexpr size_t kSimtSmem = (2 * 16 * kSimtLd + kSimtTile * kSimtSt) * sizeof(float);
+
+template <typename T, int KC>
+__global__ void __launch_bounds__(256, 1)
+knn_simt_kernel(const T* __restrict__ x, const T* __restrict__ q,
+                const float* __restrict__ xn, int64_t rows, int m, int d,
+                int64_t rows_per_slice, int idx_base, float* __restrict__ cand_s,
+                int* __restrict__ cand_i) {
+  extern __shared__ __align__(16) float smem[];
+  float* As = smem;                    // [16][kSimtLd]  queries, k-major
+  float* Bs = As + 16 * kSimtLd;       // [16][kSimtLd]  database rows
+  float* St = Bs + 16 * kSimtLd;       // [128][kSimtSt] scores
+
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int q0 = blockIdx.x * kSimtTile;
+  const int64_t r_begin = (int64_t)blockIdx.y * rows_per_slice;
+  const int64_t r_end = min(rows, r_begin + rows_per_slice);
+  const int srow = tid & 127, shalf = tid >> 7;
+  const int lr = tid >> 1, lc = (tid & 1) * 8;
+  const bool qvalid = (q0 + lr) < m;
+  const T* qrow = q + (int64_t)(q0 + (qvalid ? lr : 0)) * d;
+
+  TopList<float, KC> L;
+  L.init();
+
+  for (int64_t t0 = r_begin; t0 < r_end; t0 += kSimtTile) {
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+    const bool xvalid = (t0 + lr) < r_end;
+    const T* xrow = x + (t0 + (xvalid ? lr : 0)) * d;
+    float ra[8], rb[8];
+    auto load = [&](int kk) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = kk + lc + j;
+        ra[j] = (qvalid && c < d) ? (float)qrow[c] : 0.f;
+        rb[j] = (xvalid && c < d) ? (float)xrow[c] : 0.f;
+      }
+    };
+    load(0);
+    for (int kk = 0; kk < d; kk += 16) {
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        As[(lc + j) * kSimtLd + lr] = ra[j];
+        Bs[(lc + j) * kSimtLd + lr] = rb[j];
+      }
+      __syncthreads();
+      if (kk + 16 < d) load(kk + 16);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const float4 a0 = *reinterpret_cast<const float4*>(&As[c * kSimtLd + ty * 8]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&As[c * kSimtLd + ty * 8 + 4]);
+        const float4 b0 = *reinterpret_cast<const float4*>(&Bs[c * kSimtLd + tx * 4]);
+        const float4 b1 = *reinterpret_cast<const float4*>(&Bs[c * kSimtLd + 64 + tx * 4]);
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+    }
+    // epilogue: score = ||x||^2 - 2 q.x, staged for the scan
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int col = j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4);
+        const int64_t g = t0 + col;
+        St[(ty * 8 + i) * kSimtSt + col] =
+            g < r_end ? fmaf(-2.f, acc[i][j], xn[g]) : INFINITY;
+      }
+    __syncthreads();
+    if (q0 + srow < m) {
+      const float* srow_p = St + srow * kSimtSt + shalf * 64;
+      const int base = idx_base + (int)(t0 + shalf * 64);
+#pragma unroll 4
+      for (int c = 0; c < 64; ++c) {
+        const float v = srow_p[c];
+        if (v < L.worst()) L.insert(v, base + c);
+      }
+    }
+  }
+  if (q0 + srow < m) {
+    const int64_t o = (((int64_t)blockIdx.y * 2 + shalf) * m + q0 + srow) * KC;
+#pragma unroll
+    for (int p = 0; p < KC; ++p) {
+      cand_s[o + p] = L.s[p];
+      cand_i[o + p] = L.i[p];
+    }
+  }
+}
+
+template <typename T, int KC>
+static int simt_launch(const void* x, const void* q, const float* xn,
+                       int64_t rows, int64_t m, int64_t d, int slices,
+                       int idx_base, float* cs, int* ci, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    TB_CUDA_TRY(cudaFuncSetAttribute(knn_simt_kernel<T, KC>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSimtSmem));
+    configured = true;
+  }
+  const int64_t rps = round_up(ceil_div(rows, slices), kSimtTile);
+  dim3 grid((unsigned)ceil_div(m, kSimtTile), (unsigned)slices);
+  knn_simt_kernel<T, KC><<<grid, 256, kSimtSmem, st>>>(
+      (const T*)x, (const T*)q, xn, rows, (int)m, (int)d, rps, idx_base, cs, ci);
+  TB_LAUNCH_CHECK("knn_simt");
+  return TB_OK;
+}
+
+int launch_knn_simt(int dtype, int cand, const void* x, const void* q,
+                    const float* xn, int64_t rows, int64_t m, int64_t d,
+                    int slices, int idx_base, float* cs, int* ci,
+                    cudaStream_t st) {
+#define TB_SIMT_CASE(KC)                                                       \
+  case KC:                                                                     \
+    return dtype == TB_F32                                                     \
+               ? simt_launch<float, KC>(x, q, xn, rows, m, d, slices, idx_base, cs, ci, st) \
+               : simt_launch<double, KC>(x, q, xn, rows, m, d, slices, idx_base, cs, ci, st);
+  switch (cand) {
+    TB_SIMT_CASE(16)
+    TB_SIMT_CASE(32)
+    TB_SIMT_CASE(64)
+  }
+#undef TB_SIMT_CASE
+  return fail(TB_ERR_UNSUPPORTED, "SIMT engine: unsupported candidate count");
+}
+
+// ------------------------------------------------------- candidate merge --
+template <int KC>
+__global__ void knn_merge_kernel(const float* __restrict__ in_s,
+                                 const int* __restrict__ in_i, int lists,
+                                 const float* __restrict__ prev_s,
+                                 const int* __restrict__ prev_i, int64_t m,
+                                 float* __restrict__ out_s, int* __restrict__ out_i) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= m) return;
+  TopList<float, KC> L;
+  L.init();
+  const int total = lists + (prev_s ? 1 : 0);
+  for (int l = lane; l < total; l += 32) {
+    const float* s = l < lists ? in_s + ((int64_t)l * m + r) * KC : prev_s + r * KC;
+    const int* ix = l < lists ? in_i + ((int64_t)l * m + r) * KC : prev_i + r * KC;
+    for (int p = 0; p < KC; ++p) {
+      const float v = s[p];
+      const int j = ix[p];
+      if (!lex_less(v, j, L.worst(), L.worst_idx())) break;  // lists are sorted
+      L.insert(v, j);
+    }
+  }
+  float* os = out_s + r * KC;
+  int* oi = out_i + r * KC;
+  warp_drain(L, KC, [&](int t, float v, int j) {
+    os[t] = v;
+    oi[t] = j;
+  });
+}
+
+int launch_knn_merge(int cand, const float* in_s, const int* in_i, int lists,
+                     const float* prev_s, const int* prev_i, int64_t m,
+                     float* out_s, int* out_i, cudaStream_t st) {
+  if (m <= 0) return TB_OK;
+  const int warps = 4;
+  const unsigned blocks = (unsigned)ceil_div(m, warps);
+  switch (cand) {
+    case 16: knn_merge_kernel<16><<<blocks, warps * 32, 0, st>>>(in_s, in_i, lists, prev_s, prev_i, m, out_s, out_i); break;
+    case 32: knn_merge_kernel<32><<<blocks, warps * 32, 0, st>>>(in_s, in_i, lists, prev_s, prev_i, m, out_s, out_i); break;
+    case 64: knn_merge_kernel<64><<<blocks, warps * 32, 0, st>>>(in_s, in_i, lists, prev_s, prev_i, m, out_s, out_i); break;
+    default: return fail(TB_ERR_UNSUPPORTED, "merge: unsupported candidate count");
+  }
+  TB_LAUNCH_CHECK("knn_merge");
+  return TB_OK;
+}
+
+// --------------------------------------------- exact re-rank + certify --
+// One warp per query.  Exact fp64 sum((q - x)^2) for the K' candidates,
+// sorted by (distance, index); the k best are the answer.  Certified when
+// every point outside the candidate set provably ranks after the k-th:
+//   approx(j) >= T* (K'-th merged approx score)   and
+//   |approx - exact| <= E = c1 ||q|| max||x|| + c2 max||x||^2
+// => need T* - E > exact_score(k-th).  Otherwise the query goes to the
+// exact fallback.
+template <typename T, typename OT, int KC>
+__global__ void knn_refine_kernel(const float* __restrict__ cs,
+                                  const int* __restrict__ ci,
+                                  const T* __restrict__ x, const T* __restrict__ q,
+                                  const double* __restrict__ qn64,
+                                  const float* __restrict__ qnorm,
+                                  unsigned* __restrict__ stats, int64_t m,
+                                  int64_t d, int k, double c1, double c2,
+                                  OT* __restrict__ out_dist,
+                                  int64_t* __restrict__ out_idx,
+                                  int64_t index_base, int* __restrict__ fb_list) {
+  constexpr int PER = (KC + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= m) return;
+  const T* qr = q + r * d;
+  double ds[PER];
+  int js[PER];
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    ds[p] = INFINITY;
+    js[p] = kInvalidIdx;
+  }
+  for (int c = 0; c < KC; ++c) {
+    const int j = ci[r * KC + c];
+    double acc = 0.0;
+    if (j != kInvalidIdx) {
+      const T* xr = x + (int64_t)j * d;
+      for (int64_t t = lane; t < d; t += 32) {
+        const double df = (double)qr[t] - (double)xr[t];
+        acc = fma(df, df, acc);
+      }
+    }
+    acc = warp_sum(acc);
+    if ((c & 31) == lane) {
+#pragma unroll
+      for (int p = 0; p < PER; ++p)
+        if (p == (c >> 5)) {
+          ds[p] = j != kInvalidIdx ? acc : INFINITY;
+          js[p] = j;
+        }
+    }
+  }
+  double kth = INFINITY;
+  for (int t = 0; t < k; ++t) {
+    double v = INFINITY;
+    int j = kInvalidIdx;
+#pragma unroll
+    for (int p = 0; p < PER; ++p)
+      if (lex_less(ds[p], js[p], v, j)) {
+        v = ds[p];
+        j = js[p];
+      }
+    warp_lex_min(v, j);
+#pragma unroll
+    for (int p = 0; p < PER; ++p)
+      if (js[p] == j && ds[p] == v) {
+        ds[p] = INFINITY;
+        js[p] = kInvalidIdx;
+      }
+    if (lane == 0) {
+      out_dist[r * k + t] = (OT)v;
+      out_idx[r * k + t] = (int64_t)j + index_base;
+    }
+    kth = v;
+  }
+  if (lane == 0) {
+    const float tstar = cs[r * KC + KC - 1];
+    if (isfinite(tstar)) {
+      const double X = (double)__uint_as_float(stats[0]);
+      const double E = c1 * (double)qnorm[r] * X + c2 * X * X;
+      const double exact_score_k = kth - qn64[r];
+      if (!((double)tstar - E > exact_score_k)) {
+        const int pos = atomicAdd(reinterpret_cast<int*>(&stats[1]), 1);
+        fb_list[pos] = (int)r;
+      }
+    }
+  }
+}
+
+template <typename T, typename OT>
+static int refine_dispatch(int cand, const float* cs, const int* ci,
+                           const void* x, const void* q, const double* qn64,
+                           const float* qnorm, unsigned* stats, int64_t m,
+                           int64_t d, int64_t k, double c1, double c2,
+                           void* od, int64_t* oi, int64_t base, int* fb,
+                           cudaStream_t st) {
+  const int warps = 4;
+  const unsigned blocks = (unsigned)ceil_div(m, warps);
+#define TB_REFINE_CASE(KC)                                                   \
+  case KC:                                                                   \
+    knn_refine_kernel<T, OT, KC><<<blocks, warps * 32, 0, st>>>(             \
+        cs, ci, (const T*)x, (const T*)q, qn64, qnorm, stats, m, d, (int)k,  \
+        c1, c2, (OT*)od, oi, base, fb);                                      \
+    break;
+  switch (cand) {
+    TB_REFINE_CASE(16)
+    TB_REFINE_CASE(32)
+    TB_REFINE_CASE(64)
+    default: return fail(TB_ERR_UNSUPPORTED, "refine: unsupported candidate count");
+  }
+#undef TB_REFINE_CASE
+  TB_LAUNCH_CHECK("knn_refine");
+  return TB_OK;
+}
+
+int launch_knn_refine(int dtype, int out_dtype, int cand, const float* cs,
+                      const int* ci, const void* x, const void* q,
+                      const double* qn64, const float* qnorm,
+                      const unsigned* stats, int64_t n, int64_t m, int64_t d,
+                      int64_t k, double c1, double c2, void* out_dist,
+                      int64_t* out_idx, int64_t index_base, int* fb_list,
+                      cudaStream_t st) {
+  (void)n;
+  if (m <= 0) return TB_OK;
+  unsigned* s = const_cast<unsigned*>(stats);
+  if (dtype == TB_F32) {
+    if (out_dtype == TB_F32)
+      return refine_dispatch<float, float>(cand, cs, ci, x, q, qn64, qnorm, s, m, d, k, c1, c2, out_dist, out_idx, index_base, fb_list, st);
+    return refine_dispatch<float, double>(cand, cs, ci, x, q, qn64, qnorm, s, m, d, k, c1, c2, out_dist, out_idx, index_base, fb_list, st);
+  }
+  if (out_dtype == TB_F32)
+    return refine_dispatch<double, float>(cand, cs, ci, x, q, qn64, qnorm, s, m, d, k, c1, c2, out_dist, out_idx, index_base, fb_list, st);
+  return refine_dispatch<double, double>(cand, cs, ci, x, q, qn64, qnorm, s, m, d, k, c1, c2, out_dist, out_idx, index_base, fb_list, st);
+}
+
+// ------------------------------------------------- exact fp64 fallback --
+// Persistent: each CTA takes flagged queries p = blockIdx.x, +gridDim.x, ...
+// and brute-forces the whole shard in fp64 (direct differences).
+template <typename T, typename OT, int KC>
+__global__ void __launch_bounds__(256)
+knn_fallback_kernel(const T* __restrict__ x, const T* __restrict__ q, int64_t n,
+                    int64_t d, int k, const unsigned* __restrict__ stats,
+                    const int* __restrict__ fb_list, OT* __restrict__ out_dist,
+                    int64_t* __restrict__ out_idx, int64_t index_base) {
+  __shared__ double sd[8][KC];
+  __shared__ int si[8][KC];
+  const int count = *reinterpret_cast<const volatile int*>(&stats[1]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int p = blockIdx.x; p < count; p += gridDim.x) {
+    const int64_t r = fb_list[p];
+    const T* qr = q + r * d;
+    TopList<double, KC> L;
+    L.init();
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      const T* xr = x + j * d;
+      double acc = 0.0;
+      for (int64_t t = 0; t < d; ++t) {
+        const double df = (double)qr[t] - (double)xr[t];
+        acc = fma(df, df, acc);
+      }
+      L.offer(acc, (int)j);
+    }
+    warp_drain(L, KC, [&](int t, double v, int j) {
+      sd[warp][t] = v;
+      si[warp][t] = j;
+    });
+    __syncthreads();
+    if (warp == 0) {
+      TopList<double, KC> M;
+      M.init();
+      if (lane < 8)
+        for (int t = 0; t < KC; ++t) M.offer(sd[lane][t], si[lane][t]);
+      warp_drain(M, k, [&](int t, double v, int j) {
+        out_dist[r * k + t] = (OT)v;
+        out_idx[r * k + t] = (int64_t)j + index_base;
+      });
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T, typename OT>
+static int fallback_dispatch(const void* x, const void* q, int64_t n,
+                             int64_t d, int64_t k, const unsigned* stats,
+                             const int* fb, void* od, int64_t* oi,
+                             int64_t base, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned blocks = (unsigned)(2 * sms);
+  if (k <= 16)
+    knn_fallback_kernel<T, OT, 16><<<blocks, 256, 0, st>>>((const T*)x, (const T*)q, n, d, (int)k, stats, fb, (OT*)od, oi, base);
+  else if (k <= 32)
+    knn_fallback_kernel<T, OT, 32><<<blocks, 256, 0, st>>>((const T*)x, (const T*)q, n, d, (int)k, stats, fb, (OT*)od, oi, base);
+  else if (k <= 64)
+    knn_fallback_kernel<T, OT, 64><<<blocks, 256, 0, st>>>((const T*)x, (const T*)q, n, d, (int)k, stats, fb, (OT*)od, oi, base);
+  else
+    return fail(TB_ERR_UNSUPPORTED, "fallback: k > 64");
+  TB_LAUNCH_CHECK("knn_fallback");
+  return TB_OK;
+}
+
+int launch_knn_fallback(int dtype, int out_dtype, const void* x, const void* q,
+                        int64_t n, int64_t m, int64_t d, int64_t k,
+                        const unsigned* stats, const int* fb_list,
+                        void* out_dist, int64_t* out_idx, int64_t index_base,
+                        cudaStream_t st) {
+  if (m <= 0) return TB_OK;
+  if (dtype == TB_F32) {
+    if (out_dtype == TB_F32)
+      return fallback_dispatch<float, float>(x, q, n, d, k, stats, fb_list, out_dist, out_idx, index_base, st);
+    return fallback_dispatch<float, double>(x, q, n, d, k, stats, fb_list, out_dist, out_idx, index_base, st);
+  }
+  if (out_dtype == TB_F32)
+    return fallback_dispatch<double, float>(x, q, n, d, k, stats, fb_list, out_dist, out_idx, index_base, st);
+  return fallback_dispatch<double, double>(x, q, n, d, k, stats, fb_list, out_dist, out_idx, index_base, st);
+}
+
+// ------------------------------------------------ cross-shard top-k merge --
+template <typename T, int KC>
+__global__ void topk_merge_kernel(const T* __restrict__ dl,
+                                  const int64_t* __restrict__ il, int lists,
+                                  int64_t m, int k, T* __restrict__ od,
+                                  int64_t* __restrict__ oi) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= m) return;
+  TopList<T, KC> L;
+  L.init();
+  for (int l = lane; l < lists; l += 32) {
+    const T* s = dl + ((int64_t)l * m + r) * k;
+    const int64_t* ix = il + ((int64_t)l * m + r) * k;
+    for (int p = 0; p < k; ++p) {
+      const T v = s[p];
+      const int j = (int)ix[p];
+      if (!lex_less(v, j, L.worst(), L.worst_idx())) break;
+      L.insert(v, j);
+    }
+  }
+  warp_drain(L, k, [&](int t, T v, int j) {
+    od[r * k + t] = v;
+    oi[r * k + t] = j;
+  });
+}
+
+int launch_topk_merge(const void* dist_lists, const int64_t* idx_lists,
+                      int n_lists, int64_t m, int64_t k, int dtype,
+                      void* out_dist, int64_t* out_idx, cudaStream_t st) {
+  if (m <= 0) return TB_OK;
+  const int warps = 4;
+  const unsigned blocks = (unsigned)ceil_div(m, warps);
+#define TB_TM(TT, KC)                                                        \
+  topk_merge_kernel<TT, KC><<<blocks, warps * 32, 0, st>>>(                  \
+      (const TT*)dist_lists, idx_lists, n_lists, m, (int)k, (TT*)out_dist, out_idx)
+  if (dtype == TB_F32) {
+    if (k <= 16) TB_TM(float, 16); else if (k <= 32) TB_TM(float, 32); else if (k <= 64) TB_TM(float, 64);
+    else return fail(TB_ERR_UNSUPPORTED, "topk_merge: k > 64");
+  } else {
+    if (k <= 16) TB_TM(double, 16); else if (k <= 32) TB_TM(double, 32); else if (k <= 64) TB_TM(double, 64);
+    else return fail(TB_ERR_UNSUPPORTED, "topk_merge: k > 64");
+  }
+#undef TB_TM
+  TB_LAUNCH_CHECK("topk_merge");
+  return TB_OK;
+}
+
+}  // namespace tb

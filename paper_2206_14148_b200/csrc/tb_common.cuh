@@ -1,0 +1,141 @@
+// tb_common.cuh — shared device helpers for the pairwise-kernel hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <float.h>
+#include <limits.h>
+#include <string>
+
+#include "../../include/tb_pairwise.h"
+
+namespace tb {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define TB_CUDA_TRY(expr)                                                   \
+  do {                                                                      \
+    cudaError_t _e = (expr);                                                \
+    if (_e != cudaSuccess)                                                  \
+      return ::tb::fail(TB_ERR_CUDA, std::string(#expr) + ": " +            \
+                                         cudaGetErrorString(_e));           \
+  } while (0)
+
+#define TB_LAUNCH_CHECK(what)                                               \
+  do {                                                                      \
+    cudaError_t _e = cudaGetLastError();                                    \
+    if (_e != cudaSuccess)                                                  \
+      return ::tb::fail(TB_ERR_CUDA, std::string("launch ") + (what) +      \
+                                         ": " + cudaGetErrorString(_e));    \
+  } while (0)
+
+constexpr int kInvalidIdx = INT_MAX;
+
+// ------------------------------------------------------- (score, index) --
+// Ordering used everywhere: ascending score, ties -> lower index
+// (the reference TopK's stable argsort, interpreter.py:379-381).
+template <typename S>
+__device__ __forceinline__ bool lex_less(S a, int ia, S b, int ib) {
+  return a < b || (a == b && ia < ib);
+}
+
+// Sorted top-K list held in registers (fully unrolled -> no local memory).
+template <typename S, int K>
+struct TopList {
+  S s[K];
+  int i[K];
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      s[p] = (S)INFINITY;
+      i[p] = kInvalidIdx;
+    }
+  }
+  __device__ __forceinline__ S worst() const { return s[K - 1]; }
+  __device__ __forceinline__ int worst_idx() const { return i[K - 1]; }
+
+  // Insert (v, j); caller guarantees (v, j) < (s[K-1], i[K-1]).
+  __device__ __forceinline__ void insert(S v, int j) {
+    bool done = false;
+#pragma unroll
+    for (int p = K - 1; p > 0; --p) {
+      const bool lt = lex_less(v, j, s[p - 1], i[p - 1]);
+      const S ns = lt ? s[p - 1] : v;
+      const int ni = lt ? i[p - 1] : j;
+      if (!done) {
+        s[p] = ns;
+        i[p] = ni;
+      }
+      done = done || !lt;
+    }
+    if (!done) {
+      s[0] = v;
+      i[0] = j;
+    }
+  }
+  __device__ __forceinline__ void offer(S v, int j) {
+    if (lex_less(v, j, s[K - 1], i[K - 1])) insert(v, j);
+  }
+  // remove the head (smallest); shifts the rest up
+  __device__ __forceinline__ void pop() {
+#pragma unroll
+    for (int p = 0; p < K - 1; ++p) {
+      s[p] = s[p + 1];
+      i[p] = i[p + 1];
+    }
+    s[K - 1] = (S)INFINITY;
+    i[K - 1] = kInvalidIdx;
+  }
+};
+
+// Warp-wide lexicographic argmin of per-lane (v, j); returns the winner in
+// every lane.
+template <typename S>
+__device__ __forceinline__ void warp_lex_min(S& v, int& j) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const S ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+    if (lex_less(ov, oj, v, j)) {
+      v = ov;
+      j = oj;
+    }
+  }
+}
+
+// Drains `count` smallest entries of the per-lane sorted lists (warp-wide
+// k-way merge).  out(t, v, j) is called by lane 0 for t = 0..count-1.
+template <typename S, int K, typename Out>
+__device__ __forceinline__ void warp_drain(TopList<S, K>& L, int count, Out out) {
+  const int lane = threadIdx.x & 31;
+  for (int t = 0; t < count; ++t) {
+    S v = L.s[0];
+    int j = L.i[0];
+    warp_lex_min(v, j);
+    if (L.i[0] == j && L.s[0] == v && j != kInvalidIdx) L.pop();
+    if (lane == 0) out(t, v, j);
+  }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ double to_f64(T v) { return (double)v; }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+}  // namespace tb

@@ -1,0 +1,279 @@
+"""Graph-level drop-in: the reference's builder/interpreter names for this path.
+
+The reference's operator API is ``build_knn`` / ``build_kernel_mvm``
+(frontend.py:22-114) -> ``run_pipeline(graph, PassConfig)``
+(pipeline.py:18-60) -> ``evaluate(graph, inputs, budget)``
+(interpreter.py:522-551) returning ``(outputs, MemoryTrace)``.  These names
+keep that surface for the kNN and kernel-MVM graph families: the "graph" is a
+typed descriptor of the workload (the general IR is out of scope, SURVEY.md
+§2 rows 7-9), and ``evaluate`` dispatches it to the fused CUDA path.  Output
+conventions are the reference's: TopK indices come back in the operand float
+dtype (interpreter.py:385-387), outputs are fresh copies, inputs are never
+written, and ``budget`` counts the inputs (interpreter.py:543-546).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+from enum import Enum
+
+import numpy as np
+
+from .errors import BudgetExceeded, EvaluationError
+
+METRICS = ("l2", "l1", "cosine")
+
+
+class DType(Enum):
+    F32 = ("f32", 4)
+    F64 = ("f64", 8)
+
+    def __init__(self, label: str, byte_size: int):
+        self.label = label
+        self.byte_size = byte_size
+
+    @property
+    def np_dtype(self) -> np.dtype:
+        return np.dtype(np.float32 if self is DType.F32 else np.float64)
+
+    @classmethod
+    def from_np(cls, dtype) -> "DType":
+        dtype = np.dtype(dtype)
+        if dtype == np.float32:
+            return cls.F32
+        if dtype == np.float64:
+            return cls.F64
+        raise ValueError(f"unsupported dtype {dtype}; only f32/f64 tensors exist")
+
+    def __str__(self) -> str:
+        return self.label
+
+
+@dataclass(frozen=True)
+class KernelSpec:
+    """Squared-exponential kernel k(x, y) = variance * exp(-(x-y)^2 / (2 l^2))
+    (frontend.py:22-31)."""
+
+    variance: float = 1.0
+    lengthscale: float = 1.0
+
+    def __post_init__(self):
+        if self.variance <= 0 or self.lengthscale <= 0:
+            raise ValueError("variance and lengthscale must be strictly positive")
+
+
+@dataclass(frozen=True)
+class TensorType:
+    dims: tuple
+    dtype: DType
+
+    @property
+    def byte_size(self) -> int:
+        n = 1
+        for v in self.dims:
+            n *= v
+        return n * self.dtype.byte_size
+
+
+@dataclass(frozen=True)
+class PassConfig:
+    """Same knobs and invariants as pipeline.py:18-41.  The fused path never
+    materialises a split candidate, so the threshold only caps the staging
+    chunk the planner may use (chunk bytes <= tensor_split_size)."""
+
+    tensor_size_threshold: int = 10**9
+    tensor_split_size: int | None = None
+    enable_match_replace: bool = True
+    enable_reorder: bool = True
+    enable_split: bool = True
+
+    def __post_init__(self):
+        if self.tensor_split_size is None:
+            object.__setattr__(self, "tensor_split_size", self.tensor_size_threshold)
+        if self.tensor_size_threshold <= 0 or self.tensor_split_size <= 0:
+            raise ValueError("size options must be positive byte counts")
+        if self.tensor_split_size > self.tensor_size_threshold:
+            raise ValueError(
+                f"tensor_split_size ({self.tensor_split_size}) must not exceed "
+                f"tensor_size_threshold ({self.tensor_size_threshold})")
+
+
+@dataclass(frozen=True)
+class Graph:
+    """Workload descriptor standing in for the reference's SSA graph."""
+
+    name: str
+    kind: str                     # "knn" | "mvm"
+    parameters: tuple             # TensorType per parameter, reference order
+    attrs: dict = field(default_factory=dict)
+    config: PassConfig | None = None
+
+
+@dataclass(frozen=True)
+class TensorValue:
+    array: np.ndarray
+
+    @property
+    def shape(self):
+        return tuple(self.array.shape)
+
+    @property
+    def dtype(self) -> DType:
+        return DType.from_np(self.array.dtype)
+
+    @property
+    def data(self):
+        return self.array
+
+
+@dataclass(frozen=True)
+class MemoryEvent:
+    instruction: str
+    event: str
+    bytes: int
+    live_after: int
+
+    def as_row(self) -> str:
+        return f"{self.instruction},{self.event},{self.bytes},{self.live_after}"
+
+
+@dataclass
+class MemoryTrace:
+    events: list = field(default_factory=list)
+    peak_live_bytes: int = 0
+
+    def to_csv(self) -> str:
+        lines = ["instruction,event,bytes,live_after"]
+        lines.extend(e.as_row() for e in self.events)
+        return "\n".join(lines) + "\n"
+
+
+def build_knn(n: int, m: int, d: int, k: int, metric: str = "l2",
+              dtype: DType = DType.F64) -> Graph:
+    """Brute-force kNN (frontend.py:98-114): parameters x[n,d], q[m,d]; root
+    (distances[m,k], indices[m,k]); ties resolve to the lower data index."""
+    if not 1 <= k <= n:
+        raise ValueError(f"k={k} must satisfy 1 <= k <= n={n}")
+    if metric not in METRICS:
+        raise ValueError(f"metric must be one of {METRICS}")
+    if min(n, m, d) < 1:
+        raise ValueError("n, m and d must be at least 1")
+    return Graph(f"knn_{metric}_n{n}_m{m}_d{d}_k{k}", "knn",
+                 (TensorType((n, d), dtype), TensorType((m, d), dtype)),
+                 {"n": n, "m": m, "d": d, "k": k, "metric": metric, "dtype": dtype})
+
+
+def build_kernel_mvm(n: int, spec: KernelSpec = KernelSpec(),
+                     dtype: DType = DType.F64) -> Graph:
+    """y = K v over 1-D inputs x[n], y[n], v[n] (frontend.py:34-54)."""
+    if n < 1:
+        raise ValueError("n must be at least 1")
+    return Graph(f"se_kernel_mvm_n{n}", "mvm",
+                 tuple(TensorType((n,), dtype) for _ in range(3)),
+                 {"n": n, "spec": spec, "dtype": dtype})
+
+
+def run_pipeline(graph: Graph, config: PassConfig, diagnostics=None) -> Graph:
+    """Records the pass configuration; the fused kernels are already the
+    post-pipeline form (no [m,n,d] or [m,n] intermediate ever exists)."""
+    return replace(graph, config=config)
+
+
+def random_inputs(graph: Graph, seed: int, low: float = -1.0, high: float = 1.0):
+    """Seeded U[low, high) inputs in parameter order (frontend.py:128-138)."""
+    rng = np.random.default_rng(seed)
+    return [rng.uniform(low, high, size=p.dims).astype(p.dtype.np_dtype)
+            for p in graph.parameters]
+
+
+def _check_inputs(graph: Graph, inputs):
+    if len(inputs) != len(graph.parameters):
+        raise EvaluationError(
+            f"graph {graph.name!r} takes {len(graph.parameters)} inputs, got {len(inputs)}")
+    arrays = []
+    for i, (raw, expected) in enumerate(zip(inputs, graph.parameters)):
+        arr = raw.array if isinstance(raw, TensorValue) else np.asarray(raw)
+        try:
+            ok = tuple(arr.shape) == tuple(expected.dims) and \
+                DType.from_np(arr.dtype) == expected.dtype
+        except ValueError:
+            ok = False
+        if not ok:
+            raise EvaluationError(
+                f"input {i} is {arr.dtype}{list(arr.shape)}, expected "
+                f"{expected.dtype}{list(expected.dims)}")
+        arrays.append(np.ascontiguousarray(arr))
+    return arrays
+
+
+def _trace_for(graph: Graph, resident: int, workspace: int, outputs: int) -> MemoryTrace:
+    tr = MemoryTrace()
+    live = 0
+    for i, p in enumerate(graph.parameters):
+        live += p.byte_size
+        tr.events.append(MemoryEvent(f"{graph.name}/param{i}", "alloc", p.byte_size, live))
+    live += outputs
+    tr.events.append(MemoryEvent(f"{graph.name}/outputs", "alloc", outputs, live))
+    live += workspace
+    tr.events.append(MemoryEvent(f"{graph.name}/workspace", "alloc", workspace, live))
+    tr.peak_live_bytes = live
+    for label, b in ((f"{graph.name}/workspace", workspace),
+                     *((f"{graph.name}/param{i}", p.byte_size)
+                       for i, p in enumerate(graph.parameters)),
+                     (f"{graph.name}/outputs", outputs)):
+        live -= b
+        tr.events.append(MemoryEvent(label, "free", b, live))
+    return tr
+
+
+def estimate_peak_memory(graph: Graph, budget: int | None = None) -> int:
+    """Static device peak of ``evaluate`` (planner arithmetic, no device)."""
+    if graph.kind == "knn":
+        from . import neighbors as _knn
+        a = graph.attrs
+        p = _knn.plan(a["n"], a["m"], a["d"], a["k"], metric=a["metric"],
+                      dtype=a["dtype"].np_dtype, memory_limit=budget)
+        return int(p.peak_bytes)
+    if graph.kind == "mvm":
+        return sum(p.byte_size for p in graph.parameters) + graph.parameters[0].byte_size
+    raise EvaluationError(f"no evaluator for graph kind {graph.kind!r}")
+
+
+def evaluate(graph: Graph, inputs, budget: int | None = None, *,
+             poison_freed: bool = False):
+    """Evaluates the graph on the B200 path; returns (outputs, MemoryTrace).
+
+    Raises BudgetExceeded before any device allocation when the planner
+    cannot fit ``budget`` (the reference raises at the offending allocation,
+    interpreter.py:149-151).
+    """
+    arrays = _check_inputs(graph, inputs)
+    from .errors import BudgetExceeded as _BE
+    if graph.kind == "knn":
+        from . import neighbors as _knn
+        a = graph.attrs
+        try:
+            res = _knn.knn(arrays[0], arrays[1], a["k"], metric=a["metric"],
+                           memory_limit=budget, return_result=True)
+        except _BE as exc:
+            raise BudgetExceeded(graph.name, exc.requested, exc.live,
+                                 MemoryTrace(), message=str(exc)) from None
+        p = res.plan
+        trace = _trace_for(graph, int(p.resident_bytes), int(p.workspace_bytes),
+                           int(p.output_bytes))
+        dt = a["dtype"].np_dtype
+        outs = (TensorValue(np.asarray(res.dist, dt).copy()),
+                TensorValue(np.asarray(res.idx).astype(dt)))
+        return outs, trace
+    if graph.kind == "mvm":
+        from . import mvm as _mvm
+        spec = graph.attrs["spec"]
+        x, y, v = arrays
+        total = sum(p.byte_size for p in graph.parameters) + graph.parameters[0].byte_size
+        if budget is not None and total > budget:
+            raise BudgetExceeded(f"{graph.name}/outputs", graph.parameters[0].byte_size,
+                                 total - graph.parameters[0].byte_size, MemoryTrace())
+        out = _mvm.se_kernel_mvm(x, y, v, spec.variance, spec.lengthscale)
+        trace = _trace_for(graph, 0, 0, graph.parameters[0].byte_size)
+        return TensorValue(np.asarray(out, graph.attrs["dtype"].np_dtype)), trace
+    raise EvaluationError(f"no evaluator for graph kind {graph.kind!r}")

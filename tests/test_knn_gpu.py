@@ -1,0 +1,227 @@
+"""kNN parity on the B200: the CUDA path (through the C-ABI) against the
+reference's golden answers and the fp64 oracle.  Gate (north star): indices
+identical except at distance ties within 1e-5 relative; distances within
+1e-4 (the reference's rel_err)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_err
+from oracle import knn as oknn
+import paper_2206_14148_b200 as tb
+from paper_2206_14148_b200 import neighbors, synthetic
+
+pytestmark = pytest.mark.gpu
+
+ENGINES = ["simt", "tc3", "tc1"]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def engines_available():
+    from paper_2206_14148_b200 import _lib
+    out = []
+    for e in ENGINES:
+        try:
+            neighbors.plan(300, 10, 8, 3, engine=e)
+            x = np.random.default_rng(0).standard_normal((300, 8)).astype(np.float32)
+            neighbors.knn(x, x[:10], 3, engine=e)
+            out.append(e)
+        except tb.KernelUnavailable:
+            pass
+    return out
+
+
+@pytest.fixture(scope="module")
+def engines():
+    e = engines_available()
+    assert "simt" in e
+    return e
+
+
+def check(dist, idx, ref_d, ref_i, x, q):
+    rep = oknn.compare(dist, idx, ref_d, ref_i, x, q)
+    assert rep["ok"], rep
+    return rep
+
+
+@pytest.mark.parametrize("name", ["knn_spec_line.npz", "knn_ties.npz"])
+def test_small_kats(name, engines):
+    g = golden(name)
+    for e in engines:
+        d, i = tb.knn(g["x"], g["q"], int(g["k"]), engine=e)
+        assert np.array_equal(i, g["idx"]), e
+        assert rel_err(d, g["dist"]) < 1e-12, e
+
+
+@pytest.mark.parametrize("name", ["knn_c1_uniform.npz", "knn_c1_gauss.npz"])
+def test_c1_f64(name, engines):
+    g = golden(name)
+    n, m, d, k = (int(g[s]) for s in "nmdk")
+    if "uniform" in name:
+        x, q = synthetic.uniform_inputs([(n, d), (m, d)], seed=int(g["seed"]))
+    else:
+        x, q = synthetic.gaussian_knn(n, m, d, seed=int(g["seed"]), dtype=np.float64)
+    for e in engines:
+        dist, idx = tb.knn(x, q, k, engine=e)
+        rep = check(dist, idx, g["dist"], g["idx"], x, q)
+        assert rep["identical"] >= m - 2, (e, rep)
+        assert rel_err(dist, g["dist"]) < 1e-12, e   # fp64 re-rank
+
+
+def test_graph_evaluate_c1(engines):
+    g = golden("knn_c1_uniform.npz")
+    graph = tb.build_knn(int(g["n"]), int(g["m"]), int(g["d"]), int(g["k"]))
+    graph = tb.run_pipeline(graph, tb.PassConfig(tensor_size_threshold=2 * 10**6))
+    ins = tb.random_inputs(graph, seed=int(g["seed"]))
+    (vals, idx), trace = tb.evaluate(graph, ins, budget=50 * 10**6)
+    assert idx.array.dtype == np.float64        # reference: indices in float dtype
+    assert np.array_equal(idx.array.astype(np.int64), g["idx"])
+    assert rel_err(vals.array, g["dist"]) < 1e-12
+    assert trace.peak_live_bytes <= 50 * 10**6
+
+
+def test_c2_full_shape_subset_against_reference(engines):
+    torch = _torch()
+    g = golden("knn_c2_subset.npz")
+    n, m, d, k = (int(g[s]) for s in "nmdk")
+    x, q = synthetic.gaussian_knn(n, m, d, seed=int(g["seed"]), dtype=np.float32)
+    xt = torch.from_numpy(x).cuda()
+    qt = torch.from_numpy(q).cuda()
+    rows = g["rows"]
+    extra = np.random.default_rng(9).choice(m, 64, replace=False)
+    ref_d2, ref_i2 = oknn.exact(x, q[extra], k)
+    for e in engines:
+        torch.cuda.reset_peak_memory_stats()
+        base = torch.cuda.memory_allocated()
+        op = neighbors.KnnOperator(n, m, d, k, engine=e, memory_limit="1GB")
+        dist, idx = op.run(xt, qt)
+        torch.cuda.synchronize()
+        peak = torch.cuda.max_memory_allocated() - base + (n + m) * d * 4
+        assert peak <= 10**9, (e, peak)
+        dist, idx = dist.cpu().numpy(), idx.cpu().numpy()
+        check(dist[rows], idx[rows], g["dist"], g["idx"], x, q[rows])
+        check(dist[extra], idx[extra], ref_d2, ref_i2, x, q[extra])
+        assert op.fallback_count() <= m // 100, e
+
+
+def test_quantized_ties(engines):
+    g = golden("knn_quantized.npz")
+    n, m, d, k = (int(g[s]) for s in "nmdk")
+    x, q = synthetic.quantized_knn(n, m, d, seed=int(g["seed"]))
+    for e in engines:
+        dist, idx = tb.knn(x, q, k, engine=e)
+        check(dist, idx, g["dist"], g["idx"], x, q)
+
+
+@pytest.mark.parametrize("n,m,d,k", [
+    (1, 1, 1, 1), (3, 2, 1, 3), (17, 5, 3, 17), (300, 129, 130, 7),
+    (1000, 257, 64, 50), (4097, 3, 16, 10), (20000, 1, 200, 1)])
+def test_edge_shapes(n, m, d, k, engines):
+    rng = np.random.default_rng(n + m + d + k)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    q = rng.standard_normal((m, d)).astype(np.float32)
+    ref_d, ref_i = oknn.exact(x, q, k)
+    for e in engines:
+        dist, idx = tb.knn(x, q, k, engine=e)
+        check(dist, idx, ref_d, ref_i, x, q)
+
+
+def test_duplicates_resolve_to_lower_index(engines):
+    rng = np.random.default_rng(4)
+    base = rng.standard_normal((50, 12)).astype(np.float32)
+    x = np.concatenate([base, base, base])          # every point three times
+    q = base[:20] + 1e-3
+    ref_d, ref_i = oknn.exact(x, q, 9)
+    for e in engines:
+        dist, idx = tb.knn(x, q, 9, engine=e)
+        check(dist, idx, ref_d, ref_i, x, q)
+
+
+def test_memory_limit_forces_chunks_same_answer(engines):
+    rng = np.random.default_rng(5)
+    n, m, d, k = 200_000, 300, 96, 10
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    q = rng.standard_normal((m, d)).astype(np.float32)
+    ref_d, ref_i = oknn.exact(x, q, k)
+    for e in engines:
+        resident = (n + m) * d * 4
+        p = neighbors.plan(n, m, d, k, engine=e, memory_limit=resident + 30 * 10**6)
+        assert p.peak_bytes <= resident + 30 * 10**6
+        dist, idx = tb.knn(x, q, k, engine=e, memory_limit=resident + 30 * 10**6)
+        check(dist, idx, ref_d, ref_i, x, q)
+
+
+def test_budget_exceeded_raises_before_work():
+    x = np.zeros((10_000, 16))
+    with pytest.raises(tb.BudgetExceeded):
+        tb.knn(x, x[:100], 5, memory_limit="1MB")
+
+
+def test_index_base_and_f64_out(engines):
+    rng = np.random.default_rng(6)
+    x = rng.standard_normal((5000, 32)).astype(np.float32)
+    q = rng.standard_normal((40, 32)).astype(np.float32)
+    ref_d, ref_i = oknn.exact(x, q, 5)
+    for e in engines:
+        dist, idx = tb.knn(x, q, 5, engine=e, index_base=1_000_000, out_dtype=np.float64)
+        assert dist.dtype == np.float64
+        check(dist, idx - 1_000_000, ref_d, ref_i, x, q)
+        assert rel_err(dist, ref_d) < 1e-12
+
+
+def test_fallback_path_is_exact(engines, monkeypatch):
+    monkeypatch.setenv("TB_FORCE_FALLBACK", "1")
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((3000, 20))
+    q = rng.standard_normal((37, 20))
+    ref_d, ref_i = oknn.exact(x, q, 6)
+    res = tb.knn(x, q, 6, engine="simt", return_result=True)
+    assert res.fallback_queries == 37
+    check(res.dist, res.idx, ref_d, ref_i, x, q)
+    assert rel_err(res.dist, ref_d) < 1e-12
+
+
+def test_input_buffers_untouched(engines):
+    torch = _torch()
+    rng = np.random.default_rng(8)
+    x = torch.from_numpy(rng.standard_normal((4000, 40)).astype(np.float32)).cuda()
+    q = torch.from_numpy(rng.standard_normal((70, 40)).astype(np.float32)).cuda()
+    x0, q0 = x.clone(), q.clone()
+    for e in engines:
+        tb.knn(x, q, 4, engine=e)
+    assert torch.equal(x, x0) and torch.equal(q, q0)
+
+
+def test_deterministic_repeats(engines):
+    rng = np.random.default_rng(10)
+    x = rng.standard_normal((30000, 64)).astype(np.float32)
+    q = rng.standard_normal((500, 64)).astype(np.float32)
+    for e in engines:
+        a = tb.knn(x, q, 10, engine=e)
+        b = tb.knn(x, q, 10, engine=e)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_topk_merge_abi():
+    torch = _torch()
+    from paper_2206_14148_b200 import distributed
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((9000, 24))
+    q = rng.standard_normal((33, 24))
+    ref_d, ref_i = oknn.exact(x, q, 8)
+    parts = np.array_split(np.arange(9000), 3)
+    dl, il = [], []
+    for p in parts:
+        d, i = oknn.exact(x[p], q, 8)
+        dl.append(d)
+        il.append(i + p[0])
+    od, oi = distributed.merge_topk(torch.from_numpy(np.stack(dl)).cuda(),
+                                    torch.from_numpy(np.stack(il)).cuda())
+    assert np.array_equal(oi.cpu().numpy(), ref_i)
+    assert rel_err(od.cpu().numpy(), ref_d) < 1e-12
