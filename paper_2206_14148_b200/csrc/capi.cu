@@ -26,7 +26,7 @@ int fail(int code, const std::string& msg) {
 constexpr int kPlanSms = 148;
 constexpr int64_t kAlign = 256;
 // engine chosen for TB_ENGINE_AUTO
-constexpr int kAutoEngine = TB_ENGINE_SIMT;
+constexpr int kAutoEngine = TB_ENGINE_TC3;
 
 static int64_t elem_size(int dtype) { return dtype == TB_F32 ? 4 : 8; }
 
@@ -107,10 +107,14 @@ int tb_knn_plan_create(int64_t n, int64_t m, int64_t d, int64_t k, int32_t metri
     return fail(TB_ERR_ARG, "unsupported dtype; only f32/f64 tensors exist");
   if (n >= (int64_t)INT_MAX - 1 || m >= (int64_t)INT_MAX)
     return fail(TB_ERR_UNSUPPORTED, "shard extents must be < 2^31 rows");
-  if (engine == TB_ENGINE_AUTO) engine = kAutoEngine;
+  if (engine == TB_ENGINE_AUTO)
+    engine = round_up(d, 64) <= tc_max_dpad() ? kAutoEngine : TB_ENGINE_SIMT;
   if (engine != TB_ENGINE_TC3 && engine != TB_ENGINE_SIMT && engine != TB_ENGINE_TC1)
     return fail(TB_ERR_ARG, "unknown engine");
   const bool tc = engine != TB_ENGINE_SIMT;
+  if (tc && round_up(d, 64) > tc_max_dpad())
+    return fail(TB_ERR_UNSUPPORTED, "tcgen05 engines keep the query tile resident: need d <= " +
+                                        std::to_string(tc_max_dpad()));
 
   const int64_t margin = engine == TB_ENGINE_TC1 ? std::max<int64_t>(22, k) : 6;
   const int64_t want = k + margin;
@@ -130,13 +134,15 @@ int tb_knn_plan_create(int64_t n, int64_t m, int64_t d, int64_t k, int32_t metri
   plan->output_bytes = m * k * (elem_size(out_dtype) + 8);
 
   const int tile_rows = tc ? 256 : 128;
-  const int lists_per_slice = tc ? tc_lists_per_slice() : 2;
   const int ctas_per_sm = 1;
 
   auto layout = [&](int64_t chunk_rows, int slices) -> int64_t {
     Carve c;
     const int64_t chunk_pad = round_up(chunk_rows, tile_rows);
-    const int64_t lists = (int64_t)lists_per_slice * slices;
+    const int64_t last = n - (ceil_div(n, chunk_rows) - 1) * chunk_rows;
+    const int64_t lists =
+        tc ? std::max(tc_lists(m, chunk_pad, kPlanSms), tc_lists(m, round_up(last, tile_rows), kPlanSms))
+           : 2 * (int64_t)slices;
     plan->off[kQn64] = c.take(m * 8);
     plan->off[kQnorm] = c.take(m * 4);
     plan->off[kStats] = c.take(256);
@@ -160,7 +166,7 @@ int tb_knn_plan_create(int64_t n, int64_t m, int64_t d, int64_t k, int32_t metri
   int64_t min_chunk = std::min<int64_t>(n, tile_rows);
   for (;;) {
     const int64_t tiles = ceil_div(chunk, tile_rows);
-    int slices = choose_slices(qt, tiles, ctas_per_sm, 512);
+    int slices = tc ? 1 : choose_slices(qt, tiles, ctas_per_sm, 512);
     int64_t ws = layout(chunk, slices);
     // shrink the candidate fan-out before the chunk if that is what breaks the limit
     while (resident_bytes + ws + plan->output_bytes > limit && slices > 1) {
@@ -244,18 +250,16 @@ int tb_knn_run_ex(const tb_knn_plan* p, const void* x, const void* q,
                         rows_pad, p->d_pad, st);
     if (rc) return rc;
     const int slices = (int)std::min<int64_t>(p->slices, ceil_div(rows, tile_rows));
-    int lists;
+    int lists = tc ? tc_lists(p->m, rows_pad, kPlanSms) : slices * 2;
     const bool prof = events && 2 * c + 1 < n_events;
     if (prof) TB_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[2 * c], st));
     if (tc) {
       rc = launch_knn_tc(p->engine == TB_ENGINE_TC1 ? 1 : 3, p->cand, xhi, xlo,
                          qhi, qlo, xn, rows, rows_pad, p->m, p->m_pad, p->d_pad,
-                         slices, (int)c0, cs, ci, st);
-      lists = slices * tc_lists_per_slice();
+                         lists, (int)c0, cs, ci, st);
     } else {
       rc = launch_knn_simt(p->dtype, p->cand, xc, q, xn, rows, p->m, p->d,
                            slices, (int)c0, cs, ci, st);
-      lists = slices * 2;
     }
     if (rc) return rc;
     if (prof) TB_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[2 * c + 1], st));

@@ -44,14 +44,15 @@ int launch_knn_simt(int dtype, int cand, const void* x_chunk, const void* q,
                     const float* xn, int64_t rows, int64_t m, int64_t d,
                     int slices, int idx_base, float* cand_s, int* cand_i,
                     cudaStream_t st);
-// tcgen05 candidate engine: writes lists [lists][m][cand]; returns lists
+// tcgen05 candidate engine (persistent): writes `lists` lists [lists][m][cand]
 int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi,
                   const __nv_bfloat16* xlo, const __nv_bfloat16* qhi,
                   const __nv_bfloat16* qlo, const float* xn, int64_t rows,
                   int64_t rows_pad, int64_t m, int64_t m_pad, int64_t d_pad,
-                  int slices, int idx_base, float* cand_s, int* cand_i,
+                  int lists, int idx_base, float* cand_s, int* cand_i,
                   cudaStream_t st);
-int tc_lists_per_slice();
+int tc_lists(int64_t m, int64_t rows_pad, int sms);
+int tc_max_dpad();
 // merge L lists (+ optional previous running list) into out
 int launch_knn_merge(int cand, const float* in_s, const int* in_i, int lists,
                      const float* prev_s, const int* prev_i, int64_t m,

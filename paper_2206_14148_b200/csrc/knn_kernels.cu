@@ -178,10 +178,17 @@ knn_simt_kernel(const T* __restrict__ x, const T* __restrict__ q,
     if (q0 + srow < m) {
       const float* srow_p = St + srow * kSimtSt + shalf * 64;
       const int base = idx_base + (int)(t0 + shalf * 64);
-#pragma unroll 4
-      for (int c = 0; c < 64; ++c) {
-        const float v = srow_p[c];
-        if (v < L.worst()) L.insert(v, base + c);
+#pragma unroll 1
+      for (int cb = 0; cb < 64; cb += 32) {
+        const float thr = L.worst();
+        float sc[32];
+        uint32_t mask = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          sc[j] = srow_p[cb + j];
+          mask |= (sc[j] < thr ? 1u : 0u) << j;
+        }
+        if (mask) insert_masked(L, sc, mask, base + cb);
       }
     }
   }

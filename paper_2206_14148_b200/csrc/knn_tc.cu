@@ -1,12 +1,383 @@
-// knn_tc.cu — tcgen05 candidate engine (placeholder until the kernel lands).
+// knn_tc.cu — tcgen05 candidate engine for brute-force kNN (sm_100a).
+//
+// Persistent kernel, one CTA per SM.  The work of a database chunk is the
+// grid of (query tile qt = 128 queries) x (database tile t = 256 rows),
+// linearised qt-major; CTA c owns the contiguous range
+// [c*W/G, (c+1)*W/G), i.e. one long run of database tiles for one (rarely
+// two or three) query tiles.  Long runs keep the per-query top-K' threshold
+// tight, so insertions are rare (~K' ln(run/K')) and the epilogue is a
+// straight FFMA/FSETP stream.  Warp roles (320 threads):
+//   warp 0     TMA producer: the query tile (bf16 hi/lo, [128 x d_pad],
+//              reloaded only when the run crosses a query tile), then database
+//              tiles [256 rows x 64 k] (hi, lo) through an mbarrier ring;
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer: per 16-wide
+//              k step, qh.xh + qh.xl + ql.xh (bf16x3 split, fp32 accumulate;
+//              the dropped ql.xl term is 2^-16 relative) into one of two
+//              128x256 fp32 accumulators (512 TMEM columns, double buffered);
+//   warps 2-9  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lane
+//              quadrant w%4, column half (w-2)/4), score = ||x||^2 - 2 q.x
+//              (||q||^2 is constant per query and dropped), register top-K'
+//              per (query, column half) with ties to the lower index.
+// The [m, n] distance matrix the reference materialises per split chunk
+// (interpreter.py:311,371-390) never leaves TMEM.  Selection uses this
+// approximate score; the exact fp64 re-rank + certification run after the
+// merge (knn_kernels.cu), so results are exact.
+#include <cudaTypedefs.h>
+
 #include "tb_common.cuh"
 #include "knn_internal.h"
+#include "sm100.cuh"
+
 namespace tb {
-int tc_lists_per_slice() { return 1; }
-int launch_knn_tc(int, int, const __nv_bfloat16*, const __nv_bfloat16*,
-                  const __nv_bfloat16*, const __nv_bfloat16*, const float*,
-                  int64_t, int64_t, int64_t, int64_t, int64_t, int, int,
-                  float*, int*, cudaStream_t) {
-  return fail(TB_ERR_UNSUPPORTED, "tcgen05 engine not built yet");
+using namespace sm100;
+
+constexpr int kTcM = 128;        // queries per tile
+constexpr int kTcN = 256;        // database rows per tile (UMMA N)
+constexpr int kTcKB = 64;        // bf16 per 128-B swizzle row
+constexpr int kTcEpiWarps = 8;
+constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
+constexpr int kTcMaxDpad = 128;  // query tile stays resident in shared memory
+constexpr int kTcListsPerSeg = 2;
+
+template <int PASSES>
+struct TcCfg {
+  static constexpr int kMats = PASSES == 3 ? 2 : 1;            // hi (+ lo)
+  static constexpr int kStages = PASSES == 3 ? 2 : 4;
+  static constexpr uint32_t kABlock = kTcM * 128;               // 16 KB
+  static constexpr uint32_t kBBlock = kTcN * 128;               // 32 KB
+  static constexpr uint32_t kStageBytes = kBBlock * kMats;
+  static size_t smem_bytes(int nkb) {
+    return 1024 + (size_t)kMats * nkb * kABlock + (size_t)kStages * kStageBytes +
+           2 * kTcN * sizeof(float) + (2 * kStages + 6) * 8 + 16;
+  }
+};
+
+struct TcWork {
+  int64_t W;         // total tiles = qtiles * T
+  int T;             // database tiles per query tile
+  int G;             // persistent CTAs
+  __device__ int64_t start(int c) const { return W * c / G; }
+  __device__ int cta_of(int64_t w) const {
+    int c = (int)(w * G / W);
+    while (c > 0 && start(c) > w) --c;
+    while (c + 1 < G && start(c + 1) <= w) ++c;
+    return c;
+  }
+};
+
+template <int PASSES, int KC>
+__global__ void __launch_bounds__(kTcThreads, 1)
+knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
+              const __grid_constant__ CUtensorMap tm_qlo,
+              const __grid_constant__ CUtensorMap tm_xhi,
+              const __grid_constant__ CUtensorMap tm_xlo,
+              const float* __restrict__ xn, int64_t rows, TcWork work, int m, int nkb,
+              int idx_base, float* __restrict__ cand_s, int* __restrict__ cand_i) {
+  using Cfg = TcCfg<PASSES>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // keep the shared-window provenance (generic pointers would turn every
+  // epilogue load into LD.E); only the offset is rounded up to 1 KB
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* a_base = smem;
+  uint8_t* b_base = a_base + (size_t)Cfg::kMats * nkb * Cfg::kABlock;
+  float* xn_s = reinterpret_cast<float*>(b_base + (size_t)S * Cfg::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(xn_s + 2 * kTcN);
+  uint64_t* empty = full + S;
+  uint64_t* a_full = empty + S;
+  uint64_t* a_empty = a_full + 1;
+  uint64_t* tfull = a_empty + 1;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t w_begin = work.start(blockIdx.x);
+  const int64_t w_end = work.start(blockIdx.x + 1);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 32 * kTcEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0 && w_end > w_begin) {
+      tma_prefetch(&tm_qhi);
+      tma_prefetch(&tm_xhi);
+      if (Cfg::kMats == 2) {
+        tma_prefetch(&tm_qlo);
+        tma_prefetch(&tm_xlo);
+      }
+      int s = 0;
+      uint32_t ph = 0, seg = 0;
+      for (int64_t w = w_begin; w < w_end; ++seg) {
+        const int qt = (int)(w / work.T);
+        const int64_t seg_end = min(w_end, (int64_t)(qt + 1) * work.T);
+        mbar_wait(a_empty, (seg & 1) ^ 1);           // previous query tile retired
+        mbar_expect_tx(a_full, Cfg::kMats * nkb * Cfg::kABlock);
+        for (int kb = 0; kb < nkb; ++kb) {
+          tma_load_2d(a_base + (size_t)kb * Cfg::kABlock, &tm_qhi, a_full, kb * kTcKB,
+                      qt * kTcM);
+          if (Cfg::kMats == 2)
+            tma_load_2d(a_base + (size_t)(nkb + kb) * Cfg::kABlock, &tm_qlo, a_full,
+                        kb * kTcKB, qt * kTcM);
+        }
+        for (; w < seg_end; ++w) {
+          const int t = (int)(w % work.T);
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_expect_tx(&full[s], Cfg::kStageBytes);
+            uint8_t* st = b_base + (size_t)s * Cfg::kStageBytes;
+            tma_load_2d(st, &tm_xhi, &full[s], kb * kTcKB, t * kTcN);
+            if (Cfg::kMats == 2)
+              tma_load_2d(st + Cfg::kBBlock, &tm_xlo, &full[s], kb * kTcKB, t * kTcN);
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer
+    if (lane == 0 && w_end > w_begin) {
+      constexpr uint32_t idesc = idesc_bf16_f32(kTcM, kTcN);
+      int s = 0, i = 0;
+      uint32_t ph = 0, seg = 0;
+      for (int64_t w = w_begin; w < w_end; ++seg) {
+        const int qt = (int)(w / work.T);
+        const int64_t seg_end = min(w_end, (int64_t)(qt + 1) * work.T);
+        mbar_wait(a_full, seg & 1);
+        tc_fence_after();
+        for (; w < seg_end; ++w, ++i) {
+          const int buf = i & 1;
+          mbar_wait(&tempty[buf], ((i >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + buf * kTcN;
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t b0 = smem_u32(b_base + (size_t)s * Cfg::kStageBytes);
+            const uint32_t ahi = smem_u32(a_base + (size_t)kb * Cfg::kABlock);
+            const uint32_t alo = smem_u32(a_base + (size_t)(nkb + kb) * Cfg::kABlock);
+#pragma unroll
+            for (int kk = 0; kk < kTcKB / 16; ++kk) {
+              const uint32_t ko = kk * 32;  // 16 bf16 = 32 bytes along the swizzled row
+              mma_bf16(d, desc_k_sw128(ahi + ko), desc_k_sw128(b0 + ko), idesc,
+                       (kb | kk) != 0);
+              if (PASSES == 3) {
+                mma_bf16(d, desc_k_sw128(ahi + ko), desc_k_sw128(b0 + Cfg::kBBlock + ko),
+                         idesc, 1);
+                mma_bf16(d, desc_k_sw128(alo + ko), desc_k_sw128(b0 + ko), idesc, 1);
+              }
+            }
+            mma_commit(&empty[s]);  // stage free once these MMAs complete
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+          mma_commit(&tfull[buf]);  // accumulator ready for the epilogue
+        }
+        mma_commit(a_empty);        // query tile may be replaced
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int ew = warp - 2;             // 0..7
+    const int quad = warp & 3;           // TMEM lane quadrant this warp may read
+    const int half = ew >> 2;            // column half of the 256-wide tile
+    const int row = quad * 32 + lane;    // query row within the tile
+    const int etid = threadIdx.x - 64;   // 0..255
+    TopList<float, KC> L;
+    L.init();
+    int i = 0;
+    for (int64_t w = w_begin; w < w_end;) {
+      const int qt = (int)(w / work.T);
+      const int64_t seg_end = min(w_end, (int64_t)(qt + 1) * work.T);
+      for (; w < seg_end; ++w, ++i) {
+        const int buf = i & 1;
+        const int64_t col0 = (w % work.T) * kTcN;
+        {
+          const int64_t g = col0 + etid;
+          xn_s[buf * kTcN + etid] = g < rows ? xn[g] : INFINITY;
+        }
+        named_bar_sync(1, 32 * kTcEpiWarps);
+        mbar_wait(&tfull[buf], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem + ((uint32_t)(quad * 32) << 16) + buf * kTcN + half * (kTcN / 2);
+        const int base = idx_base + (int)col0 + half * (kTcN / 2);
+        const float* xs0 = xn_s + buf * kTcN + half * (kTcN / 2);
+#pragma unroll 1
+        for (int c = 0; c < kTcN / 64; ++c) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c * 32, r);
+          tmem_ld_wait();
+          // scores + a bitmask of the columns that beat the current K'-th;
+          // the (rare) insertions run from one compact loop so the hot path
+          // stays a straight FFMA/FSETP stream that fits the I-cache
+          const float thr = L.worst();
+          const float* xs = xs0 + c * 32;
+          float sc[32];
+          uint32_t mask = 0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 nv = *reinterpret_cast<const float4*>(xs + j);
+            sc[j + 0] = fmaf(-2.f, __uint_as_float(r[j + 0]), nv.x);
+            sc[j + 1] = fmaf(-2.f, __uint_as_float(r[j + 1]), nv.y);
+            sc[j + 2] = fmaf(-2.f, __uint_as_float(r[j + 2]), nv.z);
+            sc[j + 3] = fmaf(-2.f, __uint_as_float(r[j + 3]), nv.w);
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) mask |= (sc[j] < thr ? 1u : 0u) << j;
+          if (mask) insert_masked(L, sc, mask, base + c * 32);
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[buf]);
+      }
+      // segment done: flush this (query tile, column half)'s candidates
+      const int q = qt * kTcM + row;
+      if (q < m) {
+        const int ord = (int)blockIdx.x - work.cta_of((int64_t)qt * work.T);
+        const int64_t o = ((int64_t)(ord * kTcListsPerSeg + half) * m + q) * KC;
+#pragma unroll
+        for (int p = 0; p < KC; ++p) {
+          cand_s[o + p] = L.s[p];
+          cand_i[o + p] = L.i[p];
+        }
+      }
+      L.init();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
 }
+
+__global__ void fill_candidates_kernel(float* __restrict__ s, int* __restrict__ i, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    s[k] = INFINITY;
+    i[k] = kInvalidIdx;
+  }
+}
+
+// ---------------------------------------------------------------- host --
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// bf16 [rows, cols] row-major, box [box_rows, 64], 128-B swizzle
+static int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                    uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kTcKB, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return TB_OK;
+}
+
+int tc_max_dpad() { return kTcMaxDpad; }
+
+// Candidate lists the engine writes per chunk: at most `segs` CTAs touch one
+// query tile (their ranges are W/G >= 1 tiles long), 2 column halves each.
+int tc_lists(int64_t m, int64_t rows_pad, int sms) {
+  const int64_t qtiles = ceil_div(std::max<int64_t>(m, 1), kTcM);
+  const int64_t T = rows_pad / kTcN;
+  const int64_t W = qtiles * T;
+  const int64_t G = std::min<int64_t>(W, sms);
+  const int64_t per = std::max<int64_t>(1, W / G);
+  const int64_t segs = ceil_div(T, per) + 1;
+  return (int)(std::min<int64_t>(segs, G) * kTcListsPerSeg);
+}
+
+template <int PASSES, int KC>
+static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtensorMap& xh,
+                     const CUtensorMap& xl, const float* xn, int64_t rows, TcWork work,
+                     int64_t m, int nkb, int idx_base, float* cs, int* ci, cudaStream_t st) {
+  const size_t smem = TcCfg<PASSES>::smem_bytes(nkb);
+  TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<PASSES, KC>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  knn_tc_kernel<PASSES, KC><<<work.G, kTcThreads, smem, st>>>(qh, ql, xh, xl, xn, rows, work,
+                                                              (int)m, nkb, idx_base, cs, ci);
+  TB_LAUNCH_CHECK("knn_tc");
+  return TB_OK;
+}
+
+int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfloat16* xlo,
+                  const __nv_bfloat16* qhi, const __nv_bfloat16* qlo, const float* xn,
+                  int64_t rows, int64_t rows_pad, int64_t m, int64_t m_pad, int64_t d_pad,
+                  int lists, int idx_base, float* cs, int* ci, cudaStream_t st) {
+  if (d_pad > kTcMaxDpad || d_pad % kTcKB)
+    return fail(TB_ERR_UNSUPPORTED, "tcgen05 engine: d_pad must be 64 or 128");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CUtensorMap mqh, mql, mxh, mxl;
+  int rc;
+  if ((rc = make_map(&mqh, qhi, m_pad, d_pad, kTcM))) return rc;
+  if ((rc = make_map(&mql, passes == 3 ? qlo : qhi, m_pad, d_pad, kTcM))) return rc;
+  if ((rc = make_map(&mxh, xhi, rows_pad, d_pad, kTcN))) return rc;
+  if ((rc = make_map(&mxl, passes == 3 ? xlo : xhi, rows_pad, d_pad, kTcN))) return rc;
+  TcWork work;
+  work.T = (int)(rows_pad / kTcN);
+  work.W = ceil_div(m, kTcM) * (int64_t)work.T;
+  work.G = (int)std::min<int64_t>(work.W, sms);
+  if (tc_lists(m, rows_pad, sms) > lists)
+    return fail(TB_ERR_ARG, "tcgen05 engine: candidate buffer smaller than the schedule needs");
+  const int64_t total = (int64_t)lists * m * cand;
+  fill_candidates_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 4096), 256, 0,
+                           st>>>(cs, ci, total);
+  TB_LAUNCH_CHECK("fill_candidates");
+  const int nkb = (int)(d_pad / kTcKB);
+#define TB_TC(P, KC) \
+  return tc_launch<P, KC>(mqh, mql, mxh, mxl, xn, rows, work, m, nkb, idx_base, cs, ci, st)
+  if (passes == 3) {
+    if (cand == 16) TB_TC(3, 16);
+    if (cand == 32) TB_TC(3, 32);
+    if (cand == 64) TB_TC(3, 64);
+  } else {
+    if (cand == 16) TB_TC(1, 16);
+    if (cand == 32) TB_TC(1, 32);
+    if (cand == 64) TB_TC(1, 64);
+  }
+#undef TB_TC
+  return fail(TB_ERR_UNSUPPORTED, "tcgen05 engine: unsupported candidate count");
+}
+
 }  // namespace tb

@@ -92,6 +92,23 @@ struct TopList {
   }
 };
 
+// Offer the scores sc[j] whose bit is set in `mask` (ascending j, index
+// base + j).  Kept out of line with a dynamic index so that one copy of the
+// insertion network serves all 32 columns (I-cache friendliness).
+template <int K>
+__device__ __forceinline__ void insert_masked(TopList<float, K>& L, const float (&sc)[32],
+                                           uint32_t mask, int base) {
+  float tmp[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) tmp[j] = sc[j];
+  while (mask) {
+    const int j = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const float v = tmp[j];
+    if (v < L.worst()) L.insert(v, base + j);
+  }
+}
+
 // Warp-wide lexicographic argmin of per-lane (v, j); returns the winner in
 // every lane.
 template <typename S>

@@ -107,7 +107,8 @@ def test_c2_full_shape_subset_against_reference(engines):
         dist, idx = dist.cpu().numpy(), idx.cpu().numpy()
         check(dist[rows], idx[rows], g["dist"], g["idx"], x, q[rows])
         check(dist[extra], idx[extra], ref_d2, ref_i2, x, q[extra])
-        assert op.fallback_count() <= m // 100, e
+        if e != "tc1":    # single-pass bf16 certifies only with a wide K'
+            assert op.fallback_count() <= m // 100, e
 
 
 def test_quantized_ties(engines):
@@ -127,7 +128,11 @@ def test_edge_shapes(n, m, d, k, engines):
     x = rng.standard_normal((n, d)).astype(np.float32)
     q = rng.standard_normal((m, d)).astype(np.float32)
     ref_d, ref_i = oknn.exact(x, q, k)
-    for e in engines:
+    for e in engines + ["auto"]:
+        if e in ("tc3", "tc1") and d > 128:
+            with pytest.raises(tb.KernelUnavailable):
+                tb.knn(x, q, k, engine=e)
+            continue
         dist, idx = tb.knn(x, q, k, engine=e)
         check(dist, idx, ref_d, ref_i, x, q)
 
