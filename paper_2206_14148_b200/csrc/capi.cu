@@ -152,6 +152,7 @@ int tb_knn_plan_create(int64_t n, int64_t m, int64_t d, int64_t k, int32_t metri
     plan->off[kCandI] = c.take(lists * m * cand * 4);
     plan->off[kRunS] = c.take(2 * m * cand * 4);
     plan->off[kRunI] = c.take(2 * m * cand * 4);
+    plan->off[kGThr] = c.take(m * 4);
     if (tc) {
       plan->off[kQHi] = c.take(plan->m_pad * plan->d_pad * 2);
       plan->off[kQLo] = c.take(plan->m_pad * plan->d_pad * 2);
@@ -232,8 +233,10 @@ int tb_knn_run_ex(const tb_knn_plan* p, const void* x, const void* q,
   __nv_bfloat16* xlo = tc ? (__nv_bfloat16*)at(kXLo) : nullptr;
   const int64_t es = elem_size(p->dtype);
   const int tile_rows = tc ? 256 : 128;
+  unsigned* gthr = (unsigned*)at(kGThr);
 
   TB_CUDA_TRY(cudaMemsetAsync(stats, 0, 256, st));
+  if (tc) TB_CUDA_TRY(cudaMemsetAsync(gthr, 0xFF, p->m * 4, st));
   int rc = launch_query_prep(p->dtype, q, p->m, p->d, qn64, qnorm, qhi, qlo,
                              p->m_pad, p->d_pad, st);
   if (rc) return rc;
@@ -256,7 +259,7 @@ int tb_knn_run_ex(const tb_knn_plan* p, const void* x, const void* q,
     if (tc) {
       rc = launch_knn_tc(p->engine == TB_ENGINE_TC1 ? 1 : 3, p->cand, xhi, xlo,
                          qhi, qlo, xn, rows, rows_pad, p->m, p->m_pad, p->d_pad,
-                         lists, (int)c0, cs, ci, st);
+                         lists, (int)c0, cs, ci, gthr, st);
     } else {
       rc = launch_knn_simt(p->dtype, p->cand, xc, q, xn, rows, p->m, p->d,
                            slices, (int)c0, cs, ci, st);

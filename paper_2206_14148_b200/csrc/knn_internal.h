@@ -21,7 +21,8 @@ enum KnnSlot {
   kQLo = 10,
   kXHi = 11,    // bf16[chunk_pad][d_pad]
   kXLo = 12,
-  kNumSlots = 13
+  kGThr = 13,   // u32[m]           per-query shared K'-th score bound (ordered key)
+  kNumSlots = 14
 };
 
 struct KnnDims {
@@ -44,13 +45,14 @@ int launch_knn_simt(int dtype, int cand, const void* x_chunk, const void* q,
                     const float* xn, int64_t rows, int64_t m, int64_t d,
                     int slices, int idx_base, float* cand_s, int* cand_i,
                     cudaStream_t st);
-// tcgen05 candidate engine (persistent): writes `lists` lists [lists][m][cand]
+// tcgen05 candidate engine (persistent): writes tc_lists(...) lists
+// [lists][m][cand]; gthr[m] is the shared per-query threshold (ordered keys)
 int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi,
                   const __nv_bfloat16* xlo, const __nv_bfloat16* qhi,
                   const __nv_bfloat16* qlo, const float* xn, int64_t rows,
                   int64_t rows_pad, int64_t m, int64_t m_pad, int64_t d_pad,
                   int lists, int idx_base, float* cand_s, int* cand_i,
-                  cudaStream_t st);
+                  unsigned* gthr, cudaStream_t st);
 int tc_lists(int64_t m, int64_t rows_pad, int sms);
 int tc_max_dpad();
 // merge L lists (+ optional previous running list) into out

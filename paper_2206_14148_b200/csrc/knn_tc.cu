@@ -37,32 +37,34 @@ constexpr int kTcKB = 64;        // bf16 per 128-B swizzle row
 constexpr int kTcEpiWarps = 8;
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
 constexpr int kTcMaxDpad = 128;  // query tile stays resident in shared memory
-constexpr int kTcListsPerSeg = 2;
+constexpr int kTcStages = 4;     // 32 KB database k-blocks in flight
 
 template <int PASSES>
 struct TcCfg {
   static constexpr int kMats = PASSES == 3 ? 2 : 1;            // hi (+ lo)
-  static constexpr int kStages = PASSES == 3 ? 2 : 4;
   static constexpr uint32_t kABlock = kTcM * 128;               // 16 KB
   static constexpr uint32_t kBBlock = kTcN * 128;               // 32 KB
-  static constexpr uint32_t kStageBytes = kBBlock * kMats;
   static size_t smem_bytes(int nkb) {
-    return 1024 + (size_t)kMats * nkb * kABlock + (size_t)kStages * kStageBytes +
-           2 * kTcN * sizeof(float) + (2 * kStages + 6) * 8 + 16;
+    return 1024 + (size_t)kMats * nkb * kABlock + (size_t)kTcStages * kBBlock +
+           2 * kTcN * sizeof(float) + (2 * kTcStages + 6) * 8 + 16;
   }
 };
 
+// order-preserving float <-> u32 keys for the shared per-query threshold
+__device__ __forceinline__ uint32_t fkey(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+  if (k >= 0xFF800000u) return INFINITY;   // unset (0xFFFFFFFF) or +inf
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+// Work of one database chunk: units (query tile qt, database slice) ordered
+// slice-major, handed to the persistent CTAs round-robin, so that at any
+// time the CTAs sweep ~G/qtiles adjacent slices and share them through L2.
 struct TcWork {
-  int64_t W;         // total tiles = qtiles * T
-  int T;             // database tiles per query tile
-  int G;             // persistent CTAs
-  __device__ int64_t start(int c) const { return W * c / G; }
-  __device__ int cta_of(int64_t w) const {
-    int c = (int)(w * G / W);
-    while (c > 0 && start(c) > w) --c;
-    while (c + 1 < G && start(c + 1) <= w) ++c;
-    return c;
-  }
+  int qtiles, T, slices, tps;   // tps = database tiles per slice
 };
 
 template <int PASSES, int KC>
@@ -72,16 +74,17 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               const __grid_constant__ CUtensorMap tm_xhi,
               const __grid_constant__ CUtensorMap tm_xlo,
               const float* __restrict__ xn, int64_t rows, TcWork work, int m, int nkb,
-              int idx_base, float* __restrict__ cand_s, int* __restrict__ cand_i) {
+              int idx_base, float* __restrict__ cand_s, int* __restrict__ cand_i,
+              unsigned* __restrict__ gthr) {
   using Cfg = TcCfg<PASSES>;
-  constexpr int S = Cfg::kStages;
+  constexpr int S = kTcStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // keep the shared-window provenance (generic pointers would turn every
   // epilogue load into LD.E); only the offset is rounded up to 1 KB
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_base = smem;
   uint8_t* b_base = a_base + (size_t)Cfg::kMats * nkb * Cfg::kABlock;
-  float* xn_s = reinterpret_cast<float*>(b_base + (size_t)S * Cfg::kStageBytes);
+  float* xn_s = reinterpret_cast<float*>(b_base + (size_t)S * Cfg::kBBlock);
   uint64_t* full = reinterpret_cast<uint64_t*>(xn_s + 2 * kTcN);
   uint64_t* empty = full + S;
   uint64_t* a_full = empty + S;
@@ -91,8 +94,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w_begin = work.start(blockIdx.x);
-  const int64_t w_end = work.start(blockIdx.x + 1);
+  const int units = work.qtiles * work.slices;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -115,7 +117,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
-    if (lane == 0 && w_end > w_begin) {
+    if (lane == 0) {
       tma_prefetch(&tm_qhi);
       tma_prefetch(&tm_xhi);
       if (Cfg::kMats == 2) {
@@ -124,9 +126,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       }
       int s = 0;
       uint32_t ph = 0, seg = 0;
-      for (int64_t w = w_begin; w < w_end; ++seg) {
-        const int qt = (int)(w / work.T);
-        const int64_t seg_end = min(w_end, (int64_t)(qt + 1) * work.T);
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++seg) {
+        const int slice = u / work.qtiles, qt = u - slice * work.qtiles;
+        const int t0 = slice * work.tps, t1 = min(work.T, t0 + work.tps);
         mbar_wait(a_empty, (seg & 1) ^ 1);           // previous query tile retired
         mbar_expect_tx(a_full, Cfg::kMats * nkb * Cfg::kABlock);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -136,18 +138,18 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             tma_load_2d(a_base + (size_t)(nkb + kb) * Cfg::kABlock, &tm_qlo, a_full,
                         kb * kTcKB, qt * kTcM);
         }
-        for (; w < seg_end; ++w) {
-          const int t = (int)(w % work.T);
+        for (int t = t0; t < t1; ++t) {
           for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(&empty[s], ph ^ 1);
-            mbar_expect_tx(&full[s], Cfg::kStageBytes);
-            uint8_t* st = b_base + (size_t)s * Cfg::kStageBytes;
-            tma_load_2d(st, &tm_xhi, &full[s], kb * kTcKB, t * kTcN);
-            if (Cfg::kMats == 2)
-              tma_load_2d(st + Cfg::kBBlock, &tm_xlo, &full[s], kb * kTcKB, t * kTcN);
-            if (++s == S) {
-              s = 0;
-              ph ^= 1;
+#pragma unroll
+            for (int mat = 0; mat < Cfg::kMats; ++mat) {
+              mbar_wait(&empty[s], ph ^ 1);
+              mbar_expect_tx(&full[s], Cfg::kBBlock);
+              tma_load_2d(b_base + (size_t)s * Cfg::kBBlock, mat ? &tm_xlo : &tm_xhi,
+                          &full[s], kb * kTcKB, t * kTcN);
+              if (++s == S) {
+                s = 0;
+                ph ^= 1;
+              }
             }
           }
         }
@@ -155,41 +157,53 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
-    if (lane == 0 && w_end > w_begin) {
+    if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(kTcM, kTcN);
       int s = 0, i = 0;
       uint32_t ph = 0, seg = 0;
-      for (int64_t w = w_begin; w < w_end; ++seg) {
-        const int qt = (int)(w / work.T);
-        const int64_t seg_end = min(w_end, (int64_t)(qt + 1) * work.T);
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++seg) {
+        const int slice = u / work.qtiles;
+        const int t0 = slice * work.tps, t1 = min(work.T, t0 + work.tps);
         mbar_wait(a_full, seg & 1);
         tc_fence_after();
-        for (; w < seg_end; ++w, ++i) {
+        for (int t = t0; t < t1; ++t, ++i) {
           const int buf = i & 1;
           mbar_wait(&tempty[buf], ((i >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + buf * kTcN;
           for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(&full[s], ph);
-            tc_fence_after();
-            const uint32_t b0 = smem_u32(b_base + (size_t)s * Cfg::kStageBytes);
             const uint32_t ahi = smem_u32(a_base + (size_t)kb * Cfg::kABlock);
             const uint32_t alo = smem_u32(a_base + (size_t)(nkb + kb) * Cfg::kABlock);
+            // stage x_hi: q_hi.x_hi (+ q_lo.x_hi)
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            uint32_t b0 = smem_u32(b_base + (size_t)s * Cfg::kBBlock);
 #pragma unroll
             for (int kk = 0; kk < kTcKB / 16; ++kk) {
               const uint32_t ko = kk * 32;  // 16 bf16 = 32 bytes along the swizzled row
               mma_bf16(d, desc_k_sw128(ahi + ko), desc_k_sw128(b0 + ko), idesc,
                        (kb | kk) != 0);
-              if (PASSES == 3) {
-                mma_bf16(d, desc_k_sw128(ahi + ko), desc_k_sw128(b0 + Cfg::kBBlock + ko),
-                         idesc, 1);
+              if (PASSES == 3)
                 mma_bf16(d, desc_k_sw128(alo + ko), desc_k_sw128(b0 + ko), idesc, 1);
-              }
             }
-            mma_commit(&empty[s]);  // stage free once these MMAs complete
+            mma_commit(&empty[s]);
             if (++s == S) {
               s = 0;
               ph ^= 1;
+            }
+            if (PASSES == 3) {
+              // stage x_lo: q_hi.x_lo
+              mbar_wait(&full[s], ph);
+              tc_fence_after();
+              b0 = smem_u32(b_base + (size_t)s * Cfg::kBBlock);
+#pragma unroll
+              for (int kk = 0; kk < kTcKB / 16; ++kk)
+                mma_bf16(d, desc_k_sw128(ahi + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, 1);
+              mma_commit(&empty[s]);
+              if (++s == S) {
+                s = 0;
+                ph ^= 1;
+              }
             }
           }
           mma_commit(&tfull[buf]);  // accumulator ready for the epilogue
@@ -205,18 +219,23 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     const int row = quad * 32 + lane;    // query row within the tile
     const int etid = threadIdx.x - 64;   // 0..255
     TopList<float, KC> L;
-    L.init();
     int i = 0;
-    for (int64_t w = w_begin; w < w_end;) {
-      const int qt = (int)(w / work.T);
-      const int64_t seg_end = min(w_end, (int64_t)(qt + 1) * work.T);
-      for (; w < seg_end; ++w, ++i) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int slice = u / work.qtiles, qt = u - slice * work.qtiles;
+      const int t0 = slice * work.tps, t1 = min(work.T, t0 + work.tps);
+      const int q = qt * kTcM + row;
+      L.init();
+      for (int t = t0; t < t1; ++t, ++i) {
         const int buf = i & 1;
-        const int64_t col0 = (w % work.T) * kTcN;
+        const int64_t col0 = (int64_t)t * kTcN;
         {
           const int64_t g = col0 + etid;
           xn_s[buf * kTcN + etid] = g < rows ? xn[g] : INFINITY;
         }
+        // candidates must also beat the best K'-th score any finished unit
+        // has published for this query (a valid bound for the union)
+        const float thr_g = q < m ? fkey_inv(*reinterpret_cast<volatile unsigned*>(gthr + q))
+                                  : -INFINITY;
         named_bar_sync(1, 32 * kTcEpiWarps);
         mbar_wait(&tfull[buf], (i >> 1) & 1);
         tc_fence_after();
@@ -229,10 +248,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           uint32_t r[32];
           tmem_ld32(taddr + c * 32, r);
           tmem_ld_wait();
-          // scores + a bitmask of the columns that beat the current K'-th;
-          // the (rare) insertions run from one compact loop so the hot path
-          // stays a straight FFMA/FSETP stream that fits the I-cache
-          const float thr = L.worst();
+          // scores + a bitmask of the columns that beat the threshold; the
+          // (rare) insertions run from one compact loop so the hot path stays
+          // a straight FFMA/FSETP stream that fits the I-cache
+          const float thr = fminf(L.worst(), thr_g);
           const float* xs = xs0 + c * 32;
           float sc[32];
           uint32_t mask = 0;
@@ -246,37 +265,27 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           }
 #pragma unroll
           for (int j = 0; j < 32; ++j) mask |= (sc[j] < thr ? 1u : 0u) << j;
-          if (mask) insert_masked(L, sc, mask, base + c * 32);
+          if (mask) insert_masked(L, sc, mask, base + c * 32, thr_g);
         }
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
       }
-      // segment done: flush this (query tile, column half)'s candidates
-      const int q = qt * kTcM + row;
+      // unit done: publish this (slice, column half)'s candidates
       if (q < m) {
-        const int ord = (int)blockIdx.x - work.cta_of((int64_t)qt * work.T);
-        const int64_t o = ((int64_t)(ord * kTcListsPerSeg + half) * m + q) * KC;
+        const int64_t o = ((int64_t)(slice * 2 + half) * m + q) * KC;
 #pragma unroll
         for (int p = 0; p < KC; ++p) {
           cand_s[o + p] = L.s[p];
           cand_i[o + p] = L.i[p];
         }
+        if (L.worst() < INFINITY) atomicMin(gthr + q, fkey(L.worst()));
       }
-      L.init();
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, 512);
-}
-
-__global__ void fill_candidates_kernel(float* __restrict__ s, int* __restrict__ i, int64_t n) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    s[k] = INFINITY;
-    i[k] = kInvalidIdx;
-  }
 }
 
 // ---------------------------------------------------------------- host --
@@ -314,27 +323,44 @@ static int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 
 int tc_max_dpad() { return kTcMaxDpad; }
 
-// Candidate lists the engine writes per chunk: at most `segs` CTAs touch one
-// query tile (their ranges are W/G >= 1 tiles long), 2 column halves each.
+// Slices per query tile for a chunk of T database tiles: minimise
+// waves x (tiles per slice + ~2 tiles of per-unit overhead).
+static void tc_schedule(int64_t m, int64_t rows_pad, int sms, TcWork* w) {
+  w->qtiles = (int)ceil_div(std::max<int64_t>(m, 1), kTcM);
+  w->T = (int)(rows_pad / kTcN);
+  int best_k = 1;
+  int64_t best = INT64_MAX;
+  for (int k = 1; k <= w->T && k <= 256; ++k) {
+    const int64_t tps = ceil_div(w->T, k);
+    const int64_t keff = ceil_div(w->T, tps);
+    const int64_t units = (int64_t)w->qtiles * keff;
+    const int64_t g = std::min<int64_t>(units, sms);
+    const int64_t cost = ceil_div(units, g) * (tps + 2);
+    if (cost < best) {
+      best = cost;
+      best_k = (int)keff;
+    }
+  }
+  w->tps = (int)ceil_div(w->T, best_k);
+  w->slices = (int)ceil_div(w->T, w->tps);
+}
+
 int tc_lists(int64_t m, int64_t rows_pad, int sms) {
-  const int64_t qtiles = ceil_div(std::max<int64_t>(m, 1), kTcM);
-  const int64_t T = rows_pad / kTcN;
-  const int64_t W = qtiles * T;
-  const int64_t G = std::min<int64_t>(W, sms);
-  const int64_t per = std::max<int64_t>(1, W / G);
-  const int64_t segs = ceil_div(T, per) + 1;
-  return (int)(std::min<int64_t>(segs, G) * kTcListsPerSeg);
+  TcWork w;
+  tc_schedule(m, rows_pad, sms, &w);
+  return 2 * w.slices;
 }
 
 template <int PASSES, int KC>
 static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtensorMap& xh,
                      const CUtensorMap& xl, const float* xn, int64_t rows, TcWork work,
-                     int64_t m, int nkb, int idx_base, float* cs, int* ci, cudaStream_t st) {
+                     int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
+                     unsigned* gthr, cudaStream_t st) {
   const size_t smem = TcCfg<PASSES>::smem_bytes(nkb);
   TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<PASSES, KC>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  knn_tc_kernel<PASSES, KC><<<work.G, kTcThreads, smem, st>>>(qh, ql, xh, xl, xn, rows, work,
-                                                              (int)m, nkb, idx_base, cs, ci);
+  knn_tc_kernel<PASSES, KC><<<grid, kTcThreads, smem, st>>>(qh, ql, xh, xl, xn, rows, work,
+                                                            (int)m, nkb, idx_base, cs, ci, gthr);
   TB_LAUNCH_CHECK("knn_tc");
   return TB_OK;
 }
@@ -342,7 +368,8 @@ static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtenso
 int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfloat16* xlo,
                   const __nv_bfloat16* qhi, const __nv_bfloat16* qlo, const float* xn,
                   int64_t rows, int64_t rows_pad, int64_t m, int64_t m_pad, int64_t d_pad,
-                  int lists, int idx_base, float* cs, int* ci, cudaStream_t st) {
+                  int lists, int idx_base, float* cs, int* ci, unsigned* gthr,
+                  cudaStream_t st) {
   if (d_pad > kTcMaxDpad || d_pad % kTcKB)
     return fail(TB_ERR_UNSUPPORTED, "tcgen05 engine: d_pad must be 64 or 128");
   int dev = 0, sms = 148;
@@ -355,18 +382,15 @@ int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfl
   if ((rc = make_map(&mxh, xhi, rows_pad, d_pad, kTcN))) return rc;
   if ((rc = make_map(&mxl, passes == 3 ? xlo : xhi, rows_pad, d_pad, kTcN))) return rc;
   TcWork work;
-  work.T = (int)(rows_pad / kTcN);
-  work.W = ceil_div(m, kTcM) * (int64_t)work.T;
-  work.G = (int)std::min<int64_t>(work.W, sms);
-  if (tc_lists(m, rows_pad, sms) > lists)
+  tc_schedule(m, rows_pad, 148, &work);   // the plan's schedule (planner assumes 148 SMs)
+  if (2 * work.slices > lists)
     return fail(TB_ERR_ARG, "tcgen05 engine: candidate buffer smaller than the schedule needs");
-  const int64_t total = (int64_t)lists * m * cand;
-  fill_candidates_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 4096), 256, 0,
-                           st>>>(cs, ci, total);
-  TB_LAUNCH_CHECK("fill_candidates");
+  const int units = work.qtiles * work.slices;
+  const int grid = std::min(units, sms);
   const int nkb = (int)(d_pad / kTcKB);
-#define TB_TC(P, KC) \
-  return tc_launch<P, KC>(mqh, mql, mxh, mxl, xn, rows, work, m, nkb, idx_base, cs, ci, st)
+#define TB_TC(P, KC)                                                                      \
+  return tc_launch<P, KC>(mqh, mql, mxh, mxl, xn, rows, work, grid, m, nkb, idx_base, cs, \
+                          ci, gthr, st)
   if (passes == 3) {
     if (cand == 16) TB_TC(3, 16);
     if (cand == 32) TB_TC(3, 32);

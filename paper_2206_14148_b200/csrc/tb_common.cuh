@@ -97,7 +97,7 @@ struct TopList {
 // insertion network serves all 32 columns (I-cache friendliness).
 template <int K>
 __device__ __forceinline__ void insert_masked(TopList<float, K>& L, const float (&sc)[32],
-                                           uint32_t mask, int base) {
+                                           uint32_t mask, int base, float cap = INFINITY) {
   float tmp[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) tmp[j] = sc[j];
@@ -105,7 +105,7 @@ __device__ __forceinline__ void insert_masked(TopList<float, K>& L, const float 
     const int j = __ffs(mask) - 1;
     mask &= mask - 1;
     const float v = tmp[j];
-    if (v < L.worst()) L.insert(v, base + j);
+    if (v < L.worst() && v < cap) L.insert(v, base + j);
   }
 }
 
