@@ -46,7 +46,7 @@ struct TcCfg {
   static constexpr uint32_t kBBlock = kTcN * 128;               // 32 KB
   static size_t smem_bytes(int nkb) {
     return 1024 + (size_t)kMats * nkb * kABlock + (size_t)kTcStages * kBBlock +
-           2 * kTcN * sizeof(float) + (2 * kTcStages + 6) * 8 + 16;
+           kTcEpiWarps * kTcN * sizeof(float) + (2 * kTcStages + 6) * 8 + 16;
   }
 };
 
@@ -84,8 +84,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_base = smem;
   uint8_t* b_base = a_base + (size_t)Cfg::kMats * nkb * Cfg::kABlock;
-  float* xn_s = reinterpret_cast<float*>(b_base + (size_t)S * Cfg::kBBlock);
-  uint64_t* full = reinterpret_cast<uint64_t*>(xn_s + 2 * kTcN);
+  float* xn_w = reinterpret_cast<float*>(b_base + (size_t)S * Cfg::kBBlock);
+  uint64_t* full = reinterpret_cast<uint64_t*>(xn_w + kTcEpiWarps * kTcN);
   uint64_t* empty = full + S;
   uint64_t* a_full = empty + S;
   uint64_t* a_empty = a_full + 1;
@@ -217,68 +217,111 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     const int quad = warp & 3;           // TMEM lane quadrant this warp may read
     const int half = ew >> 2;            // column half of the 256-wide tile
     const int row = quad * 32 + lane;    // query row within the tile
-    const int etid = threadIdx.x - 64;   // 0..255
+    float* xw0 = xn_w + ew * 2 * (kTcN / 2);   // this warp's ||x||^2 double buffer
+    // ||x||^2 of the 4 columns this lane stages for tile t (per-warp copy:
+    // no cross-warp barrier on the critical path)
+    auto load_xn4 = [&](int t) {
+      const int64_t g = (int64_t)t * kTcN + half * (kTcN / 2) + 4 * lane;
+      float4 v;
+      if (g + 3 < rows) {
+        v = __ldg(reinterpret_cast<const float4*>(xn + g));
+      } else {
+        v.x = g + 0 < rows ? xn[g + 0] : INFINITY;
+        v.y = g + 1 < rows ? xn[g + 1] : INFINITY;
+        v.z = g + 2 < rows ? xn[g + 2] : INFINITY;
+        v.w = g + 3 < rows ? xn[g + 3] : INFINITY;
+      }
+      return v;
+    };
+    auto load_g = [&](int qq) -> unsigned {
+      return qq < m ? *reinterpret_cast<volatile unsigned*>(gthr + qq) : 0u;
+    };
     TopList<float, KC> L;
-    int i = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int slice = u / work.qtiles, qt = u - slice * work.qtiles;
-      const int t0 = slice * work.tps, t1 = min(work.T, t0 + work.tps);
-      const int q = qt * kTcM + row;
-      L.init();
-      for (int t = t0; t < t1; ++t, ++i) {
+    L.init();
+    int u = blockIdx.x;
+    if (u < units) {
+      int slice = u / work.qtiles, qt = u - slice * work.qtiles;
+      int t1 = min(work.T, slice * work.tps + work.tps);
+      int t = slice * work.tps;
+      int q = qt * kTcM + row;
+      float4 xv = load_xn4(t);
+      unsigned gk = load_g(q);
+      for (int i = 0;; ++i) {
         const int buf = i & 1;
-        const int64_t col0 = (int64_t)t * kTcN;
-        {
-          const int64_t g = col0 + etid;
-          xn_s[buf * kTcN + etid] = g < rows ? xn[g] : INFINITY;
-        }
+        float* xw = xw0 + buf * (kTcN / 2);
+        *reinterpret_cast<float4*>(xw + 4 * lane) = xv;
         // candidates must also beat the best K'-th score any finished unit
         // has published for this query (a valid bound for the union)
-        const float thr_g = q < m ? fkey_inv(*reinterpret_cast<volatile unsigned*>(gthr + q))
-                                  : -INFINITY;
-        named_bar_sync(1, 32 * kTcEpiWarps);
+        const float thr_g = q < m ? fkey_inv(gk) : -INFINITY;
+        // prefetch the next tile's operands (next unit if this one ends)
+        int nu = u, nt = t + 1;
+        if (nt >= t1) {
+          nu = u + gridDim.x;
+          nt = (nu / work.qtiles) * work.tps;
+        }
+        const bool more = nu < units;
+        if (more) {
+          xv = load_xn4(nt);
+          gk = load_g((nu - (nu / work.qtiles) * work.qtiles) * kTcM + row);
+        }
+        __syncwarp();
         mbar_wait(&tfull[buf], (i >> 1) & 1);
         tc_fence_after();
         const uint32_t taddr =
             tmem + ((uint32_t)(quad * 32) << 16) + buf * kTcN + half * (kTcN / 2);
-        const int base = idx_base + (int)col0 + half * (kTcN / 2);
-        const float* xs0 = xn_s + buf * kTcN + half * (kTcN / 2);
+        const int base = idx_base + t * kTcN + half * (kTcN / 2);
 #pragma unroll 1
-        for (int c = 0; c < kTcN / 64; ++c) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c * 32, r);
+        for (int c = 0; c < kTcN / 64; c += 2) {
+          uint32_t ra[32], rb[32];
+          tmem_ld32(taddr + c * 32, ra);
+          tmem_ld32(taddr + (c + 1) * 32, rb);
           tmem_ld_wait();
-          // scores + a bitmask of the columns that beat the threshold; the
-          // (rare) insertions run from one compact loop so the hot path stays
-          // a straight FFMA/FSETP stream that fits the I-cache
-          const float thr = fminf(L.worst(), thr_g);
-          const float* xs = xs0 + c * 32;
-          float sc[32];
-          uint32_t mask = 0;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float4 nv = *reinterpret_cast<const float4*>(xs + j);
-            sc[j + 0] = fmaf(-2.f, __uint_as_float(r[j + 0]), nv.x);
-            sc[j + 1] = fmaf(-2.f, __uint_as_float(r[j + 1]), nv.y);
-            sc[j + 2] = fmaf(-2.f, __uint_as_float(r[j + 2]), nv.z);
-            sc[j + 3] = fmaf(-2.f, __uint_as_float(r[j + 3]), nv.w);
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t(&r)[32] = h ? rb : ra;
+            // scores + a bitmask of the columns that beat the threshold; the
+            // (rare) insertions run from one compact loop so the hot path
+            // stays a straight FFMA/FSETP stream that fits the I-cache
+            const float thr = fminf(L.worst(), thr_g);
+            const float* xs = xw + (c + h) * 32;
+            float sc[32];
+            uint32_t mask = 0;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 nv = *reinterpret_cast<const float4*>(xs + j);
+              sc[j + 0] = fmaf(-2.f, __uint_as_float(r[j + 0]), nv.x);
+              sc[j + 1] = fmaf(-2.f, __uint_as_float(r[j + 1]), nv.y);
+              sc[j + 2] = fmaf(-2.f, __uint_as_float(r[j + 2]), nv.z);
+              sc[j + 3] = fmaf(-2.f, __uint_as_float(r[j + 3]), nv.w);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) mask |= (sc[j] < thr ? 1u : 0u) << j;
+            if (mask) insert_masked(L, sc, mask, base + (c + h) * 32, thr_g);
           }
-#pragma unroll
-          for (int j = 0; j < 32; ++j) mask |= (sc[j] < thr ? 1u : 0u) << j;
-          if (mask) insert_masked(L, sc, mask, base + c * 32, thr_g);
         }
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
-      }
-      // unit done: publish this (slice, column half)'s candidates
-      if (q < m) {
-        const int64_t o = ((int64_t)(slice * 2 + half) * m + q) * KC;
+        __syncwarp();
+        if (nu != u) {
+          // unit done: publish this (slice, column half)'s candidates
+          if (q < m) {
+            const int64_t o = ((int64_t)(slice * 2 + half) * m + q) * KC;
 #pragma unroll
-        for (int p = 0; p < KC; ++p) {
-          cand_s[o + p] = L.s[p];
-          cand_i[o + p] = L.i[p];
+            for (int p = 0; p < KC; ++p) {
+              cand_s[o + p] = L.s[p];
+              cand_i[o + p] = L.i[p];
+            }
+            if (L.worst() < INFINITY) atomicMin(gthr + q, fkey(L.worst()));
+          }
+          L.init();
+          if (!more) break;
+          u = nu;
+          slice = u / work.qtiles;
+          qt = u - slice * work.qtiles;
+          t1 = min(work.T, slice * work.tps + work.tps);
+          q = qt * kTcM + row;
         }
-        if (L.worst() < INFINITY) atomicMin(gthr + q, fkey(L.worst()));
+        t = nt;
       }
     }
   }
