@@ -170,6 +170,12 @@ TB_API int tb_kernel_mvm(const void* X, const void* Z, const double* w, int64_t 
                   double variance, const double* lengthscales, double* out,
                   void* stream);
 
+/* out[i, j] = k(A_i, B_j), fp64 [na, nb]; the same kernel code as the
+ * statistics (so Kuu and Kuf agree bit for bit).  Feeds the O(M^3) tail. */
+TB_API int tb_kernel_matrix(const void* A, const void* B, int64_t na, int64_t nb,
+                            int64_t dim, int32_t kernel, int32_t dtype, double variance,
+                            const double* lengthscales, double* out, void* stream);
+
 /* ---------------- misc ---------------------------------------------------*/
 TB_API const char* tb_last_error(void);
 /* compiled-in capabilities: bit0 tcgen05 kNN, bit1 SIMT kNN, bit2 SGPR,

@@ -14,7 +14,9 @@ from .errors import (BudgetExceeded, EvaluationError, KernelUnavailable,
 from .graph import (DType, Graph, KernelSpec, MemoryEvent, MemoryTrace,
                     PassConfig, TensorValue, build_kernel_mvm, build_knn,
                     estimate_peak_memory, evaluate, random_inputs, run_pipeline)
+from .mvm import kernel_mvm, se_kernel_mvm
 from .neighbors import KnnOperator, knn
+from .sgpr import SGPR, sgpr_elbo, sgpr_predict_mean
 from .sizes import format_size, parse_size
 
 __all__ = [
@@ -22,5 +24,6 @@ __all__ = [
     "KernelUnavailable", "KnnOperator", "MemoryEvent", "MemoryTrace",
     "PassConfig", "TensorValue", "UnsplittableCandidate", "build_kernel_mvm",
     "build_knn", "estimate_peak_memory", "evaluate", "format_size", "knn",
-    "parse_size", "random_inputs", "run_pipeline",
+    "parse_size", "random_inputs", "run_pipeline", "SGPR", "sgpr_elbo",
+    "sgpr_predict_mean", "kernel_mvm", "se_kernel_mvm",
 ]

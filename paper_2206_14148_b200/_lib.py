@@ -69,6 +69,8 @@ _SIGS = {
                                          _vp, _i64, _vp]),
     "tb_kernel_mvm": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _i32,
                                      ctypes.c_double, _vp, _vp, _vp]),
+    "tb_kernel_matrix": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i32, _i32,
+                                        ctypes.c_double, _vp, _vp, _vp]),
     "tb_last_error": (ctypes.c_char_p, []),
     "tb_capabilities": (ctypes.c_int32, []),
 }

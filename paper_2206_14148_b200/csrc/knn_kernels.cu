@@ -31,28 +31,94 @@ __global__ void rows_prep_kernel(const T* __restrict__ src, int64_t rows,
                                  __nv_bfloat16* __restrict__ lo,
                                  int64_t rows_pad, int64_t d_pad) {
   const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t limit = hi ? rows_pad : rows;
-  if (r >= limit) return;
   const int64_t cols = hi ? d_pad : d;
-  double acc = 0.0;
-  for (int64_t j = lane; j < cols; j += 32) {
-    const double v = (r < rows && j < d) ? (double)src[r * d + j] : 0.0;
-    acc += v * v;
-    if (hi) {
-      const __nv_bfloat16 h = __double2bfloat16(v);
-      const __nv_bfloat16 l = __double2bfloat16(v - (double)__bfloat162float(h));
-      hi[r * d_pad + j] = h;
-      lo[r * d_pad + j] = l;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  float wmax = 0.f;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < limit;
+       r += nwarps) {
+    double acc = 0.0;
+    for (int64_t j = lane; j < cols; j += 32) {
+      const double v = (r < rows && j < d) ? (double)src[r * d + j] : 0.0;
+      acc += v * v;
+      if (hi) {
+        const __nv_bfloat16 h = __double2bfloat16(v);
+        const __nv_bfloat16 l = __double2bfloat16(v - (double)__bfloat162float(h));
+        hi[r * d_pad + j] = h;
+        lo[r * d_pad + j] = l;
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0 && r < rows) {
+      if (n64) n64[r] = acc;
+      if (n32) n32[r] = (float)acc;
+      const float nrm = (float)sqrt(acc) * (1.0f + 1e-6f);
+      if (norm32) norm32[r] = nrm;
+      wmax = fmaxf(wmax, nrm);
     }
   }
-  acc = warp_sum(acc);
-  if (lane == 0 && r < rows) {
+  // one atomic per warp (a per-row atomic on one address serialises)
+  if (max_bits && lane == 0 && wmax > 0.f) atomicMax(max_bits, __float_as_uint(wmax));
+}
+
+// Tensor-core operand prep, G = d_pad / 8 threads per row, 8 elements per
+// thread: 16-byte loads/stores of the bf16 hi/lo split, fp64 norms reduced
+// over the row's lanes, and one max-norm atomic per block (not per row).
+template <typename T, int G>
+__global__ void __launch_bounds__(256)
+rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
+                  double* __restrict__ n64, float* __restrict__ n32,
+                  float* __restrict__ norm32, unsigned* __restrict__ max_bits,
+                  __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
+                  int64_t rows_pad, int64_t d_pad) {
+  __shared__ float wmax[8];
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = gt / G;
+  const int seg = (int)(gt % G);
+  double acc = 0.0;
+  if (r < rows_pad) {
+    double v[8];
+    const int64_t c0 = (int64_t)seg * 8;
+    if (r < rows && c0 + 8 <= d && sizeof(T) == 4 && (d & 3) == 0) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(src + r * d + c0));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(src + r * d + c0 + 4));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        v[j] = (r < rows && c0 + j < d) ? (double)src[r * d + c0 + j] : 0.0;
+    }
+    __align__(16) __nv_bfloat16 h[8];
+    __align__(16) __nv_bfloat16 l[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      acc = fma(v[j], v[j], acc);
+      h[j] = __double2bfloat16(v[j]);
+      l[j] = __double2bfloat16(v[j] - (double)__bfloat162float(h[j]));
+    }
+    *reinterpret_cast<uint4*>(hi + r * d_pad + c0) = *reinterpret_cast<const uint4*>(h);
+    *reinterpret_cast<uint4*>(lo + r * d_pad + c0) = *reinterpret_cast<const uint4*>(l);
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  float nrm = 0.f;
+  if (seg == 0 && r < rows) {
     if (n64) n64[r] = acc;
     if (n32) n32[r] = (float)acc;
-    const float nrm = (float)sqrt(acc) * (1.0f + 1e-6f);
+    nrm = (float)sqrt(acc) * (1.0f + 1e-6f);
     if (norm32) norm32[r] = nrm;
-    if (max_bits) atomicMax(max_bits, __float_as_uint(nrm));
+  }
+  if (max_bits) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nrm = fmaxf(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float m = 0.f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, wmax[w]);
+      atomicMax(max_bits, __float_as_uint(m));
+    }
   }
 }
 
@@ -63,8 +129,20 @@ static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
                      int64_t d_pad, cudaStream_t st) {
   const int64_t limit = hi ? rows_pad : rows;
   if (limit <= 0) return TB_OK;
+  if (hi && (d_pad == 64 || d_pad == 128)) {
+    const int64_t threads = rows_pad * (d_pad / 8);
+    const unsigned blocks = (unsigned)ceil_div(threads, 256);
+    if (d_pad == 64)
+      rows_split_kernel<T, 8><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32, norm32,
+                                                      max_bits, hi, lo, rows_pad, d_pad);
+    else
+      rows_split_kernel<T, 16><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32, norm32,
+                                                       max_bits, hi, lo, rows_pad, d_pad);
+    TB_LAUNCH_CHECK("rows_split");
+    return TB_OK;
+  }
   const int warps = 8;
-  const int64_t blocks = ceil_div(limit, warps);
+  const int64_t blocks = std::min<int64_t>(ceil_div(limit, warps), 148 * 16);
   rows_prep_kernel<T><<<(unsigned)blocks, warps * 32, 0, st>>>(
       (const T*)src, rows, d, n64, n32, norm32, max_bits, hi, lo, rows_pad, d_pad);
   TB_LAUNCH_CHECK("rows_prep");

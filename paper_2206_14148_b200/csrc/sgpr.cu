@@ -1,16 +1,411 @@
-// sgpr.cu — SGPR sufficient statistics and kernel MVM (placeholder).
+// sgpr.cu — SGPR sufficient statistics (Sigma = Kuf Kuf^T, v = Kuf y,
+// yy = y^T y) and the kernel matrix-vector product (predictive mean,
+// paper §5.1 MVM).
+//
+// Statistics, v1 ("exact Gram"): the training axis N
+// is streamed in chunks of Nc points sized by the planner under
+// memory_limit.  Per chunk:
+//   kuf_gen   K[i, n] = k(Z_i, X_n) in fp64 from direct differences
+//             (RBF: s2 exp(-r2/2); Matern-3/2: s2 (1+sqrt3 r) exp(-sqrt3 r)),
+//             written [M_pad, Nc] (n contiguous);
+//   kuf_gemv  v[i] += sum_n K[i,n] y[n]   (one warp per row, deterministic);
+//   syrk      Sigma[a-tile, b-tile] += K_a K_b^T for lower tiles a >= b,
+//             fp64 FMA on 128x128 register-blocked tiles (exact products of
+//             the fp64 kernel values, fp64 accumulation, ascending n).
+// The reference cannot split Kuf Kuf^T at all (split.py:210-214); the
+// contracted-dim running add it uses for Kuf y (split.py:322-324) is what
+// kuf_gemv does per chunk.  The O(M^3) tail runs in fp64 on cuSOLVER via
+// torch.linalg (paper_2206_14148_b200/sgpr.py).
+#include <cmath>
+#include <cstring>
+
 #include "tb_common.cuh"
+
+namespace tb {
+
+constexpr int kMaxDim = 64;
+constexpr int kSyrkTile = 128;
+constexpr int kSyrkKc = 8;
+
+struct KernParams {
+  int kernel;   // TB_KERNEL_RBF / TB_KERNEL_MATERN32
+  int dim;
+  double variance;
+  double inv_ls[kMaxDim];
+};
+
+__device__ __forceinline__ double kern_from_r2(const KernParams& p, double r2) {
+  if (p.kernel == TB_KERNEL_RBF) return p.variance * exp(-0.5 * r2);
+  const double r = sqrt(fmax(r2, 1e-36));
+  const double s3 = 1.7320508075688772 * r;
+  return p.variance * (1.0 + s3) * exp(-s3);
+}
+
+// ------------------------------------------------------------- kuf_gen --
+// Block: 32 inducing rows x 128 data points; Z rows (scaled) staged in smem.
+template <typename T>
+__global__ void __launch_bounds__(256)
+kuf_gen_kernel(const T* __restrict__ X, const T* __restrict__ Z, int64_t n0, int64_t nc,
+               int64_t N, int64_t M, int64_t M_pad, KernParams p, double* __restrict__ K) {
+  __shared__ double zs[32][kMaxDim + 1];
+  const int i0 = blockIdx.y * 32;
+  const int64_t c0 = (int64_t)blockIdx.x * 128;
+  for (int e = threadIdx.x; e < 32 * p.dim; e += blockDim.x) {
+    const int r = e / p.dim, t = e % p.dim;
+    zs[r][t] = (i0 + r < M) ? (double)Z[(int64_t)(i0 + r) * p.dim + t] * p.inv_ls[t] : 0.0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 127, ty = threadIdx.x >> 7;   // 2 row groups of 16
+  const int64_t c = c0 + tx;
+  const bool valid = c < nc && n0 + c < N;
+  double xs[kMaxDim];
+#pragma unroll
+  for (int t = 0; t < kMaxDim; ++t)
+    if (t < p.dim) xs[t] = valid ? (double)X[(n0 + c) * p.dim + t] * p.inv_ls[t] : 0.0;
+  for (int r = ty; r < 32; r += 2) {
+    const int i = i0 + r;
+    if (i >= M_pad || c >= nc) continue;
+    double r2 = 0.0;
+#pragma unroll
+    for (int t = 0; t < kMaxDim; ++t)
+      if (t < p.dim) {
+        const double df = zs[r][t] - xs[t];
+        r2 = fma(df, df, r2);
+      }
+    K[(int64_t)i * nc + c] = (valid && i < M) ? kern_from_r2(p, r2) : 0.0;
+  }
+}
+
+// v[i] += sum_n K[i, n] y[n]  (one warp per inducing row)
+template <typename T>
+__global__ void kuf_gemv_kernel(const double* __restrict__ K, const T* __restrict__ y,
+                                int64_t n0, int64_t nc, int64_t N, int64_t M,
+                                double* __restrict__ v) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= M) return;
+  double acc = 0.0;
+  for (int64_t c = lane; c < nc && n0 + c < N; c += 32) acc = fma(K[i * nc + c], (double)y[n0 + c], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) v[i] += acc;
+}
+
+// yy += sum y^2 over the chunk (single block, fixed order -> deterministic)
+template <typename T>
+__global__ void sumsq_kernel(const T* __restrict__ y, int64_t n0, int64_t n1,
+                             double* __restrict__ out) {
+  __shared__ double part[32];
+  double acc = 0.0;
+  for (int64_t k = n0 + threadIdx.x; k < n1; k += blockDim.x) {
+    const double v = (double)y[k];
+    acc = fma(v, v, acc);
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) *out += v;
+  }
+}
+
+// ---------------------------------------------------------------- syrk --
+// Sigma[a, b] += sum_n K[a, n] K[b, n] on lower tile pairs (ta >= tb).
+// 256 threads, 8x8 fp64 micro-tile per thread over a 128x128 tile.
+__global__ void __launch_bounds__(256)
+syrk_f64_kernel(const double* __restrict__ K, int64_t nc, int64_t M, int ntiles,
+                double* __restrict__ Sigma) {
+  __shared__ __align__(16) double As[2][kSyrkKc][kSyrkTile];
+  __shared__ __align__(16) double Bs[2][kSyrkKc][kSyrkTile];
+  // blockIdx.x -> (ta, tb) with ta >= tb
+  int ta = (int)((sqrt(8.0 * blockIdx.x + 1.0) - 1.0) * 0.5);
+  while ((ta + 1) * (ta + 2) / 2 <= (int)blockIdx.x) ++ta;
+  while (ta * (ta + 1) / 2 > (int)blockIdx.x) --ta;
+  const int tb = blockIdx.x - ta * (ta + 1) / 2;
+  const int a0 = ta * kSyrkTile, b0 = tb * kSyrkTile;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  // loader: 128 rows x 8 k per operand; thread -> row tid/2, k (tid&1)*4..+3
+  const int lr = tid >> 1, lk = (tid & 1) * 4;
+  const double* arow = K + (int64_t)(a0 + lr) * nc;
+  const double* brow = K + (int64_t)(b0 + lr) * nc;
+  double ra[4], rb[4];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t k = k0 + lk + j;
+      ra[j] = k < nc ? arow[k] : 0.0;
+      rb[j] = k < nc ? brow[k] : 0.0;
+    }
+  };
+  load(0);
+  int stage = 0;
+  for (int64_t k0 = 0; k0 < nc; k0 += kSyrkKc) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      As[stage][lk + j][lr] = ra[j];
+      Bs[stage][lk + j][lr] = rb[j];
+    }
+    __syncthreads();
+    if (k0 + kSyrkKc < nc) load(k0 + kSyrkKc);
+#pragma unroll
+    for (int kk = 0; kk < kSyrkKc; ++kk) {
+      double a[8], b[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = As[stage][kk][ty * 8 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        b[j] = Bs[stage][kk][tx * 4 + j];
+        b[4 + j] = Bs[stage][kk][64 + tx * 4 + j];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    stage ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = a0 + ty * 8 + i;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = b0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+      if (c < M && c <= r) Sigma[(int64_t)r * M + c] += acc[i][j];
+    }
+  }
+}
+
+// copy the lower triangle to the upper one
+__global__ void symmetrize_kernel(double* __restrict__ S, int64_t M) {
+  const int64_t r = blockIdx.y * 32 + threadIdx.y;
+  const int64_t c = blockIdx.x * 32 + threadIdx.x;
+  if (r < M && c < M && c > r) S[r * M + c] = S[c * M + r];
+}
+
+// ---------------------------------------------------------- kernel MVM --
+// out[i] = sum_j k(X_i, Z_j) w_j; one thread per X row, Z tiles staged in
+// shared memory (scaled by 1/l), fp64 throughout.
+template <typename T>
+__global__ void __launch_bounds__(256)
+kernel_mvm_kernel(const T* __restrict__ X, const T* __restrict__ Z,
+                  const double* __restrict__ w, int64_t n, int64_t M, KernParams p,
+                  double* __restrict__ out) {
+  constexpr int TZ = 64;
+  __shared__ double zs[TZ][kMaxDim + 1];
+  __shared__ double ws[TZ];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double xs[kMaxDim];
+#pragma unroll
+  for (int t = 0; t < kMaxDim; ++t)
+    if (t < p.dim) xs[t] = i < n ? (double)X[i * p.dim + t] * p.inv_ls[t] : 0.0;
+  double acc = 0.0;
+  for (int64_t z0 = 0; z0 < M; z0 += TZ) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < TZ * p.dim; e += blockDim.x) {
+      const int r = e / p.dim, t = e % p.dim;
+      zs[r][t] = z0 + r < M ? (double)Z[(z0 + r) * p.dim + t] * p.inv_ls[t] : 0.0;
+    }
+    for (int e = threadIdx.x; e < TZ; e += blockDim.x) ws[e] = z0 + e < M ? w[z0 + e] : 0.0;
+    __syncthreads();
+    const int lim = (int)((M - z0) < TZ ? (M - z0) : TZ);
+    for (int r = 0; r < lim; ++r) {
+      double r2 = 0.0;
+#pragma unroll
+      for (int t = 0; t < kMaxDim; ++t)
+        if (t < p.dim) {
+          const double df = xs[t] - zs[r][t];
+          r2 = fma(df, df, r2);
+        }
+      acc = fma(kern_from_r2(p, r2), ws[r], acc);
+    }
+  }
+  if (i < n) out[i] = acc;
+}
+
+static int make_params(int32_t kernel, int64_t dim, double variance,
+                       const double* lengthscales, KernParams* p) {
+  if (kernel != TB_KERNEL_RBF && kernel != TB_KERNEL_MATERN32)
+    return fail(TB_ERR_ARG, "kernel must be rbf or matern32");
+  if (dim < 1 || dim > kMaxDim)
+    return fail(TB_ERR_UNSUPPORTED, "input dimension must be in [1, 64]");
+  if (!(variance > 0)) return fail(TB_ERR_ARG, "variance must be strictly positive");
+  if (!lengthscales) return fail(TB_ERR_ARG, "lengthscales pointer is null");
+  p->kernel = kernel;
+  p->dim = (int)dim;
+  p->variance = variance;
+  for (int t = 0; t < kMaxDim; ++t) p->inv_ls[t] = 0.0;
+  for (int64_t t = 0; t < dim; ++t) {
+    if (!(lengthscales[t] > 0)) return fail(TB_ERR_ARG, "lengthscales must be strictly positive");
+    p->inv_ls[t] = 1.0 / lengthscales[t];
+  }
+  return TB_OK;
+}
+
+static bool sm100(std::string* why) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    *why = "no CUDA device visible";
+    return false;
+  }
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) {
+    *why = "this library is built for sm_100a (B200)";
+    return false;
+  }
+  return true;
+}
+
+}  // namespace tb
+
 using namespace tb;
+
 extern "C" {
-int tb_sgpr_plan_create(int64_t, int64_t, int64_t, int32_t, int32_t, int64_t, int64_t, tb_sgpr_plan*) {
-  return fail(TB_ERR_UNSUPPORTED, "sgpr not built yet");
+
+int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel, int32_t dtype,
+                        int64_t memory_limit, int64_t resident_bytes, tb_sgpr_plan* plan) {
+  if (!plan) return fail(TB_ERR_ARG, "plan pointer is null");
+  std::memset(plan, 0, sizeof(*plan));
+  if (N < 1 || M < 1 || dim < 1) return fail(TB_ERR_ARG, "N, M and dim must be at least 1");
+  if (dim > kMaxDim) return fail(TB_ERR_UNSUPPORTED, "input dimension must be <= 64");
+  if (kernel != TB_KERNEL_RBF && kernel != TB_KERNEL_MATERN32)
+    return fail(TB_ERR_ARG, "kernel must be rbf or matern32");
+  if (dtype != TB_F32 && dtype != TB_F64) return fail(TB_ERR_ARG, "dtype must be f32 or f64");
+  if (M >= (1 << 20)) return fail(TB_ERR_UNSUPPORTED, "M must be < 2^20");
+  plan->N = N; plan->M = M; plan->dim = dim; plan->kernel = kernel; plan->dtype = dtype;
+  plan->memory_limit = memory_limit; plan->resident_bytes = resident_bytes;
+  plan->output_bytes = M * M * 8 + M * 8 + 8;
+  const int64_t M_pad = round_up(M, kSyrkTile);
+  const int64_t limit = memory_limit > 0 ? memory_limit : INT64_MAX;
+  // chunk of training points: big enough to amortise the Sigma tile
+  // read-modify-write (>= 1024), capped at 8192 and by the budget
+  int64_t nc = std::min<int64_t>(8192, round_up(N, 128));
+  for (;;) {
+    const int64_t ws = round_up(M_pad * nc * 8, 256);
+    if (resident_bytes + plan->output_bytes + ws <= limit) {
+      plan->chunk_n = nc;
+      plan->workspace_bytes = ws;
+      plan->peak_bytes = resident_bytes + plan->output_bytes + ws;
+      plan->off[0] = 0;
+      return TB_OK;
+    }
+    if (nc <= 128)
+      return fail(TB_ERR_BUDGET, "sgpr: allocating " + std::to_string(plan->output_bytes + ws) +
+                                     " bytes would exceed the budget (live=" +
+                                     std::to_string(resident_bytes) + ", limit=" +
+                                     std::to_string(memory_limit) + ")");
+    nc = std::max<int64_t>(128, round_up(nc / 2, 128));
+  }
 }
-int tb_sgpr_stats_run(const tb_sgpr_plan*, const void*, const void*, const void*, double,
-                      const double*, double*, double*, double*, int32_t, void*, int64_t, void*) {
-  return fail(TB_ERR_UNSUPPORTED, "sgpr not built yet");
+
+int tb_sgpr_stats_run(const tb_sgpr_plan* p, const void* X, const void* y, const void* Z,
+                      double variance, const double* lengthscales, double* Sigma, double* v,
+                      double* yy, int32_t accumulate, void* workspace,
+                      int64_t workspace_bytes, void* stream) {
+  if (!p) return fail(TB_ERR_ARG, "plan pointer is null");
+  if (!X || !y || !Z || !Sigma || !v || !yy || !workspace)
+    return fail(TB_ERR_ARG, "null buffer passed to tb_sgpr_stats_run");
+  if (workspace_bytes < p->workspace_bytes)
+    return fail(TB_ERR_ARG, "workspace smaller than plan->workspace_bytes");
+  std::string why;
+  if (!sm100(&why)) return fail(TB_ERR_NO_DEVICE, why);
+  KernParams kp;
+  int rc = make_params(p->kernel, p->dim, variance, lengthscales, &kp);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t M = p->M, N = p->N, nc = p->chunk_n;
+  const int64_t M_pad = round_up(M, kSyrkTile);
+  double* K = (double*)workspace;
+  if (!accumulate) {
+    TB_CUDA_TRY(cudaMemsetAsync(Sigma, 0, M * M * 8, st));
+    TB_CUDA_TRY(cudaMemsetAsync(v, 0, M * 8, st));
+    TB_CUDA_TRY(cudaMemsetAsync(yy, 0, 8, st));
+  }
+  const int ntiles = (int)(M_pad / kSyrkTile);
+  const unsigned pairs = (unsigned)(ntiles * (ntiles + 1) / 2);
+  for (int64_t n0 = 0; n0 < N; n0 += nc) {
+    const int64_t cur = std::min(nc, N - n0);
+    dim3 g1((unsigned)ceil_div(cur, 128), (unsigned)(M_pad / 32));
+    if (p->dtype == TB_F32)
+      kuf_gen_kernel<float><<<g1, 256, 0, st>>>((const float*)X, (const float*)Z, n0, cur, N, M,
+                                                M_pad, kp, K);
+    else
+      kuf_gen_kernel<double><<<g1, 256, 0, st>>>((const double*)X, (const double*)Z, n0, cur, N,
+                                                 M, M_pad, kp, K);
+    TB_LAUNCH_CHECK("kuf_gen");
+    const unsigned gb = (unsigned)ceil_div(M, 8);
+    if (p->dtype == TB_F32) {
+      kuf_gemv_kernel<float><<<gb, 256, 0, st>>>(K, (const float*)y, n0, cur, N, M, v);
+      sumsq_kernel<float><<<1, 1024, 0, st>>>((const float*)y, n0, n0 + cur, yy);
+    } else {
+      kuf_gemv_kernel<double><<<gb, 256, 0, st>>>(K, (const double*)y, n0, cur, N, M, v);
+      sumsq_kernel<double><<<1, 1024, 0, st>>>((const double*)y, n0, n0 + cur, yy);
+    }
+    TB_LAUNCH_CHECK("kuf_gemv");
+    syrk_f64_kernel<<<pairs, 256, 0, st>>>(K, cur, M, ntiles, Sigma);
+    TB_LAUNCH_CHECK("syrk_f64");
+  }
+  dim3 gs((unsigned)ceil_div(M, 32), (unsigned)ceil_div(M, 32));
+  symmetrize_kernel<<<gs, dim3(32, 32), 0, st>>>(Sigma, M);
+  TB_LAUNCH_CHECK("symmetrize");
+  return TB_OK;
 }
-int tb_kernel_mvm(const void*, const void*, const double*, int64_t, int64_t, int64_t, int32_t,
-                  int32_t, double, const double*, double*, void*) {
-  return fail(TB_ERR_UNSUPPORTED, "kernel mvm not built yet");
+
+int tb_kernel_matrix(const void* A, const void* B, int64_t na, int64_t nb, int64_t dim,
+                     int32_t kernel, int32_t dtype, double variance,
+                     const double* lengthscales, double* out, void* stream) {
+  if (na < 0 || nb < 0) return fail(TB_ERR_ARG, "bad kernel_matrix extents");
+  if (!A || !B || !out) return fail(TB_ERR_ARG, "null buffer passed to tb_kernel_matrix");
+  if (dtype != TB_F32 && dtype != TB_F64) return fail(TB_ERR_ARG, "dtype must be f32 or f64");
+  KernParams kp;
+  int rc = make_params(kernel, dim, variance, lengthscales, &kp);
+  if (rc) return rc;
+  if (na == 0 || nb == 0) return TB_OK;
+  std::string why;
+  if (!sm100(&why)) return fail(TB_ERR_NO_DEVICE, why);
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 g((unsigned)ceil_div(nb, 128), (unsigned)ceil_div(na, 32));
+  // rows = A (the "inducing" role), columns = B, out[na, nb] (no padding rows)
+  if (dtype == TB_F32)
+    kuf_gen_kernel<float><<<g, 256, 0, st>>>((const float*)B, (const float*)A, 0, nb, nb, na,
+                                             na, kp, out);
+  else
+    kuf_gen_kernel<double><<<g, 256, 0, st>>>((const double*)B, (const double*)A, 0, nb, nb,
+                                              na, na, kp, out);
+  TB_LAUNCH_CHECK("kernel_matrix");
+  return TB_OK;
 }
+
+int tb_kernel_mvm(const void* X, const void* Z, const double* w, int64_t n, int64_t M,
+                  int64_t dim, int32_t kernel, int32_t dtype, double variance,
+                  const double* lengthscales, double* out, void* stream) {
+  if (n < 0 || M < 1) return fail(TB_ERR_ARG, "bad kernel_mvm extents");
+  if (!X || !Z || !w || !out) return fail(TB_ERR_ARG, "null buffer passed to tb_kernel_mvm");
+  if (dtype != TB_F32 && dtype != TB_F64) return fail(TB_ERR_ARG, "dtype must be f32 or f64");
+  KernParams kp;
+  int rc = make_params(kernel, dim, variance, lengthscales, &kp);
+  if (rc) return rc;
+  if (n == 0) return TB_OK;
+  std::string why;
+  if (!sm100(&why)) return fail(TB_ERR_NO_DEVICE, why);
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned blocks = (unsigned)ceil_div(n, 256);
+  if (dtype == TB_F32)
+    kernel_mvm_kernel<float><<<blocks, 256, 0, st>>>((const float*)X, (const float*)Z, w, n, M,
+                                                     kp, out);
+  else
+    kernel_mvm_kernel<double><<<blocks, 256, 0, st>>>((const double*)X, (const double*)Z, w, n,
+                                                      M, kp, out);
+  TB_LAUNCH_CHECK("kernel_mvm");
+  return TB_OK;
 }
+
+}  // extern "C"

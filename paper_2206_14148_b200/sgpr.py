@@ -1,0 +1,213 @@
+"""Sparse GP regression (Titsias ELBO + predictive mean) on B200.
+
+The paper's §5.3 workload (GPflow 2.3.1 ``SGPR`` with
+eXLA splitting).  The reference package has no SGPR code;
+this module follows GPflow 2.3.1 ``SGPR.elbo`` / ``SGPR.predict_f`` (zero
+mean function, one output, ``default_jitter() = 1e-6``) in the Sigma-first
+order: the N-streaming sufficient statistics Sigma = Kuf Kuf^T, v = Kuf y,
+yy = y^T y come from the CUDA library (``tb_sgpr_stats_run``, fused Kuf tile
+generation + exact fp64 Gram, never materialising the M x N matrix beyond one
+planner-sized chunk), the O(M^3) tail runs in fp64 on cuSOLVER via
+torch.linalg, and the predictive mean is the fused kernel MVM K(X*, Z) w.
+
+Multi-GPU: each rank passes its own rows of (X, y); the statistics are
+summed with one NCCL ``all_reduce`` before the (redundant, per-rank) tail.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import EvaluationError
+from .mvm import _as_lengthscales
+from .sizes import as_limit
+
+LOG2PI = math.log(2.0 * math.pi)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev_tensor(a, device):
+    torch = _torch()
+    if isinstance(a, np.ndarray):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(device)
+    return a.to(device).contiguous()
+
+
+def plan(N: int, M: int, dim: int, *, kernel: str = "rbf", dtype=np.float32,
+         memory_limit=None, resident_bytes: int | None = None) -> _lib.SgprPlan:
+    """Planner only (CPU): chunk of training points so that resident inputs +
+    Sigma/v + workspace fit ``memory_limit``."""
+    if kernel not in _lib.KERNELS:
+        raise ValueError(f"kernel must be one of {tuple(_lib.KERNELS)}")
+    es = np.dtype(dtype).itemsize
+    if resident_bytes is None:
+        resident_bytes = (N * dim + N + M * dim) * es
+    p = _lib.SgprPlan()
+    rc = _lib.load().tb_sgpr_plan_create(N, M, dim, _lib.KERNELS[kernel],
+                                         _lib.TB_F32 if np.dtype(dtype) == np.float32 else _lib.TB_F64,
+                                         as_limit(memory_limit), resident_bytes, ctypes.byref(p))
+    _lib.check(rc, f"sgpr_N{N}_M{M}_d{dim}", live=resident_bytes)
+    return p
+
+
+def kernel_matrix(A, B, kind="rbf", variance=1.0, lengthscales=1.0, stream=None):
+    """fp64 K(A, B) on the device (same kernel code as the statistics)."""
+    torch = _torch()
+    dim = int(A.shape[1])
+    ls = _as_lengthscales(lengthscales, dim)
+    out = torch.empty((int(A.shape[0]), int(B.shape[0])), dtype=torch.float64, device=A.device)
+    st = stream if stream is not None else torch.cuda.current_stream(A.device)
+    rc = _lib.load().tb_kernel_matrix(
+        A.data_ptr(), B.data_ptr(), int(A.shape[0]), int(B.shape[0]), dim, _lib.KERNELS[kind],
+        _lib.TB_F32 if A.dtype == torch.float32 else _lib.TB_F64, float(variance),
+        ls.ctypes.data_as(ctypes.c_void_p), out.data_ptr(), st.cuda_stream)
+    _lib.check(rc, "kernel_matrix")
+    return out
+
+
+@dataclass
+class SgprStats:
+    Sigma: object    # torch fp64 [M, M]
+    v: object        # torch fp64 [M]
+    yy: float
+    N: int
+    plan: _lib.SgprPlan
+
+
+class SGPR:
+    """GPflow-2.3.1-compatible SGPR on B200 (zero mean, single output).
+
+    X[N, dim], y[N] (or [N, 1]), Z[M, dim]: numpy arrays or CUDA tensors (f32
+    or f64, shared dtype).  ``memory_limit`` bounds the statistics pass
+    (inputs + Sigma + v + workspace).  With ``group`` set, X/y are this
+    rank's shard and the statistics are all-reduced over the group.
+    """
+
+    def __init__(self, X, y, Z, kernel: str = "rbf", variance: float = 1.0,
+                 lengthscales=1.0, noise_variance: float = 0.01, jitter: float = 1e-6,
+                 memory_limit=None, group=None, device=None):
+        torch = _torch()
+        if kernel not in _lib.KERNELS:
+            raise ValueError(f"kernel must be one of {tuple(_lib.KERNELS)}")
+        if variance <= 0 or noise_variance <= 0 or jitter < 0:
+            raise ValueError("variance and noise_variance must be positive, jitter >= 0")
+        self.device = torch.device(device or "cuda")
+        self.X = _dev_tensor(X, self.device)
+        self.y = _dev_tensor(y, self.device).reshape(-1)
+        self.Z = _dev_tensor(Z, self.device)
+        if self.X.ndim != 2 or self.Z.ndim != 2 or self.X.shape[1] != self.Z.shape[1]:
+            raise EvaluationError("X[N,dim] and Z[M,dim] must share the feature dim")
+        if self.y.numel() != self.X.shape[0]:
+            raise EvaluationError("y must have one entry per row of X")
+        if not (self.X.dtype == self.Z.dtype == self.y.dtype) or \
+                self.X.dtype not in (torch.float32, torch.float64):
+            raise EvaluationError("X, y, Z must share an f32/f64 dtype")
+        self.kernel = kernel
+        self.variance = float(variance)
+        self.dim = int(self.X.shape[1])
+        self.lengthscales = _as_lengthscales(lengthscales, self.dim)
+        self.noise_variance = float(noise_variance)
+        self.jitter = float(jitter)
+        self.memory_limit = memory_limit
+        self.group = group
+        self._stats = None
+        self._w = None
+
+    # -- hot path -----------------------------------------------------------
+    def statistics(self, stream=None) -> SgprStats:
+        torch = _torch()
+        N, dim = int(self.X.shape[0]), self.dim
+        M = int(self.Z.shape[0])
+        es = self.X.element_size()
+        p = plan(N, M, dim, kernel=self.kernel,
+                 dtype=np.float32 if self.X.dtype == torch.float32 else np.float64,
+                 memory_limit=self.memory_limit,
+                 resident_bytes=(N * dim + N + M * dim) * es)
+        Sigma = torch.empty((M, M), dtype=torch.float64, device=self.device)
+        v = torch.empty(M, dtype=torch.float64, device=self.device)
+        yy = torch.empty(1, dtype=torch.float64, device=self.device)
+        ws = torch.empty(max(int(p.workspace_bytes), 1), dtype=torch.uint8, device=self.device)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = _lib.load().tb_sgpr_stats_run(
+            ctypes.byref(p), self.X.data_ptr(), self.y.data_ptr(), self.Z.data_ptr(),
+            self.variance, self.lengthscales.ctypes.data_as(ctypes.c_void_p),
+            Sigma.data_ptr(), v.data_ptr(), yy.data_ptr(), 0, ws.data_ptr(), ws.numel(),
+            st.cuda_stream)
+        _lib.check(rc, "sgpr_stats")
+        del ws
+        n_total = N
+        if self.group is not None:
+            import torch.distributed as dist
+            dist.all_reduce(Sigma, group=self.group)
+            dist.all_reduce(v, group=self.group)
+            dist.all_reduce(yy, group=self.group)
+            nt = torch.tensor([N], dtype=torch.float64, device=self.device)
+            dist.all_reduce(nt, group=self.group)
+            n_total = int(nt.item())
+        self._stats = SgprStats(Sigma, v, float(yy.item()), n_total, p)
+        return self._stats
+
+    # -- O(M^3) tail (cuSOLVER / cuBLAS through torch.linalg, fp64) ----------
+    def _tail(self):
+        torch = _torch()
+        s = self._stats or self.statistics()
+        M = s.v.numel()
+        s2 = self.noise_variance
+        Kuu = kernel_matrix(self.Z, self.Z, self.kernel, self.variance, self.lengthscales)
+        Kuu.diagonal().add_(self.jitter)
+        L = torch.linalg.cholesky(Kuu)
+        del Kuu
+        tmp = torch.linalg.solve_triangular(L, s.Sigma, upper=False)          # L^-1 Sigma
+        AAT = torch.linalg.solve_triangular(L, tmp.mT, upper=False).mT          # L^-1 Sigma L^-T
+        del tmp
+        AAT = 0.5 * (AAT + AAT.mT) / s2
+        trAAT = float(AAT.diagonal().sum().item())
+        AAT.diagonal().add_(1.0)
+        LB = torch.linalg.cholesky(AAT)
+        del AAT
+        Lv = torch.linalg.solve_triangular(L, s.v.reshape(M, 1), upper=False)
+        c = torch.linalg.solve_triangular(LB, Lv, upper=False) / s2
+        N = s.N
+        bound = (-0.5 * N * LOG2PI - float(torch.log(LB.diagonal()).sum().item())
+                 - 0.5 * N * math.log(s2) - 0.5 * s.yy / s2 + 0.5 * float((c * c).sum().item())
+                 - 0.5 * N * self.variance / s2 + 0.5 * trAAT)
+        t = torch.linalg.solve_triangular(LB.mT, c, upper=True)
+        w = torch.linalg.solve_triangular(L.mT, t, upper=True).reshape(M)
+        self._w = w
+        return bound
+
+    def elbo(self) -> float:
+        return self._tail()
+
+    def predict_mean(self, Xnew):
+        """mu(X*) = K(X*, Z) L^-T LB^-T c (GPflow predict_f mean)."""
+        from .mvm import kernel_mvm
+        if self._w is None:
+            self._tail()
+        host = isinstance(Xnew, np.ndarray)
+        Xt = _dev_tensor(Xnew, self.device).to(self.Z.dtype)
+        mu = kernel_mvm(Xt, self.Z, self._w, self.kernel, self.variance, self.lengthscales)
+        return mu.cpu().numpy() if host else mu
+
+
+def sgpr_elbo(X, y, Z, kernel="rbf", variance=1.0, lengthscales=1.0,
+              noise_variance=0.01, *, jitter=1e-6, memory_limit=None, group=None) -> float:
+    """Titsias collapsed ELBO of GPflow 2.3.1 SGPR, on the B200 path."""
+    return SGPR(X, y, Z, kernel, variance, lengthscales, noise_variance, jitter,
+                memory_limit, group).elbo()
+
+
+def sgpr_predict_mean(Xnew, X, y, Z, kernel="rbf", variance=1.0, lengthscales=1.0,
+                      noise_variance=0.01, *, jitter=1e-6, memory_limit=None, group=None):
+    m = SGPR(X, y, Z, kernel, variance, lengthscales, noise_variance, jitter,
+             memory_limit, group)
+    return m.predict_mean(Xnew)

@@ -1,0 +1,77 @@
+"""SGPR + kernel MVM parity on the B200 against the fp64 oracle (SURVEY.md
+§8(c) restatement of GPflow 2.3.1) and the reference's kernel-MVM goldens.
+Gate: ELBO and predictive mean within 1e-4 relative (north star)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_err
+from oracle import mvm as omvm
+from oracle import sgpr as osgpr
+import paper_2206_14148_b200 as tb
+from paper_2206_14148_b200 import synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("kind,ls,dtype", [("rbf", 1.3, np.float64), ("rbf", 0.8, np.float32),
+                                           ("matern32", 0.5, np.float64),
+                                           ("matern32", 0.7, np.float32)])
+def test_sgpr_elbo_and_mean(kind, ls, dtype):
+    X, y, Z, Xs = synthetic.sgpr_data(3000, 3, 150, seed=4, n_test=200, dtype=dtype)
+    ref, w = osgpr.elbo(X, y, Z, kind, 1.2, ls, 0.05)
+    mu_ref = osgpr.predict_mean(Xs, Z, w, kind, 1.2, ls)
+    m = tb.SGPR(X, y, Z, kind, 1.2, ls, 0.05)
+    e = m.elbo()
+    assert abs(e - ref) <= 1e-4 * abs(ref), (e, ref)
+    mu = m.predict_mean(Xs)
+    assert rel_err(mu, mu_ref) <= 1e-4
+
+
+def test_sgpr_statistics_exact():
+    X, y, Z, _ = synthetic.sgpr_data(5000, 4, 300, seed=5, dtype=np.float64)
+    S, v, yy = osgpr.sufficient_stats(X, y, Z, "rbf", 1.0, [0.7, 1.1, 0.9, 1.3])
+    m = tb.SGPR(X, y, Z, "rbf", 1.0, [0.7, 1.1, 0.9, 1.3], 0.01)
+    st = m.statistics()
+    assert rel_err(st.Sigma.cpu().numpy(), S) < 1e-12
+    assert rel_err(st.v.cpu().numpy(), v) < 1e-12
+    assert abs(st.yy - yy) <= 1e-12 * yy
+    assert np.allclose(st.Sigma.cpu().numpy(), st.Sigma.cpu().numpy().T)
+
+
+def test_sgpr_chunking_under_memory_limit():
+    X, y, Z, _ = synthetic.sgpr_data(20000, 3, 500, seed=6, dtype=np.float32)
+    ref, _ = osgpr.elbo(X, y, Z, "matern32", 1.0, 0.5, 0.02)
+    resident = (20000 * 3 + 20000 + 500 * 3) * 4
+    limit = resident + 500 * 500 * 8 + 500 * 8 + 8 + 500 * 128 * 8 * 2   # forces small chunks
+    p = tb.sgpr.plan(20000, 500, 3, kernel="matern32", memory_limit=limit)
+    assert p.chunk_n < 20000 and p.peak_bytes <= limit
+    e = tb.sgpr_elbo(X, y, Z, "matern32", 1.0, 0.5, 0.02, memory_limit=limit)
+    assert abs(e - ref) <= 1e-4 * abs(ref)
+
+
+def test_sgpr_budget_exceeded():
+    X, y, Z, _ = synthetic.sgpr_data(1000, 3, 400, seed=7)
+    with pytest.raises(tb.BudgetExceeded):
+        tb.sgpr_elbo(X, y, Z, memory_limit="1MB")
+
+
+def test_kernel_mvm_matches_reference_golden():
+    g = golden("mvm_se.npz")
+    graph = tb.build_kernel_mvm(700, tb.KernelSpec(float(g["variance"]), float(g["lengthscale"])))
+    out, trace = tb.evaluate(graph, [g["x"], g["y"], g["v"]])
+    assert rel_err(out.array, g["out"]) < 1e-13
+    out2 = tb.se_kernel_mvm(g["x"], g["y"], g["v"], float(g["variance"]), float(g["lengthscale"]))
+    assert rel_err(out2, g["out"]) < 1e-13
+
+
+@pytest.mark.parametrize("kind", ["rbf", "matern32"])
+def test_kernel_mvm_ard(kind):
+    rng = np.random.default_rng(8)
+    X = rng.standard_normal((777, 5))
+    Z = rng.standard_normal((333, 5))
+    w = rng.standard_normal(333)
+    ls = [0.5, 1.0, 1.5, 2.0, 0.8]
+    ref = omvm.kernel_mvm(X, Z, w, kind, 1.7, ls)
+    out = tb.kernel_mvm(X, Z, w, kind, 1.7, ls)
+    assert rel_err(out, ref) < 1e-13
