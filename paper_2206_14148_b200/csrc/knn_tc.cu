@@ -285,7 +285,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             const float thr = fminf(L.worst(), thr_g);
             const float* xs = xw + (c + h) * 32;
             float sc[32];
-            uint32_t mask = 0;
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               const float4 nv = *reinterpret_cast<const float4*>(xs + j);
@@ -294,13 +293,23 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               sc[j + 2] = fmaf(-2.f, __uint_as_float(r[j + 2]), nv.z);
               sc[j + 3] = fmaf(-2.f, __uint_as_float(r[j + 3]), nv.w);
             }
+            // common case: nothing beats the threshold -> one min tree
+            float lo = sc[0];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) mask |= (sc[j] < thr ? 1u : 0u) << j;
-            if (mask) insert_masked(L, sc, mask, base + (c + h) * 32, thr_g);
+            for (int j = 1; j < 32; ++j) lo = fminf(lo, sc[j]);
+            if (lo < thr) {
+              uint32_t mask = 0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) mask |= (sc[j] < thr ? 1u : 0u) << j;
+              insert_masked(L, sc, mask, base + (c + h) * 32, thr_g);
+            }
           }
         }
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
+        // publish the running K'-th score every tile: the other column half
+        // and every other CTA on this query tighten their thresholds with it
+        if (q < m && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst()));
         __syncwarp();
         if (nu != u) {
           // unit done: publish this (slice, column half)'s candidates
