@@ -23,6 +23,7 @@
 // approximate score; the exact fp64 re-rank + certification run after the
 // merge (knn_kernels.cu), so results are exact.
 #include <cudaTypedefs.h>
+#include <cstdlib>
 
 #include "tb_common.cuh"
 #include "knn_internal.h"
@@ -64,7 +65,11 @@ __device__ __forceinline__ float fkey_inv(uint32_t k) {
 // slice-major, handed to the persistent CTAs round-robin, so that at any
 // time the CTAs sweep ~G/qtiles adjacent slices and share them through L2.
 struct TcWork {
-  int qtiles, T, slices, tps;   // tps = database tiles per slice
+  int qtiles;      // query tiles
+  int t0, T;       // database tile range [t0, T) of this launch
+  int slices, tps; // slices of the range, tiles per slice
+  int list0;       // first candidate list index written by this launch
+  int drain_only;  // debug (TB_TC_DRAIN_ONLY=1): epilogue only drains TMEM
 };
 
 template <int PASSES, int KC>
@@ -128,7 +133,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       uint32_t ph = 0, seg = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++seg) {
         const int slice = u / work.qtiles, qt = u - slice * work.qtiles;
-        const int t0 = slice * work.tps, t1 = min(work.T, t0 + work.tps);
+        const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
         mbar_wait(a_empty, (seg & 1) ^ 1);           // previous query tile retired
         mbar_expect_tx(a_full, Cfg::kMats * nkb * Cfg::kABlock);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -163,7 +168,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       uint32_t ph = 0, seg = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++seg) {
         const int slice = u / work.qtiles;
-        const int t0 = slice * work.tps, t1 = min(work.T, t0 + work.tps);
+        const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
         mbar_wait(a_full, seg & 1);
         tc_fence_after();
         for (int t = t0; t < t1; ++t, ++i) {
@@ -241,8 +246,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     int u = blockIdx.x;
     if (u < units) {
       int slice = u / work.qtiles, qt = u - slice * work.qtiles;
-      int t1 = min(work.T, slice * work.tps + work.tps);
-      int t = slice * work.tps;
+      int t1 = min(work.T, work.t0 + slice * work.tps + work.tps);
+      int t = work.t0 + slice * work.tps;
       int q = qt * kTcM + row;
       float4 xv = load_xn4(t);
       unsigned gk = load_g(q);
@@ -257,7 +262,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         int nu = u, nt = t + 1;
         if (nt >= t1) {
           nu = u + gridDim.x;
-          nt = (nu / work.qtiles) * work.tps;
+          nt = work.t0 + (nu / work.qtiles) * work.tps;
         }
         const bool more = nu < units;
         if (more) {
@@ -276,6 +281,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           tmem_ld32(taddr + c * 32, ra);
           tmem_ld32(taddr + (c + 1) * 32, rb);
           tmem_ld_wait();
+          if (work.drain_only) continue;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint32_t(&r)[32] = h ? rb : ra;
@@ -314,7 +320,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         if (nu != u) {
           // unit done: publish this (slice, column half)'s candidates
           if (q < m) {
-            const int64_t o = ((int64_t)(slice * 2 + half) * m + q) * KC;
+            const int64_t o = ((int64_t)(work.list0 + slice * 2 + half) * m + q) * KC;
 #pragma unroll
             for (int p = 0; p < KC; ++p) {
               cand_s[o + p] = L.s[p];
@@ -327,7 +333,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           u = nu;
           slice = u / work.qtiles;
           qt = u - slice * work.qtiles;
-          t1 = min(work.T, slice * work.tps + work.tps);
+          t1 = min(work.T, work.t0 + slice * work.tps + work.tps);
           q = qt * kTcM + row;
         }
         t = nt;
@@ -375,32 +381,43 @@ static int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 
 int tc_max_dpad() { return kTcMaxDpad; }
 
-// Slices per query tile for a chunk of T database tiles: minimise
-// waves x (tiles per slice + ~2 tiles of per-unit overhead).
-static void tc_schedule(int64_t m, int64_t rows_pad, int sms, TcWork* w) {
-  w->qtiles = (int)ceil_div(std::max<int64_t>(m, 1), kTcM);
-  w->T = (int)(rows_pad / kTcN);
-  int best_k = 1;
-  int64_t best = INT64_MAX;
-  for (int k = 1; k <= w->T && k <= 256; ++k) {
-    const int64_t tps = ceil_div(w->T, k);
-    const int64_t keff = ceil_div(w->T, tps);
-    const int64_t units = (int64_t)w->qtiles * keff;
-    const int64_t g = std::min<int64_t>(units, sms);
-    const int64_t cost = ceil_div(units, g) * (tps + 2);
-    if (cost < best) {
-      best = cost;
-      best_k = (int)keff;
+// Schedule of one database chunk of T tiles: a short seed launch over the
+// first kTcSeedTiles tiles (one unit per query tile) publishes per-query
+// thresholds; the main launch splits the remaining tiles into slices,
+// minimising waves x (tiles per slice + ~2 tiles of per-unit overhead).
+constexpr int kTcSeedTiles = 8;
+
+static void tc_schedule(int64_t m, int64_t rows_pad, int sms, TcWork* seed, TcWork* main_) {
+  const int qtiles = (int)ceil_div(std::max<int64_t>(m, 1), kTcM);
+  const int T = (int)(rows_pad / kTcN);
+  const int S = std::min(T, kTcSeedTiles);
+  const char* dbg = std::getenv("TB_TC_DRAIN_ONLY");
+  const int drain = dbg && dbg[0] == '1';
+  *seed = TcWork{qtiles, 0, S, 1, S, 0, drain};
+  const int R = T - S;
+  int best_k = 0;
+  if (R > 0) {
+    int64_t best = INT64_MAX;
+    for (int k = 1; k <= R && k <= 256; ++k) {
+      const int64_t tps = ceil_div(R, k);
+      const int64_t keff = ceil_div(R, tps);
+      const int64_t units = (int64_t)qtiles * keff;
+      const int64_t g = std::min<int64_t>(units, sms);
+      const int64_t cost = ceil_div(units, g) * (tps + 2);
+      if (cost < best) {
+        best = cost;
+        best_k = (int)keff;
+      }
     }
   }
-  w->tps = (int)ceil_div(w->T, best_k);
-  w->slices = (int)ceil_div(w->T, w->tps);
+  const int tps = best_k ? (int)ceil_div(R, best_k) : 0;
+  *main_ = TcWork{qtiles, S, T, best_k, tps, 2, drain};
 }
 
 int tc_lists(int64_t m, int64_t rows_pad, int sms) {
-  TcWork w;
-  tc_schedule(m, rows_pad, sms, &w);
-  return 2 * w.slices;
+  TcWork a, b;
+  tc_schedule(m, rows_pad, sms, &a, &b);
+  return 2 + 2 * b.slices;
 }
 
 template <int PASSES, int KC>
@@ -416,6 +433,11 @@ static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtenso
   TB_LAUNCH_CHECK("knn_tc");
   return TB_OK;
 }
+
+int tc_dispatch(int passes, int cand, const CUtensorMap& mqh, const CUtensorMap& mql,
+                const CUtensorMap& mxh, const CUtensorMap& mxl, const float* xn, int64_t rows,
+                TcWork work, int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
+                unsigned* gthr, cudaStream_t st);
 
 int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfloat16* xlo,
                   const __nv_bfloat16* qhi, const __nv_bfloat16* qlo, const float* xn,
@@ -433,13 +455,23 @@ int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfl
   if ((rc = make_map(&mql, passes == 3 ? qlo : qhi, m_pad, d_pad, kTcM))) return rc;
   if ((rc = make_map(&mxh, xhi, rows_pad, d_pad, kTcN))) return rc;
   if ((rc = make_map(&mxl, passes == 3 ? xlo : xhi, rows_pad, d_pad, kTcN))) return rc;
-  TcWork work;
-  tc_schedule(m, rows_pad, 148, &work);   // the plan's schedule (planner assumes 148 SMs)
-  if (2 * work.slices > lists)
+  TcWork seed, work;
+  tc_schedule(m, rows_pad, 148, &seed, &work);   // the plan's schedule (planner assumes 148 SMs)
+  if (2 + 2 * work.slices > lists)
     return fail(TB_ERR_ARG, "tcgen05 engine: candidate buffer smaller than the schedule needs");
-  const int units = work.qtiles * work.slices;
-  const int grid = std::min(units, sms);
   const int nkb = (int)(d_pad / kTcKB);
+  // every list slot the merge reads must be written: unused ones stay INF
+  rc = tc_dispatch(passes, cand, mqh, mql, mxh, mxl, xn, rows, seed, std::min(seed.qtiles, sms),
+                   m, nkb, idx_base, cs, ci, gthr, st);
+  if (rc || work.slices == 0) return rc;
+  return tc_dispatch(passes, cand, mqh, mql, mxh, mxl, xn, rows, work,
+                     std::min(work.qtiles * work.slices, sms), m, nkb, idx_base, cs, ci, gthr, st);
+}
+
+int tc_dispatch(int passes, int cand, const CUtensorMap& mqh, const CUtensorMap& mql,
+                const CUtensorMap& mxh, const CUtensorMap& mxl, const float* xn, int64_t rows,
+                TcWork work, int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
+                unsigned* gthr, cudaStream_t st) {
 #define TB_TC(P, KC)                                                                      \
   return tc_launch<P, KC>(mqh, mql, mxh, mxl, xn, rows, work, grid, m, nkb, idx_base, cs, \
                           ci, gthr, st)
