@@ -158,6 +158,7 @@ int tb_knn_plan_create(int64_t n, int64_t m, int64_t d, int64_t k, int32_t metri
       plan->off[kQLo] = c.take(plan->m_pad * plan->d_pad * 2);
       plan->off[kXHi] = c.take(chunk_pad * plan->d_pad * 2);
       plan->off[kXLo] = c.take(chunk_pad * plan->d_pad * 2);
+      plan->off[kXExt] = c.take(chunk_pad * 32);
     }
     return c.used;
   };
@@ -231,6 +232,7 @@ int tb_knn_run_ex(const tb_knn_plan* p, const void* x, const void* q,
   __nv_bfloat16* qlo = tc ? (__nv_bfloat16*)at(kQLo) : nullptr;
   __nv_bfloat16* xhi = tc ? (__nv_bfloat16*)at(kXHi) : nullptr;
   __nv_bfloat16* xlo = tc ? (__nv_bfloat16*)at(kXLo) : nullptr;
+  uint8_t* xext = tc ? (uint8_t*)at(kXExt) : nullptr;
   const int64_t es = elem_size(p->dtype);
   const int tile_rows = tc ? 256 : 128;
   unsigned* gthr = (unsigned*)at(kGThr);
@@ -250,7 +252,7 @@ int tb_knn_run_ex(const tb_knn_plan* p, const void* x, const void* q,
     const int64_t rows_pad = round_up(rows, tile_rows);
     const char* xc = (const char*)x + c0 * p->d * es;
     rc = launch_db_prep(p->dtype, xc, rows, p->d, xn, stats, xhi, xlo,
-                        rows_pad, p->d_pad, st);
+                        rows_pad, p->d_pad, xext, st);
     if (rc) return rc;
     const int slices = (int)std::min<int64_t>(p->slices, ceil_div(rows, tile_rows));
     int lists = tc ? tc_lists(p->m, rows_pad, kPlanSms) : slices * 2;
@@ -258,7 +260,7 @@ int tb_knn_run_ex(const tb_knn_plan* p, const void* x, const void* q,
     if (prof) TB_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[2 * c], st));
     if (tc) {
       rc = launch_knn_tc(p->engine == TB_ENGINE_TC1 ? 1 : 3, p->cand, xhi, xlo,
-                         qhi, qlo, xn, rows, rows_pad, p->m, p->m_pad, p->d_pad,
+                         qhi, qlo, xext, rows, rows_pad, p->m, p->m_pad, p->d_pad,
                          lists, (int)c0, cs, ci, gthr, st);
     } else {
       rc = launch_knn_simt(p->dtype, p->cand, xc, q, xn, rows, p->m, p->d,

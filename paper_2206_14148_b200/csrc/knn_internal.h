@@ -22,7 +22,8 @@ enum KnnSlot {
   kXHi = 11,    // bf16[chunk_pad][d_pad]
   kXLo = 12,
   kGThr = 13,   // u32[m]           per-query shared K'-th score bound (ordered key)
-  kNumSlots = 14
+  kXExt = 14,   // bf16[chunk_pad][16] augmented-K rows -(h,m,l) of ||x||^2 (core matrices)
+  kNumSlots = 15
 };
 
 struct KnnDims {
@@ -39,7 +40,7 @@ int launch_query_prep(int dtype, const void* q, int64_t m, int64_t d,
 int launch_db_prep(int dtype, const void* x, int64_t rows, int64_t d,
                    float* xn, unsigned* xmax_bits, __nv_bfloat16* xhi,
                    __nv_bfloat16* xlo, int64_t rows_pad, int64_t d_pad,
-                   cudaStream_t st);
+                   uint8_t* xext, cudaStream_t st);
 // SIMT candidate engine: writes lists [2*slices][m][cand]
 int launch_knn_simt(int dtype, int cand, const void* x_chunk, const void* q,
                     const float* xn, int64_t rows, int64_t m, int64_t d,
@@ -49,7 +50,7 @@ int launch_knn_simt(int dtype, int cand, const void* x_chunk, const void* q,
 // [lists][m][cand]; gthr[m] is the shared per-query threshold (ordered keys)
 int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi,
                   const __nv_bfloat16* xlo, const __nv_bfloat16* qhi,
-                  const __nv_bfloat16* qlo, const float* xn, int64_t rows,
+                  const __nv_bfloat16* qlo, const uint8_t* xext, int64_t rows,
                   int64_t rows_pad, int64_t m, int64_t m_pad, int64_t d_pad,
                   int lists, int idx_base, float* cand_s, int* cand_i,
                   unsigned* gthr, cudaStream_t st);

@@ -70,7 +70,8 @@ rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
                   double* __restrict__ n64, float* __restrict__ n32,
                   float* __restrict__ norm32, unsigned* __restrict__ max_bits,
                   __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
-                  int64_t rows_pad, int64_t d_pad) {
+                  int64_t rows_pad, int64_t d_pad, double scale,
+                  uint8_t* __restrict__ ext) {
   __shared__ float wmax[8];
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t r = gt / G;
@@ -94,14 +95,37 @@ rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       acc = fma(v[j], v[j], acc);
-      h[j] = __double2bfloat16(v[j]);
-      l[j] = __double2bfloat16(v[j] - (double)__bfloat162float(h[j]));
+      const double sv = scale * v[j];          // exact (power-of-two scale)
+      h[j] = __double2bfloat16(sv);
+      l[j] = __double2bfloat16(sv - (double)__bfloat162float(h[j]));
     }
     *reinterpret_cast<uint4*>(hi + r * d_pad + c0) = *reinterpret_cast<const uint4*>(h);
     *reinterpret_cast<uint4*>(lo + r * d_pad + c0) = *reinterpret_cast<const uint4*>(l);
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (ext && seg == 0 && r < rows_pad) {
+    // augmented-K row for the tensor-core engine: -(h, m, l) with
+    // h + m + l = ||x||^2 to ~2^-24 (padding rows: -inf, never selected),
+    // stored as 8-row x 16-byte core matrices (SWIZZLE_NONE, K-major)
+    __nv_bfloat16 e[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) e[j] = __float2bfloat16(0.f);
+    if (r < rows) {
+      const __nv_bfloat16 h0 = __double2bfloat16(acc);
+      const double r1 = acc - (double)__bfloat162float(h0);
+      const __nv_bfloat16 h1 = __double2bfloat16(r1);
+      const __nv_bfloat16 h2 = __double2bfloat16(r1 - (double)__bfloat162float(h1));
+      e[0] = __hneg(h0);
+      e[1] = __hneg(h1);
+      e[2] = __hneg(h2);
+    } else {
+      e[0] = __float2bfloat16(-INFINITY);
+    }
+    uint8_t* base = ext + (r >> 8) * 8192 + ((r & 255) >> 3) * 256 + (r & 7) * 16;
+    *reinterpret_cast<uint4*>(base) = *reinterpret_cast<const uint4*>(e);
+    *reinterpret_cast<uint4*>(base + 128) = make_uint4(0u, 0u, 0u, 0u);
+  }
   float nrm = 0.f;
   if (seg == 0 && r < rows) {
     if (n64) n64[r] = acc;
@@ -126,7 +150,8 @@ template <typename T>
 static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
                      float* n32, float* norm32, unsigned* max_bits,
                      __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t rows_pad,
-                     int64_t d_pad, cudaStream_t st) {
+                     int64_t d_pad, cudaStream_t st, double scale = 1.0,
+                     uint8_t* ext = nullptr) {
   const int64_t limit = hi ? rows_pad : rows;
   if (limit <= 0) return TB_OK;
   if (hi && (d_pad == 64 || d_pad == 128)) {
@@ -134,10 +159,12 @@ static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
     const unsigned blocks = (unsigned)ceil_div(threads, 256);
     if (d_pad == 64)
       rows_split_kernel<T, 8><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32, norm32,
-                                                      max_bits, hi, lo, rows_pad, d_pad);
+                                                      max_bits, hi, lo, rows_pad, d_pad, scale,
+                                                      ext);
     else
       rows_split_kernel<T, 16><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32, norm32,
-                                                       max_bits, hi, lo, rows_pad, d_pad);
+                                                       max_bits, hi, lo, rows_pad, d_pad, scale,
+                                                       ext);
     TB_LAUNCH_CHECK("rows_split");
     return TB_OK;
   }
@@ -153,18 +180,21 @@ int launch_query_prep(int dtype, const void* q, int64_t m, int64_t d,
                       double* qn64, float* qnorm, __nv_bfloat16* qhi,
                       __nv_bfloat16* qlo, int64_t m_pad, int64_t d_pad,
                       cudaStream_t st) {
+  // the tensor-core engines use 2q (exact) so that acc' = 2 q.x - ||x||^2
   if (dtype == TB_F32)
-    return rows_prep<float>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st);
-  return rows_prep<double>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st);
+    return rows_prep<float>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st, 2.0);
+  return rows_prep<double>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st, 2.0);
 }
 
 int launch_db_prep(int dtype, const void* x, int64_t rows, int64_t d,
                    float* xn, unsigned* xmax_bits, __nv_bfloat16* xhi,
                    __nv_bfloat16* xlo, int64_t rows_pad, int64_t d_pad,
-                   cudaStream_t st) {
+                   uint8_t* xext, cudaStream_t st) {
   if (dtype == TB_F32)
-    return rows_prep<float>(x, rows, d, nullptr, xn, nullptr, xmax_bits, xhi, xlo, rows_pad, d_pad, st);
-  return rows_prep<double>(x, rows, d, nullptr, xn, nullptr, xmax_bits, xhi, xlo, rows_pad, d_pad, st);
+    return rows_prep<float>(x, rows, d, nullptr, xn, nullptr, xmax_bits, xhi, xlo, rows_pad, d_pad,
+                            st, 1.0, xext);
+  return rows_prep<double>(x, rows, d, nullptr, xn, nullptr, xmax_bits, xhi, xlo, rows_pad, d_pad,
+                           st, 1.0, xext);
 }
 
 // ------------------------------------------------- SIMT candidate engine --

@@ -39,6 +39,9 @@ constexpr int kTcEpiWarps = 8;
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
 constexpr int kTcMaxDpad = 128;  // query tile stays resident in shared memory
 constexpr int kTcStages = 4;     // 32 KB database k-blocks in flight
+constexpr int kTcExtK = 16;      // augmented K block carrying -||x||^2
+constexpr uint32_t kTcAExt = kTcM * kTcExtK * 2;   // 4 KB  [128 x 16] bf16
+constexpr uint32_t kTcBExt = kTcN * kTcExtK * 2;   // 8 KB  [256 x 16] bf16
 
 template <int PASSES>
 struct TcCfg {
@@ -46,8 +49,8 @@ struct TcCfg {
   static constexpr uint32_t kABlock = kTcM * 128;               // 16 KB
   static constexpr uint32_t kBBlock = kTcN * 128;               // 32 KB
   static size_t smem_bytes(int nkb) {
-    return 1024 + (size_t)kMats * nkb * kABlock + (size_t)kTcStages * kBBlock +
-           kTcEpiWarps * kTcN * sizeof(float) + (2 * kTcStages + 6) * 8 + 16;
+    return 1024 + (size_t)kMats * nkb * kABlock + kTcAExt + (size_t)kTcStages * kBBlock +
+           2 * kTcBExt + (2 * kTcStages + 10) * 8 + 16;
   }
 };
 
@@ -72,35 +75,50 @@ struct TcWork {
   int drain_only;  // debug (TB_TC_DRAIN_ONLY=1): epilogue only drains TMEM
 };
 
+// The accumulator holds acc' = (2q).x - ||x||^2: the norm enters through one
+// extra K=16 MMA per tile (A_ext rows = [1,1,1,0...], B_ext rows =
+// -(h,m,l), the bf16 triple split of ||x||^2; SWIZZLE_NONE K-major core
+// matrices).  The selection score is s = -acc' = ||x||^2 - 2 q.x.
 template <int PASSES, int KC>
 __global__ void __launch_bounds__(kTcThreads, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               const __grid_constant__ CUtensorMap tm_qlo,
               const __grid_constant__ CUtensorMap tm_xhi,
               const __grid_constant__ CUtensorMap tm_xlo,
-              const float* __restrict__ xn, int64_t rows, TcWork work, int m, int nkb,
+              const uint8_t* __restrict__ xext, TcWork work, int m, int nkb,
               int idx_base, float* __restrict__ cand_s, int* __restrict__ cand_i,
               unsigned* __restrict__ gthr) {
   using Cfg = TcCfg<PASSES>;
   constexpr int S = kTcStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // keep the shared-window provenance (generic pointers would turn every
-  // epilogue load into LD.E); only the offset is rounded up to 1 KB
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_base = smem;
   uint8_t* b_base = a_base + (size_t)Cfg::kMats * nkb * Cfg::kABlock;
-  float* xn_w = reinterpret_cast<float*>(b_base + (size_t)S * Cfg::kBBlock);
-  uint64_t* full = reinterpret_cast<uint64_t*>(xn_w + kTcEpiWarps * kTcN);
+  uint8_t* bext = b_base + (size_t)S * Cfg::kBBlock;          // 2 x 8 KB
+  uint8_t* aext = bext + 2 * kTcBExt;                          // 4 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(aext + kTcAExt);
   uint64_t* empty = full + S;
   uint64_t* a_full = empty + S;
   uint64_t* a_empty = a_full + 1;
   uint64_t* tfull = a_empty + 1;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* efull = tempty + 2;
+  uint64_t* eempty = efull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(eempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = work.qtiles * work.slices;
 
+  // constant A_ext: row r = [1, 1, 1, 0 ... 0] in the interleaved layout
+  // (8-row groups of 256 B: k-chunk 0 at +0, k-chunk 1 at +128)
+  for (int r = threadIdx.x; r < kTcM; r += blockDim.x) {
+    uint4* c0 = reinterpret_cast<uint4*>(aext + (r >> 3) * 256 + (r & 7) * 16);
+    uint4* c1 = reinterpret_cast<uint4*>(aext + (r >> 3) * 256 + 128 + (r & 7) * 16);
+    const uint32_t one = 0x3F80u;                        // bf16(1.0)
+    *c0 = make_uint4(one | (one << 16), one, 0u, 0u);
+    *c1 = make_uint4(0u, 0u, 0u, 0u);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -111,6 +129,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 32 * kTcEpiWarps);
+      mbar_init(&efull[b], 1);
+      mbar_init(&eempty[b], 1);
     }
     fence_mbar_init();
   }
@@ -129,7 +149,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         tma_prefetch(&tm_qlo);
         tma_prefetch(&tm_xlo);
       }
-      int s = 0;
+      int s = 0, i = 0;
       uint32_t ph = 0, seg = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++seg) {
         const int slice = u / work.qtiles, qt = u - slice * work.qtiles;
@@ -143,7 +163,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             tma_load_2d(a_base + (size_t)(nkb + kb) * Cfg::kABlock, &tm_qlo, a_full,
                         kb * kTcKB, qt * kTcM);
         }
-        for (int t = t0; t < t1; ++t) {
+        for (int t = t0; t < t1; ++t, ++i) {
+          const int e = i & 1;
+          mbar_wait(&eempty[e], ((i >> 1) & 1) ^ 1);
+          mbar_expect_tx(&efull[e], kTcBExt);
+          bulk_load(bext + e * kTcBExt, xext + (size_t)t * kTcBExt, kTcBExt, &efull[e]);
           for (int kb = 0; kb < nkb; ++kb) {
 #pragma unroll
             for (int mat = 0; mat < Cfg::kMats; ++mat) {
@@ -164,6 +188,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     // -------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(kTcM, kTcN);
+      const uint32_t aext_a = smem_u32(aext);
       int s = 0, i = 0;
       uint32_t ph = 0, seg = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++seg) {
@@ -174,8 +199,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         for (int t = t0; t < t1; ++t, ++i) {
           const int buf = i & 1;
           mbar_wait(&tempty[buf], ((i >> 1) & 1) ^ 1);
+          mbar_wait(&efull[buf], (i >> 1) & 1);
           tc_fence_after();
           const uint32_t d = tmem + buf * kTcN;
+          // acc = -||x||^2  (K = 16 augmented block, initialises the tile)
+          mma_bf16(d, desc_k_inter(aext_a, 128, 256), desc_k_inter(smem_u32(bext + buf * kTcBExt), 128, 256),
+                   idesc, 0);
           for (int kb = 0; kb < nkb; ++kb) {
             const uint32_t ahi = smem_u32(a_base + (size_t)kb * Cfg::kABlock);
             const uint32_t alo = smem_u32(a_base + (size_t)(nkb + kb) * Cfg::kABlock);
@@ -186,8 +215,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
 #pragma unroll
             for (int kk = 0; kk < kTcKB / 16; ++kk) {
               const uint32_t ko = kk * 32;  // 16 bf16 = 32 bytes along the swizzled row
-              mma_bf16(d, desc_k_sw128(ahi + ko), desc_k_sw128(b0 + ko), idesc,
-                       (kb | kk) != 0);
+              mma_bf16(d, desc_k_sw128(ahi + ko), desc_k_sw128(b0 + ko), idesc, 1);
               if (PASSES == 3)
                 mma_bf16(d, desc_k_sw128(alo + ko), desc_k_sw128(b0 + ko), idesc, 1);
             }
@@ -211,9 +239,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               }
             }
           }
-          mma_commit(&tfull[buf]);  // accumulator ready for the epilogue
+          mma_commit(&eempty[buf]);  // norm block may be replaced
+          mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
         }
-        mma_commit(a_empty);        // query tile may be replaced
+        mma_commit(a_empty);         // query tile may be replaced
       }
     }
   } else {
@@ -222,22 +251,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     const int quad = warp & 3;           // TMEM lane quadrant this warp may read
     const int half = ew >> 2;            // column half of the 256-wide tile
     const int row = quad * 32 + lane;    // query row within the tile
-    float* xw0 = xn_w + ew * 2 * (kTcN / 2);   // this warp's ||x||^2 double buffer
-    // ||x||^2 of the 4 columns this lane stages for tile t (per-warp copy:
-    // no cross-warp barrier on the critical path)
-    auto load_xn4 = [&](int t) {
-      const int64_t g = (int64_t)t * kTcN + half * (kTcN / 2) + 4 * lane;
-      float4 v;
-      if (g + 3 < rows) {
-        v = __ldg(reinterpret_cast<const float4*>(xn + g));
-      } else {
-        v.x = g + 0 < rows ? xn[g + 0] : INFINITY;
-        v.y = g + 1 < rows ? xn[g + 1] : INFINITY;
-        v.z = g + 2 < rows ? xn[g + 2] : INFINITY;
-        v.w = g + 3 < rows ? xn[g + 3] : INFINITY;
-      }
-      return v;
-    };
     auto load_g = [&](int qq) -> unsigned {
       return qq < m ? *reinterpret_cast<volatile unsigned*>(gthr + qq) : 0u;
     };
@@ -249,27 +262,19 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       int t1 = min(work.T, work.t0 + slice * work.tps + work.tps);
       int t = work.t0 + slice * work.tps;
       int q = qt * kTcM + row;
-      float4 xv = load_xn4(t);
       unsigned gk = load_g(q);
       for (int i = 0;; ++i) {
         const int buf = i & 1;
-        float* xw = xw0 + buf * (kTcN / 2);
-        *reinterpret_cast<float4*>(xw + 4 * lane) = xv;
-        // candidates must also beat the best K'-th score any finished unit
-        // has published for this query (a valid bound for the union)
+        // candidates must also beat the best K'-th score any list has
+        // published for this query (a valid bound for the union)
         const float thr_g = q < m ? fkey_inv(gk) : -INFINITY;
-        // prefetch the next tile's operands (next unit if this one ends)
         int nu = u, nt = t + 1;
         if (nt >= t1) {
           nu = u + gridDim.x;
           nt = work.t0 + (nu / work.qtiles) * work.tps;
         }
         const bool more = nu < units;
-        if (more) {
-          xv = load_xn4(nt);
-          gk = load_g((nu - (nu / work.qtiles) * work.qtiles) * kTcM + row);
-        }
-        __syncwarp();
+        if (more) gk = load_g((nu - (nu / work.qtiles) * work.qtiles) * kTcM + row);
         mbar_wait(&tfull[buf], (i >> 1) & 1);
         tc_fence_after();
         const uint32_t taddr =
@@ -285,28 +290,21 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint32_t(&r)[32] = h ? rb : ra;
-            // scores + a bitmask of the columns that beat the threshold; the
-            // (rare) insertions run from one compact loop so the hot path
-            // stays a straight FFMA/FSETP stream that fits the I-cache
+            // common case: no column beats the threshold -> one max tree
+            // over acc' (score = -acc'); the rare insertions run from one
+            // compact loop so the hot path fits the I-cache
             const float thr = fminf(L.worst(), thr_g);
-            const float* xs = xw + (c + h) * 32;
-            float sc[32];
+            float hi = __uint_as_float(r[0]);
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 nv = *reinterpret_cast<const float4*>(xs + j);
-              sc[j + 0] = fmaf(-2.f, __uint_as_float(r[j + 0]), nv.x);
-              sc[j + 1] = fmaf(-2.f, __uint_as_float(r[j + 1]), nv.y);
-              sc[j + 2] = fmaf(-2.f, __uint_as_float(r[j + 2]), nv.z);
-              sc[j + 3] = fmaf(-2.f, __uint_as_float(r[j + 3]), nv.w);
-            }
-            // common case: nothing beats the threshold -> one min tree
-            float lo = sc[0];
-#pragma unroll
-            for (int j = 1; j < 32; ++j) lo = fminf(lo, sc[j]);
-            if (lo < thr) {
+            for (int j = 1; j < 32; ++j) hi = fmaxf(hi, __uint_as_float(r[j]));
+            if (-hi < thr) {
+              float sc[32];
               uint32_t mask = 0;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) mask |= (sc[j] < thr ? 1u : 0u) << j;
+              for (int j = 0; j < 32; ++j) {
+                sc[j] = -__uint_as_float(r[j]);
+                mask |= (sc[j] < thr ? 1u : 0u) << j;
+              }
               insert_masked(L, sc, mask, base + (c + h) * 32, thr_g);
             }
           }
@@ -316,7 +314,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         // publish the running K'-th score every tile: the other column half
         // and every other CTA on this query tighten their thresholds with it
         if (q < m && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst()));
-        __syncwarp();
         if (nu != u) {
           // unit done: publish this (slice, column half)'s candidates
           if (q < m) {
@@ -326,7 +323,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               cand_s[o + p] = L.s[p];
               cand_i[o + p] = L.i[p];
             }
-            if (L.worst() < INFINITY) atomicMin(gthr + q, fkey(L.worst()));
           }
           L.init();
           if (!more) break;
@@ -422,25 +418,25 @@ int tc_lists(int64_t m, int64_t rows_pad, int sms) {
 
 template <int PASSES, int KC>
 static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtensorMap& xh,
-                     const CUtensorMap& xl, const float* xn, int64_t rows, TcWork work,
+                     const CUtensorMap& xl, const uint8_t* xext, TcWork work,
                      int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
                      unsigned* gthr, cudaStream_t st) {
   const size_t smem = TcCfg<PASSES>::smem_bytes(nkb);
   TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<PASSES, KC>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  knn_tc_kernel<PASSES, KC><<<grid, kTcThreads, smem, st>>>(qh, ql, xh, xl, xn, rows, work,
+  knn_tc_kernel<PASSES, KC><<<grid, kTcThreads, smem, st>>>(qh, ql, xh, xl, xext, work,
                                                             (int)m, nkb, idx_base, cs, ci, gthr);
   TB_LAUNCH_CHECK("knn_tc");
   return TB_OK;
 }
 
 int tc_dispatch(int passes, int cand, const CUtensorMap& mqh, const CUtensorMap& mql,
-                const CUtensorMap& mxh, const CUtensorMap& mxl, const float* xn, int64_t rows,
+                const CUtensorMap& mxh, const CUtensorMap& mxl, const uint8_t* xext,
                 TcWork work, int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
                 unsigned* gthr, cudaStream_t st);
 
 int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfloat16* xlo,
-                  const __nv_bfloat16* qhi, const __nv_bfloat16* qlo, const float* xn,
+                  const __nv_bfloat16* qhi, const __nv_bfloat16* qlo, const uint8_t* xext,
                   int64_t rows, int64_t rows_pad, int64_t m, int64_t m_pad, int64_t d_pad,
                   int lists, int idx_base, float* cs, int* ci, unsigned* gthr,
                   cudaStream_t st) {
@@ -461,19 +457,19 @@ int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfl
     return fail(TB_ERR_ARG, "tcgen05 engine: candidate buffer smaller than the schedule needs");
   const int nkb = (int)(d_pad / kTcKB);
   // every list slot the merge reads must be written: unused ones stay INF
-  rc = tc_dispatch(passes, cand, mqh, mql, mxh, mxl, xn, rows, seed, std::min(seed.qtiles, sms),
+  rc = tc_dispatch(passes, cand, mqh, mql, mxh, mxl, xext, seed, std::min(seed.qtiles, sms),
                    m, nkb, idx_base, cs, ci, gthr, st);
   if (rc || work.slices == 0) return rc;
-  return tc_dispatch(passes, cand, mqh, mql, mxh, mxl, xn, rows, work,
+  return tc_dispatch(passes, cand, mqh, mql, mxh, mxl, xext, work,
                      std::min(work.qtiles * work.slices, sms), m, nkb, idx_base, cs, ci, gthr, st);
 }
 
 int tc_dispatch(int passes, int cand, const CUtensorMap& mqh, const CUtensorMap& mql,
-                const CUtensorMap& mxh, const CUtensorMap& mxl, const float* xn, int64_t rows,
+                const CUtensorMap& mxh, const CUtensorMap& mxl, const uint8_t* xext,
                 TcWork work, int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
                 unsigned* gthr, cudaStream_t st) {
 #define TB_TC(P, KC)                                                                      \
-  return tc_launch<P, KC>(mqh, mql, mxh, mxl, xn, rows, work, grid, m, nkb, idx_base, cs, \
+  return tc_launch<P, KC>(mqh, mql, mxh, mxl, xext, work, grid, m, nkb, idx_base, cs, \
                           ci, gthr, st)
   if (passes == 3) {
     if (cand == 16) TB_TC(3, 16);

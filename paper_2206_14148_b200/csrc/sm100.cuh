@@ -149,6 +149,17 @@ __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;                         // SWIZZLE_128B   [61,64)
   return d;
 }
+// K-major operand without swizzle ("interleaved"): 8-row x 16-byte core
+// matrices; lbo = byte stride between the two K core matrices of a K=16
+// step, sbo = byte stride between 8-row groups.
+__device__ __forceinline__ uint64_t desc_k_inter(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;                         // version = 1, layout 0 (none)
+  return d;
+}
 // instruction descriptor, kind::f16: bf16 x bf16 -> f32, both K-major
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4)            // D format f32
