@@ -18,6 +18,7 @@
 // torch.linalg (paper_2206_14148_b200/sgpr.py).
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 
 #include "tb_common.cuh"
 
@@ -182,6 +183,95 @@ syrk_f64_kernel(const double* __restrict__ K, int64_t nc, int64_t M, int ntiles,
   }
 }
 
+// Same contract on the FP64 tensor cores: DMMA mma.sync m8n8k4 (fp64
+// products and accumulation, i.e. the same exact-Gram numerics).  128x128
+// CTA tile, 8 warps as 2 (rows) x 4 (cols), 64x32 per warp = 8x4 m8n8 tiles;
+// K staged 16 deep, double buffered, k-major with a 4-double pad.
+constexpr int kDmKc = 16;
+constexpr int kDmLd = kSyrkTile + 4;
+constexpr size_t kDmSmem = 2 * 2 * kDmKc * kDmLd * sizeof(double);
+
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256, 1)
+syrk_dmma_kernel(const double* __restrict__ K, int64_t nc, int64_t M, int ntiles,
+                 double* __restrict__ Sigma) {
+  extern __shared__ __align__(16) double dsm[];
+  double* As = dsm;                              // [2][kDmKc][kDmLd]
+  double* Bs = dsm + 2 * kDmKc * kDmLd;
+  int ta = (int)((sqrt(8.0 * blockIdx.x + 1.0) - 1.0) * 0.5);
+  while ((ta + 1) * (ta + 2) / 2 <= (int)blockIdx.x) ++ta;
+  while (ta * (ta + 1) / 2 > (int)blockIdx.x) --ta;
+  const int tb = blockIdx.x - ta * (ta + 1) / 2;
+  const int a0 = ta * kSyrkTile, b0 = tb * kSyrkTile;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wr = warp >> 2, wc = warp & 3;       // 2 x 4 warps
+  const int g = lane >> 2, tg = lane & 3;        // fragment coordinates
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // loader: 128 rows x 16 k per operand; thread -> row tid/2, k (tid&1)*8..+7
+  const int lr = tid >> 1, lk = (tid & 1) * 8;
+  const double* arow = K + (int64_t)(a0 + lr) * nc;
+  const double* brow = K + (int64_t)(b0 + lr) * nc;
+  double ra[8], rb[8];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t k = k0 + lk + j;
+      ra[j] = k < nc ? arow[k] : 0.0;
+      rb[j] = k < nc ? brow[k] : 0.0;
+    }
+  };
+  load(0);
+  int stage = 0;
+  for (int64_t k0 = 0; k0 < nc; k0 += kDmKc) {
+    double* as = As + stage * kDmKc * kDmLd;
+    double* bs = Bs + stage * kDmKc * kDmLd;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      as[(lk + j) * kDmLd + lr] = ra[j];
+      bs[(lk + j) * kDmLd + lr] = rb[j];
+    }
+    __syncthreads();
+    if (k0 + kDmKc < nc) load(k0 + kDmKc);
+#pragma unroll
+    for (int ks = 0; ks < kDmKc / 4; ++ks) {
+      double af[8], bf[4];
+      const double* ak = as + (ks * 4 + tg) * kDmLd + wr * 64 + g;
+      const double* bk = bs + (ks * 4 + tg) * kDmLd + wc * 32 + g;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) af[i] = ak[i * 8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = bk[j * 8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    stage ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = a0 + wr * 64 + i * 8 + g;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = b0 + wc * 32 + j * 8 + 2 * tg + e;
+        if (c < M && c <= r) Sigma[(int64_t)r * M + c] += acc[i][j][e];
+      }
+    }
+  }
+}
+
 // copy the lower triangle to the upper one
 __global__ void symmetrize_kernel(double* __restrict__ S, int64_t M) {
   const int64_t r = blockIdx.y * 32 + threadIdx.y;
@@ -331,6 +421,13 @@ int tb_sgpr_stats_run(const tb_sgpr_plan* p, const void* X, const void* y, const
   }
   const int ntiles = (int)(M_pad / kSyrkTile);
   const unsigned pairs = (unsigned)(ntiles * (ntiles + 1) / 2);
+  // Gram engine: FP64 tensor cores (DMMA) by default; TB_SGPR_GRAM=simt
+  // selects the CUDA-core fp64 SYRK (same numerics, used as a cross-check)
+  const char* eng = std::getenv("TB_SGPR_GRAM");
+  const bool use_dmma = !(eng && std::strcmp(eng, "simt") == 0);
+  if (use_dmma)
+    TB_CUDA_TRY(cudaFuncSetAttribute(syrk_dmma_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDmSmem));
   for (int64_t n0 = 0; n0 < N; n0 += nc) {
     const int64_t cur = std::min(nc, N - n0);
     dim3 g1((unsigned)ceil_div(cur, 128), (unsigned)(M_pad / 32));
@@ -350,8 +447,13 @@ int tb_sgpr_stats_run(const tb_sgpr_plan* p, const void* X, const void* y, const
       sumsq_kernel<double><<<1, 1024, 0, st>>>((const double*)y, n0, n0 + cur, yy);
     }
     TB_LAUNCH_CHECK("kuf_gemv");
-    syrk_f64_kernel<<<pairs, 256, 0, st>>>(K, cur, M, ntiles, Sigma);
-    TB_LAUNCH_CHECK("syrk_f64");
+    if (use_dmma) {
+      syrk_dmma_kernel<<<pairs, 256, kDmSmem, st>>>(K, cur, M, ntiles, Sigma);
+      TB_LAUNCH_CHECK("syrk_dmma");
+    } else {
+      syrk_f64_kernel<<<pairs, 256, 0, st>>>(K, cur, M, ntiles, Sigma);
+      TB_LAUNCH_CHECK("syrk_f64");
+    }
   }
   dim3 gs((unsigned)ceil_div(M, 32), (unsigned)ceil_div(M, 32));
   symmetrize_kernel<<<gs, dim3(32, 32), 0, st>>>(Sigma, M);

@@ -28,7 +28,9 @@ def test_sgpr_elbo_and_mean(kind, ls, dtype):
     assert rel_err(mu, mu_ref) <= 1e-4
 
 
-def test_sgpr_statistics_exact():
+@pytest.mark.parametrize("gram", ["dmma", "simt"])
+def test_sgpr_statistics_exact(gram, monkeypatch):
+    monkeypatch.setenv("TB_SGPR_GRAM", gram)
     X, y, Z, _ = synthetic.sgpr_data(5000, 4, 300, seed=5, dtype=np.float64)
     S, v, yy = osgpr.sufficient_stats(X, y, Z, "rbf", 1.0, [0.7, 1.1, 0.9, 1.3])
     m = tb.SGPR(X, y, Z, "rbf", 1.0, [0.7, 1.1, 0.9, 1.3], 0.01)
