@@ -128,6 +128,91 @@ def host_cores() -> int:
 
 
 # ---------------------------------------------------------------------------
+# SGPR (BASELINE.json configs[3]): ELBO evaluations/s at C4
+
+
+SG_N, SG_D, SG_M = 2_000_000, 11, 10_000
+
+
+def sgpr_cpu_baseline(n_sample: int, threads: int):
+    """fp64 numpy restatement (oracle/sgpr.py) on a bounded sample of N; the
+    statistics are linear in N, so evals/s = 1 / (t_stats * N / n + t_tail)."""
+    from oracle import sgpr as osgpr
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((n_sample, SG_D))
+    y = np.sin(X.sum(axis=1)) + 0.1 * rng.standard_normal(n_sample)
+    Z = X[:SG_M] if n_sample >= SG_M else rng.standard_normal((SG_M, SG_D))
+    t0 = time.perf_counter()
+    S, v, yy = osgpr.sufficient_stats(X, y, Z, "rbf", 1.0, 1.0)
+    t_stats = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    osgpr.elbo_from_stats(S, v, yy, SG_N, osgpr.kuu(Z, "rbf", 1.0, 1.0), 0.01, 1.0)
+    t_tail = time.perf_counter() - t0
+    per_eval = t_stats * SG_N / n_sample + t_tail
+    return {"value": 1.0 / per_eval, "unit": "elbo_evals/s", "cores": threads, "kind": "port",
+            "sample": f"Sigma/v/yy over {n_sample} of N={SG_N} points ({t_stats:.1f}s, "
+                      f"linear in N) + fp64 tail ({t_tail:.1f}s): oracle/sgpr.py (GPflow 2.3.1 "
+                      "SGPR restatement, numpy/OpenBLAS fp64)"}
+
+
+def run_sgpr(args, dev, world, rank, dist):
+    import torch
+
+    from paper_2206_14148_b200 import SGPR
+    from paper_2206_14148_b200.distributed import shard_range
+    start, stop = shard_range(SG_N, rank, world)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77 + rank)
+    X = torch.randn((stop - start, SG_D), generator=g, device=dev)
+    y = (torch.sin(X.double().sum(1)) + 0.1 * torch.randn(stop - start, generator=g, device=dev,
+                                                          dtype=torch.float64)).float()
+    g.manual_seed(5)
+    Z = torch.randn((SG_M, SG_D), generator=g, device=dev)       # same on every rank
+    group = dist.group.WORLD if dist is not None else None
+    # warm the kernels on a small problem, then time one full evaluation
+    SGPR(X[:4096], y[:4096], Z[:512], "rbf", 1.0, 1.0, 0.01).elbo()
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)
+    base = torch.cuda.memory_allocated(dev) - (X.numel() + y.numel() + Z.numel()) * 4
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    m = SGPR(X, y, Z, "rbf", 1.0, 1.0, 0.01, memory_limit=LIMIT, group=group)
+    e0.record()
+    st = m.statistics()
+    e1.record()
+    torch.cuda.synchronize()
+    peak_stats = torch.cuda.max_memory_allocated(dev) - base
+    elbo = m.elbo()
+    e2.record()
+    torch.cuda.synchronize()
+    stats_ms, total_ms = e0.elapsed_time(e1), e0.elapsed_time(e2)
+    if dist is not None:
+        t = torch.tensor([stats_ms, total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        stats_ms, total_ms = (float(v) for v in t.tolist())
+    useful = SG_N * SG_M * (SG_M + 1)
+    achieved = useful / (stats_ms / 1e3) / 1e12
+    out = {"metric": "sgpr_elbo_evals_per_s", "value": 1e3 / total_ms, "unit": "elbo_evals/s",
+           "ms_per_eval": total_ms, "stats_ms": stats_ms, "tail_ms": total_ms - stats_ms,
+           "elbo": elbo, "dtype": "f32 inputs, fp64 statistics and tail",
+           "config": {"workload": "sgpr_c4_rbf_N2e6_d11_M1e4_1GB", "N": SG_N, "d": SG_D,
+                      "M": SG_M, "kernel": "rbf", "lengthscale": 1.0, "noise": 0.01,
+                      "memory_limit": LIMIT, "chunk_n": int(st.plan.chunk_n),
+                      "parallelism": f"N-shard{world}", "timed": "1 evaluation after a "
+                      "small-problem warm-up (one C4 evaluation takes seconds)"},
+           "peak_stats_mb": peak_stats / 1e6, "planned_peak_mb": st.plan.peak_bytes / 1e6,
+           "roofline": {"bound": "tensor", "achieved": achieved, "peak": 40.0, "unit": "TFLOP/s",
+                        "frac": achieved / 40.0, "traffic": None,
+                        "kernel": "syrk_dmma (fp64 tensor-core exact Gram)",
+                        "peak_source": "nominal B200 FP64 tensor 40 TF/s (not in "
+                                       "MEASURED_PEAKS.json)",
+                        "useful_flops": useful}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = sgpr_cpu_baseline(args.sgpr_cpu_n, host_cores())
+    del m, X, y, Z
+    return out
 
 
 def run_reference(args):
@@ -174,9 +259,11 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TB_FORCE_DIST=1 exercises the NCCL gather/merge path even at world 1
+    use_dist = world > 1 or os.environ.get("TB_FORCE_DIST") == "1"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if use_dist:
         dist.init_process_group("nccl", device_id=dev)
     start, stop = distributed.shard_range(N_DB, rank, world)
     rows = stop - start
@@ -191,7 +278,7 @@ def run_ours(args):
     torch.cuda.reset_peak_memory_stats(dev)
     base_alloc = torch.cuda.memory_allocated(dev) - (x.numel() + q.numel()) * 4
 
-    out_dtype = np.float64 if world > 1 else np.float32
+    out_dtype = np.float64 if use_dist else np.float32
     op = neighbors.KnnOperator(rows, M_Q, DIM, K, dtype=np.float32, out_dtype=out_dtype,
                                engine=args.engine, memory_limit=LIMIT, device=dev)
     plan = op.plan
@@ -205,30 +292,30 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     def step(events=None):
-        if world == 1:
+        if not use_dist:
             return op.run(x, q, out, events=events)
         return distributed.knn_sharded(x, q, K, index_base=start, operator=op)
 
-    launches_per_step = 2 + 3 * int(plan.n_chunks) + (1 if world > 1 else 0)
+    launches_per_step = 2 + 3 * int(plan.n_chunks) + (1 if use_dist else 0)
     sampler = ClockSampler(local)
     sampler.start()
     for _ in range(args.warmup):
         step()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
     for s in range(args.steps):
-        step(ev_sets[s] if world == 1 else None)
+        step(ev_sets[s] if not use_dist else None)
     t1.record()
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     clocks = sampler.stop()
     ms = t0.elapsed_time(t1)
-    if world > 1:
+    if use_dist:
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
@@ -238,7 +325,7 @@ def run_ours(args):
 
     # dominant kernel (candidate engine) time, measured inside the timed region
     eng_ms = None
-    if world == 1:
+    if not use_dist:
         per = []
         for evs in ev_sets:
             per.append(sum(evs[2 * c].elapsed_time(evs[2 * c + 1])
@@ -304,6 +391,12 @@ def run_ours(args):
                "sample": f"{nq} queries vs the full 1e6x128 db in {dt:.1f}s "
                          "(tensorbudget pipelined kNN algorithm, oracle/knn.py)"}
 
+    sgpr = None
+    if not args.no_sgpr:
+        del op
+        torch.cuda.empty_cache()
+        sgpr = run_sgpr(args, dev, world, rank, dist if use_dist else None)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -328,9 +421,10 @@ def run_ours(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "sgpr": sgpr,
         }
         print(json.dumps(line))
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
     return 0
 
@@ -346,6 +440,8 @@ def main():
     ap.add_argument("--ref-queries", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sgpr", action="store_true")
+    ap.add_argument("--sgpr-cpu-n", type=int, default=16384)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
