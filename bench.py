@@ -32,6 +32,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep stdout to the one JSON line
 
 N_DB, M_Q, DIM, K = 1_000_000, 10_000, 128, 10
 LIMIT = 10**9
