@@ -133,32 +133,62 @@ TB_API int tb_knn_fallback_count(const tb_knn_plan* plan, const void* workspace,
                           void* stream, int64_t* count);
 
 /* ---------------- SGPR sufficient statistics ----------------------------
- * Sigma = Kuf Kuf^T (M x M, fp64, full symmetric), v = Kuf y (M, fp64),
- * yy = y^T y, for X[N,dim], y[N], Z[M,dim] (dtype), accumulated over N in
- * ascending order.  No reference counterpart; the nearest
- * is the contracted-dim running add of split.py:322-324,539-547, which the
+ * Sigma = Kuf Kuf^T (M x M, fp64), v = Kuf y (M, fp64), yy = y^T y, for
+ * X[N,dim], y[N], Z[M,dim] (dtype), accumulated over N in ascending order.
+ * No reference counterpart; the nearest is the
+ * contracted-dim running add of split.py:322-324,539-547, which the
  * reference cannot apply to Kuf Kuf^T (split.py:210-214).  accumulate != 0
- * adds into Sigma/v/yy instead of overwriting (for N streamed in calls). */
+ * adds into Sigma/v/yy instead of overwriting (for N streamed in calls).
+ *
+ * Engines:
+ *   TB_SGPR_ENGINE_I8   exact Gram of Kuf rounded once to 24-bit fixed point
+ *                       (Sigma = var^2 2^-48 Q Q^T, v = var 2^-24 Q y, both
+ *                       exact for that Q) on the INT8 tensor cores; Sigma is
+ *                       returned as packed lower tiles (TB_SIGMA_TILES);
+ *   TB_SGPR_ENGINE_F64  fp64 products + fp64 accumulation on the FP64 tensor
+ *                       cores (DMMA); Sigma full symmetric (TB_SIGMA_FULL);
+ *   TB_SGPR_ENGINE_F64_SIMT  the same numerics on CUDA cores (cross-check).
+ *   TB_SGPR_ENGINE_AUTO = I8. */
+#define TB_SGPR_ENGINE_AUTO 0
+#define TB_SGPR_ENGINE_I8 1
+#define TB_SGPR_ENGINE_F64 2
+#define TB_SGPR_ENGINE_F64_SIMT 3
+
+/* Sigma layouts: FULL = row-major symmetric [M, M]; TILES = lower 128x128
+ * tiles (a >= b) packed at index a(a+1)/2 + b, each tile column-major,
+ * M_pad = round_up(M, 128); rows/cols >= M are zero. */
+#define TB_SIGMA_FULL 0
+#define TB_SIGMA_TILES 1
+
 typedef struct tb_sgpr_plan {
   int64_t N, M, dim;
   int32_t kernel, dtype;
   int64_t memory_limit, resident_bytes;
+  int32_t engine;           /* engine actually used (never AUTO)            */
+  int32_t sigma_layout;     /* TB_SIGMA_FULL / TB_SIGMA_TILES               */
+  int64_t M_pad;
+  int64_t sigma_bytes;      /* size of the Sigma buffer tb_sgpr_stats_run writes */
   int64_t chunk_n;          /* training points per streamed chunk           */
   int64_t workspace_bytes;
   int64_t output_bytes;     /* Sigma + v + yy                               */
-  int64_t peak_bytes;
+  int64_t peak_bytes;       /* resident + outputs + workspace <= limit      */
   int64_t off[8];
 } tb_sgpr_plan;
 
 TB_API int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel,
-                 int32_t dtype, int64_t memory_limit, int64_t resident_bytes,
-                 tb_sgpr_plan* plan);
+                 int32_t dtype, int32_t engine, int64_t memory_limit,
+                 int64_t resident_bytes, tb_sgpr_plan* plan);
 
 TB_API int tb_sgpr_stats_run(const tb_sgpr_plan* plan, const void* X, const void* y,
                       const void* Z, double variance,
                       const double* lengthscales, double* Sigma, double* v,
                       double* yy, int32_t accumulate, void* workspace,
                       int64_t workspace_bytes, void* stream);
+
+/* Expand a TB_SIGMA_TILES Sigma into the full symmetric [M, M] matrix the
+ * O(M^3) tail (cuSOLVER) consumes; for TB_SIGMA_FULL plans it is a copy. */
+TB_API int tb_sgpr_sigma_unpack(const tb_sgpr_plan* plan, const double* Sigma,
+                                double* full, void* stream);
 
 /* ---------------- kernel MVM --------------------------------------------
  * out[i] = sum_j k(X_i, Z_j) w_j in fp64 accumulation, X[n,dim], Z[M,dim]

@@ -55,6 +55,35 @@ def sufficient_stats(X, y, Z, kind="rbf", variance=1.0, lengthscales=1.0,
     return Sigma, v, float(y @ y)
 
 
+def sufficient_stats_fixed24(X, y, Z, kind="rbf", variance=1.0, lengthscales=1.0,
+                             chunk: int = 8192):
+    """Statistics of the B200 fixed-point engine (TB_SGPR_ENGINE_I8), restated
+    exactly: Q = min(rint(Kuf / variance * 2^24), 2^24 - 1) once, then
+    Sigma = variance^2 2^-48 Q Q^T and v = variance 2^-24 Q y with no rounding
+    inside the integer Gram (digit planes a2 2^16 + a1 2^8 + a0, each level
+    sum < 2^53, so float64 matmuls of the digit planes are exact)."""
+    X = np.asarray(X, np.float64)
+    y = np.asarray(y, np.float64).reshape(-1)
+    M = Z.shape[0]
+    Sigma = np.zeros((M, M))
+    v = np.zeros(M)
+    for s in range(0, X.shape[0], chunk):
+        K = kernel_matrix(Z, X[s:s + chunk], kind, variance, lengthscales)
+        Q = np.minimum(np.rint(K * (2.0 ** 24 / variance)), 2.0 ** 24 - 1)
+        a2 = np.floor(Q / 65536.0)
+        a1 = np.floor((Q - a2 * 65536.0) / 256.0)
+        a0 = Q - a2 * 65536.0 - a1 * 256.0
+        L4 = a2 @ a2.T
+        L3 = a2 @ a1.T + a1 @ a2.T
+        L2 = a2 @ a0.T + a1 @ a1.T + a0 @ a2.T
+        L1 = a1 @ a0.T + a0 @ a1.T
+        L0 = a0 @ a0.T
+        P = (((L4 * 256.0 + L3) * 256.0 + L2) * 256.0 + L1) * 256.0 + L0
+        Sigma += P * (variance * variance * 2.0 ** -48)
+        v += (Q @ y[s:s + chunk]) * (variance * 2.0 ** -24)
+    return Sigma, v, float(y @ y)
+
+
 def kuu(Z, kind="rbf", variance=1.0, lengthscales=1.0, jitter=1e-6):
     K = kernel_matrix(Z, Z, kind, variance, lengthscales)
     return K + jitter * np.eye(Z.shape[0])

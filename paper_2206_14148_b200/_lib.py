@@ -24,6 +24,8 @@ TB_F32, TB_F64 = 0, 1
 METRICS = {"l2": 0, "l1": 1, "cosine": 2}
 ENGINES = {"auto": 0, "tc3": 1, "simt": 2, "tc1": 3}
 KERNELS = {"rbf": 0, "matern32": 1}
+SGPR_ENGINES = {"auto": 0, "i8": 1, "f64": 2, "f64_simt": 3}
+TB_SIGMA_FULL, TB_SIGMA_TILES = 0, 1
 
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32
@@ -47,6 +49,7 @@ class SgprPlan(ctypes.Structure):
         ("N", _i64), ("M", _i64), ("dim", _i64),
         ("kernel", _i32), ("dtype", _i32),
         ("memory_limit", _i64), ("resident_bytes", _i64),
+        ("engine", _i32), ("sigma_layout", _i32), ("M_pad", _i64), ("sigma_bytes", _i64),
         ("chunk_n", _i64), ("workspace_bytes", _i64), ("output_bytes", _i64),
         ("peak_bytes", _i64), ("off", _i64 * 8),
     ]
@@ -62,11 +65,12 @@ _SIGS = {
     "tb_topk_merge": (ctypes.c_int, [_vp, _vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp]),
     "tb_knn_fallback_count": (ctypes.c_int, [ctypes.POINTER(KnnPlan), _vp, _vp,
                                              ctypes.POINTER(_i64)]),
-    "tb_sgpr_plan_create": (ctypes.c_int, [_i64, _i64, _i64, _i32, _i32, _i64, _i64,
+    "tb_sgpr_plan_create": (ctypes.c_int, [_i64, _i64, _i64, _i32, _i32, _i32, _i64, _i64,
                                            ctypes.POINTER(SgprPlan)]),
     "tb_sgpr_stats_run": (ctypes.c_int, [ctypes.POINTER(SgprPlan), _vp, _vp, _vp,
                                          ctypes.c_double, _vp, _vp, _vp, _vp, _i32,
                                          _vp, _i64, _vp]),
+    "tb_sgpr_sigma_unpack": (ctypes.c_int, [ctypes.POINTER(SgprPlan), _vp, _vp, _vp]),
     "tb_kernel_mvm": (ctypes.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _i32,
                                      ctypes.c_double, _vp, _vp, _vp]),
     "tb_kernel_matrix": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _i32, _i32,

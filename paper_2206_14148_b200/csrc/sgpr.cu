@@ -20,27 +20,12 @@
 #include <cstring>
 #include <cstdlib>
 
-#include "tb_common.cuh"
+#include "sgpr_internal.h"
 
 namespace tb {
 
-constexpr int kMaxDim = 64;
 constexpr int kSyrkTile = 128;
 constexpr int kSyrkKc = 8;
-
-struct KernParams {
-  int kernel;   // TB_KERNEL_RBF / TB_KERNEL_MATERN32
-  int dim;
-  double variance;
-  double inv_ls[kMaxDim];
-};
-
-__device__ __forceinline__ double kern_from_r2(const KernParams& p, double r2) {
-  if (p.kernel == TB_KERNEL_RBF) return p.variance * exp(-0.5 * r2);
-  const double r = sqrt(fmax(r2, 1e-36));
-  const double s3 = 1.7320508075688772 * r;
-  return p.variance * (1.0 + s3) * exp(-s3);
-}
 
 // ------------------------------------------------------------- kuf_gen --
 // Block: 32 inducing rows x 128 data points; Z rows (scaled) staged in smem.
@@ -361,7 +346,8 @@ using namespace tb;
 extern "C" {
 
 int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel, int32_t dtype,
-                        int64_t memory_limit, int64_t resident_bytes, tb_sgpr_plan* plan) {
+                        int32_t engine, int64_t memory_limit, int64_t resident_bytes,
+                        tb_sgpr_plan* plan) {
   if (!plan) return fail(TB_ERR_ARG, "plan pointer is null");
   std::memset(plan, 0, sizeof(*plan));
   if (N < 1 || M < 1 || dim < 1) return fail(TB_ERR_ARG, "N, M and dim must be at least 1");
@@ -369,22 +355,35 @@ int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel, int32
   if (kernel != TB_KERNEL_RBF && kernel != TB_KERNEL_MATERN32)
     return fail(TB_ERR_ARG, "kernel must be rbf or matern32");
   if (dtype != TB_F32 && dtype != TB_F64) return fail(TB_ERR_ARG, "dtype must be f32 or f64");
+  if (engine < TB_SGPR_ENGINE_AUTO || engine > TB_SGPR_ENGINE_F64_SIMT)
+    return fail(TB_ERR_ARG, "unknown SGPR engine");
   if (M >= (1 << 20)) return fail(TB_ERR_UNSUPPORTED, "M must be < 2^20");
+  if (engine == TB_SGPR_ENGINE_AUTO) engine = TB_SGPR_ENGINE_I8;
   plan->N = N; plan->M = M; plan->dim = dim; plan->kernel = kernel; plan->dtype = dtype;
   plan->memory_limit = memory_limit; plan->resident_bytes = resident_bytes;
-  plan->output_bytes = M * M * 8 + M * 8 + 8;
+  plan->engine = engine;
   const int64_t M_pad = round_up(M, kSyrkTile);
+  plan->M_pad = M_pad;
+  const bool i8 = engine == TB_SGPR_ENGINE_I8;
+  plan->sigma_layout = i8 ? TB_SIGMA_TILES : TB_SIGMA_FULL;
+  plan->sigma_bytes = i8 ? i8_tiles(M_pad) * kI8Tile * kI8Tile * 8 : M * M * 8;
+  plan->output_bytes = plan->sigma_bytes + M * 8 + 8;
   const int64_t limit = memory_limit > 0 ? memory_limit : INT64_MAX;
-  // chunk of training points: big enough to amortise the Sigma tile
-  // read-modify-write (>= 1024), capped at 8192 and by the budget
-  int64_t nc = std::min<int64_t>(8192, round_up(N, 128));
+  // chunk of training points: as large as the budget allows (amortises the
+  // per-chunk Sigma tile read-modify-write); fp64 engines cap at 8192, the
+  // fixed-point engine at kI8MaxChunk (s32 accumulator range)
+  int64_t nc = i8 ? std::min<int64_t>(kI8MaxChunk, round_up(N, 128))
+                  : std::min<int64_t>(8192, round_up(N, 128));
   for (;;) {
-    const int64_t ws = round_up(M_pad * nc * 8, 256);
+    const int64_t ws = i8 ? round_up(i8_planes_bytes(M_pad, nc), 256) +
+                                round_up(i8_vpart_bytes(M_pad, nc), 256)
+                          : round_up(M_pad * nc * 8, 256);
     if (resident_bytes + plan->output_bytes + ws <= limit) {
       plan->chunk_n = nc;
       plan->workspace_bytes = ws;
       plan->peak_bytes = resident_bytes + plan->output_bytes + ws;
       plan->off[0] = 0;
+      plan->off[1] = i8 ? round_up(i8_planes_bytes(M_pad, nc), 256) : 0;   // vpart
       return TB_OK;
     }
     if (nc <= 128)
@@ -412,19 +411,34 @@ int tb_sgpr_stats_run(const tb_sgpr_plan* p, const void* X, const void* y, const
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t M = p->M, N = p->N, nc = p->chunk_n;
-  const int64_t M_pad = round_up(M, kSyrkTile);
-  double* K = (double*)workspace;
+  const int64_t M_pad = p->M_pad;
   if (!accumulate) {
-    TB_CUDA_TRY(cudaMemsetAsync(Sigma, 0, M * M * 8, st));
+    TB_CUDA_TRY(cudaMemsetAsync(Sigma, 0, p->sigma_bytes, st));
     TB_CUDA_TRY(cudaMemsetAsync(v, 0, M * 8, st));
     TB_CUDA_TRY(cudaMemsetAsync(yy, 0, 8, st));
   }
+  if (p->engine == TB_SGPR_ENGINE_I8) {
+    uint8_t* planes = (uint8_t*)workspace + p->off[0];
+    double* vpart = (double*)((uint8_t*)workspace + p->off[1]);
+    for (int64_t n0 = 0; n0 < N; n0 += nc) {
+      const int64_t cur = std::min(nc, N - n0);
+      rc = i8_stats_chunk(X, y, Z, p->dtype, n0, cur, N, M, M_pad, nc, kp, planes, vpart,
+                          Sigma, v, st);
+      if (rc) return rc;
+      if (p->dtype == TB_F32)
+        sumsq_kernel<float><<<1, 1024, 0, st>>>((const float*)y, n0, n0 + cur, yy);
+      else
+        sumsq_kernel<double><<<1, 1024, 0, st>>>((const double*)y, n0, n0 + cur, yy);
+      TB_LAUNCH_CHECK("sumsq");
+    }
+    return TB_OK;
+  }
+  double* K = (double*)workspace;
   const int ntiles = (int)(M_pad / kSyrkTile);
   const unsigned pairs = (unsigned)(ntiles * (ntiles + 1) / 2);
-  // Gram engine: FP64 tensor cores (DMMA) by default; TB_SGPR_GRAM=simt
-  // selects the CUDA-core fp64 SYRK (same numerics, used as a cross-check)
-  const char* eng = std::getenv("TB_SGPR_GRAM");
-  const bool use_dmma = !(eng && std::strcmp(eng, "simt") == 0);
+  // fp64 Gram: FP64 tensor cores (DMMA), or the CUDA-core SYRK (same
+  // numerics, kept as an independent cross-check)
+  const bool use_dmma = p->engine == TB_SGPR_ENGINE_F64;
   if (use_dmma)
     TB_CUDA_TRY(cudaFuncSetAttribute(syrk_dmma_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDmSmem));
@@ -459,6 +473,20 @@ int tb_sgpr_stats_run(const tb_sgpr_plan* p, const void* X, const void* y, const
   symmetrize_kernel<<<gs, dim3(32, 32), 0, st>>>(Sigma, M);
   TB_LAUNCH_CHECK("symmetrize");
   return TB_OK;
+}
+
+int tb_sgpr_sigma_unpack(const tb_sgpr_plan* p, const double* Sigma, double* full,
+                         void* stream) {
+  if (!p || !Sigma || !full) return fail(TB_ERR_ARG, "null argument to tb_sgpr_sigma_unpack");
+  std::string why;
+  if (!sm100(&why)) return fail(TB_ERR_NO_DEVICE, why);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->sigma_layout == TB_SIGMA_FULL) {
+    if (full != Sigma)
+      TB_CUDA_TRY(cudaMemcpyAsync(full, Sigma, p->M * p->M * 8, cudaMemcpyDeviceToDevice, st));
+    return TB_OK;
+  }
+  return i8_unpack(Sigma, p->M, p->M_pad, full, st);
 }
 
 int tb_kernel_matrix(const void* A, const void* B, int64_t na, int64_t nb, int64_t dim,

@@ -1,0 +1,378 @@
+// sgpr_i8.cu — SGPR sufficient statistics with an EXACT fixed-point Gram on
+// the INT8 tensor cores (tcgen05.mma kind::i8, s32 accumulators in TMEM).
+//
+// Why fixed point (re-checked in DESIGN.md §4): an
+// error in Sigma = Kuf Kuf^T that is not itself of Gram form (K+d)(K+d)^T is
+// amplified by cond(Kuu); every fp32-class product scheme (fp32, 3xTF32)
+// misses the 1e-4 predictive-mean tolerance at cond ~1e5.  Here Kuf is
+// rounded ONCE to 24-bit fixed point, q = rint(k / variance * 2^24), and
+//     Sigma = variance^2 * 2^-48 * Q Q^T,   v = variance * 2^-24 * Q y
+// are computed EXACTLY for that Q (integer products, no rounding inside a
+// chunk), i.e. the statistics of a consistently perturbed Kuf.  Q is split
+// into three u8 digit planes, Q = a2 2^16 + a1 2^8 + a0, and
+//     Q_a Q_b^T = sum_{s,t} 2^{8(s+t)} A_s B_t^T
+// is 9 u8 x u8 products grouped into 5 weight levels l = s + t.
+//
+// Per streamed chunk of Nc training points (planner, <= kI8MaxChunk so no
+// s32 level can overflow):
+//   kuf_quant   q[i, n] from fp64 direct differences (the same kernel code
+//               as Kuu), written as 3 planes [3][M_pad][Nc] u8 (n contiguous:
+//               K-major for both MMA operands); v partial sums per
+//               128-point segment from the SAME q (exact products q*y in fp64);
+//   v_reduce    v[i] += variance 2^-24 sum_seg vpart[seg][i] (fixed order);
+//   gram_i8     persistent, one CTA per SM, units = lower 128x128 Sigma tiles.
+//     warp 0    TMA producer: per 64-point k-block the plane tiles
+//               (A_p rows of tile a, B_p rows of tile b), 64-B swizzle,
+//               through a 12-stage mbarrier ring (16 KB per stage);
+//     warp 1    TMEM (512 columns = 4 accumulators x 128) + MMA issuer:
+//               phase A: levels 4..1 (8 products per k-block):
+//                 acc0 = A2B2, acc1 = A2B1 + A1B2, acc2 = A2B0 + A1B1 + A0B2,
+//                 acc3 = A1B0 + A0B1;
+//               phase B (after the epilogue drained acc0): acc0 = A0B0
+//               (plane 0 streamed a second time);
+//     warps 2-9 epilogue: P = ((((L4 256 + L3) 256 + L2) 256 + L1) 256 + L0
+//               in fp64 registers (64 per thread), then one read-modify-write
+//               of the fp64 Sigma tile: Sigma += variance^2 2^-48 P.
+// Sigma is kept as packed lower tiles (column-major 128x128, tile (a, b),
+// a >= b, at index a(a+1)/2 + b): 414 MB at M = 1e4 instead of 800 MB, so a
+// 10880-point chunk fits the 1 GB budget of C4.  tb_sgpr_sigma_unpack
+// expands it for the O(M^3) tail.
+#include <cmath>
+
+#include "sgpr_internal.h"
+#include "sm100.cuh"
+
+namespace tb {
+using namespace sm100;
+
+constexpr int kI8Stages = 12;
+constexpr uint32_t kI8TileBytes = kI8Tile * kI8KB;        // 8 KB
+constexpr uint32_t kI8StageBytes = 2 * kI8TileBytes;      // A + B
+constexpr int kI8EpiWarps = 8;
+constexpr int kI8Threads = 64 + 32 * kI8EpiWarps;
+constexpr size_t kI8Smem = 1024 + (size_t)kI8Stages * kI8StageBytes + 256;
+
+// ------------------------------------------------------------ kuf_quant --
+// Block: 32 inducing rows x 128 points (256 threads: 128 points x 2 row
+// groups of 16).  Each thread keeps its scaled x in fp64 registers.
+template <typename T>
+__global__ void __launch_bounds__(256)
+kuf_quant_kernel(const T* __restrict__ X, const T* __restrict__ y, const T* __restrict__ Z,
+                 int64_t n0, int64_t cur, int64_t M, int64_t M_pad, int64_t nc, KernParams p,
+                 double qscale, uint8_t* __restrict__ planes, double* __restrict__ vpart) {
+  __shared__ double zs[32][kMaxDim + 1];
+  __shared__ double red[32][4];
+  const int i0 = blockIdx.y * 32;
+  const int64_t c = (int64_t)blockIdx.x * 128 + (threadIdx.x & 127);
+  const int ty = threadIdx.x >> 7;
+  for (int e = threadIdx.x; e < 32 * p.dim; e += blockDim.x) {
+    const int r = e / p.dim, t = e % p.dim;
+    zs[r][t] = (i0 + r < M) ? (double)Z[(int64_t)(i0 + r) * p.dim + t] * p.inv_ls[t] : 0.0;
+  }
+  __syncthreads();
+  const bool valid = c < cur;
+  double xs[kMaxDim];
+#pragma unroll
+  for (int t = 0; t < kMaxDim; ++t)
+    if (t < p.dim) xs[t] = valid ? (double)X[(n0 + c) * p.dim + t] * p.inv_ls[t] : 0.0;
+  const double yc = valid ? (double)y[n0 + c] : 0.0;
+  const int64_t plane = M_pad * nc;
+  const int lane = threadIdx.x & 31, wq = (threadIdx.x & 127) >> 5;
+  for (int r = ty; r < 32; r += 2) {
+    const int64_t i = i0 + r;
+    uint32_t q = 0;
+    if (valid && i < M) {
+      double r2 = 0.0;
+#pragma unroll
+      for (int t = 0; t < kMaxDim; ++t)
+        if (t < p.dim) {
+          const double df = zs[r][t] - xs[t];
+          r2 = fma(df, df, r2);
+        }
+      const double k = kern_from_r2(p, r2);
+      q = (uint32_t)fmin(rint(k * qscale), 16777215.0);
+    }
+    uint8_t* dst = planes + i * nc + c;
+    dst[0] = (uint8_t)(q & 255u);
+    dst[plane] = (uint8_t)((q >> 8) & 255u);
+    dst[2 * plane] = (uint8_t)(q >> 16);
+    // v partial: exact products q * y (24 + 24 bits), warp-ordered sums
+    const double s = warp_sum((double)q * yc);
+    if (lane == 0) red[r][wq] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32)
+    vpart[(int64_t)blockIdx.x * M_pad + i0 + threadIdx.x] =
+        ((red[threadIdx.x][0] + red[threadIdx.x][1]) + red[threadIdx.x][2]) + red[threadIdx.x][3];
+}
+
+__global__ void v_reduce_kernel(const double* __restrict__ vpart, int nseg, int64_t M,
+                                int64_t M_pad, double scale, double* __restrict__ v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  double s = 0.0;
+  for (int g = 0; g < nseg; ++g) s += vpart[(int64_t)g * M_pad + i];
+  v[i] += s * scale;
+}
+
+// ------------------------------------------------------------- gram_i8 --
+__device__ __forceinline__ void tile_of_unit(int u, int& ta, int& tb) {
+  int a = (int)((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
+  while ((a + 1) * (a + 2) / 2 <= u) ++a;
+  while (a * (a + 1) / 2 > u) --a;
+  ta = a;
+  tb = u - a * (a + 1) / 2;
+}
+
+__global__ void __launch_bounds__(kI8Threads, 1)
+sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, int m_pad,
+                    double scale, double* __restrict__ sig) {
+  constexpr int S = kI8Stages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * kI8StageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull_a = empty + S;      // levels 4..1 ready
+  uint64_t* acc0_free = tfull_a + 1;  // epilogue drained acc0 (level 4)
+  uint64_t* tfull_b = acc0_free + 1;  // level 0 ready
+  uint64_t* tempty = tfull_b + 1;     // all accumulators drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull_a, 1);
+    mbar_init(acc0_free, 32 * kI8EpiWarps);
+    mbar_init(tfull_b, 1);
+    mbar_init(tempty, 32 * kI8EpiWarps);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      tma_prefetch(&tm);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int ta, tb;
+        tile_of_unit(u, ta, tb);
+        for (int phase = 0; phase < 2; ++phase) {
+          for (int kb = 0; kb < nkb; ++kb) {
+            for (int pl = phase ? 0 : 2; pl >= 0; --pl) {
+              mbar_wait(&empty[s], ph ^ 1);
+              mbar_expect_tx(&full[s], kI8StageBytes);
+              uint8_t* st = smem + (size_t)s * kI8StageBytes;
+              tma_load_2d(st, &tm, &full[s], kb * kI8KB, pl * m_pad + ta * kI8Tile);
+              tma_load_2d(st + kI8TileBytes, &tm, &full[s], kb * kI8KB, pl * m_pad + tb * kI8Tile);
+              if (++s == S) {
+                s = 0;
+                ph ^= 1;
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_u8_s32(kI8Tile, kI8Tile);
+      const uint32_t acc0 = tmem, acc1 = tmem + 128, acc2 = tmem + 256, acc3 = tmem + 384;
+      int s = 0;
+      uint32_t ph = 0;
+      auto next = [&](uint32_t& a, uint32_t& b) {
+        mbar_wait(&full[s], ph);
+        a = smem_u32(smem + (size_t)s * kI8StageBytes);
+        b = a + kI8TileBytes;
+        const int cur = s;
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+        return cur;
+      };
+      int i = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+        mbar_wait(tempty, (i & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb) {
+          uint32_t a2, b2, a1, b1, a0, b0;
+          const int s2 = next(a2, b2), s1 = next(a1, b1), s0 = next(a0, b0);
+          tc_fence_after();
+#pragma unroll
+          for (int ks = 0; ks < kI8KB / 32; ++ks) {
+            const uint32_t o = ks * 32;
+            const uint32_t acc = (kb | ks) ? 1u : 0u;
+            mma_i8(acc0, desc_k_sw64(a2 + o), desc_k_sw64(b2 + o), idesc, acc);
+            mma_i8(acc1, desc_k_sw64(a2 + o), desc_k_sw64(b1 + o), idesc, acc);
+            mma_i8(acc1, desc_k_sw64(a1 + o), desc_k_sw64(b2 + o), idesc, 1);
+            mma_i8(acc2, desc_k_sw64(a2 + o), desc_k_sw64(b0 + o), idesc, acc);
+            mma_i8(acc2, desc_k_sw64(a1 + o), desc_k_sw64(b1 + o), idesc, 1);
+            mma_i8(acc2, desc_k_sw64(a0 + o), desc_k_sw64(b2 + o), idesc, 1);
+            mma_i8(acc3, desc_k_sw64(a1 + o), desc_k_sw64(b0 + o), idesc, acc);
+            mma_i8(acc3, desc_k_sw64(a0 + o), desc_k_sw64(b1 + o), idesc, 1);
+          }
+          mma_commit(&empty[s2]);
+          mma_commit(&empty[s1]);
+          mma_commit(&empty[s0]);
+        }
+        mma_commit(tfull_a);
+        mbar_wait(acc0_free, i & 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb) {
+          uint32_t a0, b0;
+          const int s0 = next(a0, b0);
+          tc_fence_after();
+#pragma unroll
+          for (int ks = 0; ks < kI8KB / 32; ++ks)
+            mma_i8(acc0, desc_k_sw64(a0 + ks * 32), desc_k_sw64(b0 + ks * 32), idesc,
+                   (kb | ks) ? 1u : 0u);
+          mma_commit(&empty[s0]);
+        }
+        mma_commit(tfull_b);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int ew = warp - 2;
+    const int quad = warp & 3;          // TMEM lane quadrant this warp may read
+    const int half = ew >> 2;           // 64-column half of the tile
+    const int row = quad * 32 + lane;
+    const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + half * 64;
+    int i = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      double P[64];
+      uint32_t r[32];
+      mbar_wait(tfull_a, i & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        tmem_ld32(tbase + h * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) P[h * 32 + j] = (double)(int)r[j];
+      }
+      tc_fence_before();
+      mbar_arrive(acc0_free);
+#pragma unroll
+      for (int a = 1; a < 4; ++a) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          tmem_ld32(tbase + a * 128 + h * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) P[h * 32 + j] = fma(P[h * 32 + j], 256.0, (double)(int)r[j]);
+        }
+      }
+      mbar_wait(tfull_b, i & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        tmem_ld32(tbase + h * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) P[h * 32 + j] = fma(P[h * 32 + j], 256.0, (double)(int)r[j]);
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+      // column-major tile: lanes (consecutive rows) hit consecutive doubles
+      double* t = sig + (int64_t)u * (kI8Tile * kI8Tile) + (int64_t)(half * 64) * kI8Tile + row;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) t[j * kI8Tile] += P[j] * scale;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// ------------------------------------------------------------ unpack --
+// full[r, c] (M x M, symmetric) from the packed lower tiles.
+__global__ void sigma_unpack_kernel(const double* __restrict__ tiles, int64_t M,
+                                    double* __restrict__ full) {
+  const int64_t r = (int64_t)blockIdx.y * 32 + threadIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  if (r >= M || c >= M) return;
+  const int64_t lo = r >= c ? r : c, hi = r >= c ? c : r;   // (row, col) in the lower half
+  const int64_t ta = lo / kI8Tile, tb = hi / kI8Tile;
+  const int64_t u = ta * (ta + 1) / 2 + tb;
+  full[r * M + c] = tiles[u * (kI8Tile * kI8Tile) + (hi % kI8Tile) * kI8Tile + (lo % kI8Tile)];
+}
+
+// --------------------------------------------------------------- host --
+static int make_plane_map(CUtensorMap* map, const uint8_t* base, int64_t M_pad, int64_t nc) {
+  auto fn = tensor_map_encoder();
+  if (!fn) return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)nc, (cuuint64_t)(3 * M_pad)};
+  cuuint64_t strides[1] = {(cuuint64_t)nc};
+  cuuint32_t box[2] = {(cuuint32_t)kI8KB, (cuuint32_t)kI8Tile};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled (u8 planes) failed: " + std::to_string((int)r));
+  return TB_OK;
+}
+
+int i8_stats_chunk(const void* X, const void* y, const void* Z, int dtype, int64_t n0,
+                   int64_t cur, int64_t N, int64_t M, int64_t M_pad, int64_t nc,
+                   const KernParams& kp, uint8_t* planes, double* vpart, double* Sigma_tiles,
+                   double* v, cudaStream_t st) {
+  (void)N;
+  const int64_t ncur = round_up(cur, 128);           // columns written this chunk
+  const double qscale = std::ldexp(1.0, kI8FracBits) / kp.variance;
+  dim3 g((unsigned)(ncur / 128), (unsigned)(M_pad / 32));
+  if (dtype == TB_F32)
+    kuf_quant_kernel<float><<<g, 256, 0, st>>>((const float*)X, (const float*)y,
+                                               (const float*)Z, n0, cur, M, M_pad, nc, kp,
+                                               qscale, planes, vpart);
+  else
+    kuf_quant_kernel<double><<<g, 256, 0, st>>>((const double*)X, (const double*)y,
+                                                (const double*)Z, n0, cur, M, M_pad, nc, kp,
+                                                qscale, planes, vpart);
+  TB_LAUNCH_CHECK("kuf_quant");
+  v_reduce_kernel<<<(unsigned)ceil_div(M, 256), 256, 0, st>>>(
+      vpart, (int)(ncur / 128), M, M_pad, kp.variance * std::ldexp(1.0, -kI8FracBits), v);
+  TB_LAUNCH_CHECK("v_reduce");
+  CUtensorMap tm;
+  int rc = make_plane_map(&tm, planes, M_pad, nc);
+  if (rc) return rc;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int units = (int)i8_tiles(M_pad);
+  const int nkb = (int)ceil_div(cur, kI8KB);
+  static bool attr = false;
+  if (!attr) {
+    TB_CUDA_TRY(cudaFuncSetAttribute(sgpr_gram_i8_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem));
+    attr = true;
+  }
+  const double scale = kp.variance * kp.variance * std::ldexp(1.0, -2 * kI8FracBits);
+  sgpr_gram_i8_kernel<<<std::min(units, sms), kI8Threads, kI8Smem, st>>>(tm, units, nkb,
+                                                                         (int)M_pad, scale,
+                                                                         Sigma_tiles);
+  TB_LAUNCH_CHECK("sgpr_gram_i8");
+  return TB_OK;
+}
+
+int i8_unpack(const double* tiles, int64_t M, int64_t M_pad, double* full, cudaStream_t st) {
+  (void)M_pad;
+  dim3 g((unsigned)ceil_div(M, 32), (unsigned)ceil_div(M, 32));
+  sigma_unpack_kernel<<<g, dim3(32, 32), 0, st>>>(tiles, M, full);
+  TB_LAUNCH_CHECK("sigma_unpack");
+  return TB_OK;
+}
+
+}  // namespace tb

@@ -3,6 +3,7 @@
 // tcgen05 MMA / TMEM alloc / TMEM loads, and UMMA descriptors.
 #pragma once
 #include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -149,6 +150,17 @@ __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;                         // SWIZZLE_128B   [61,64)
   return d;
 }
+// K-major operand, 64-byte swizzle: rows of 64 B, 8-row atoms of 512 B
+// (start address in a 512-B aligned atom + k offset in bytes).
+__device__ __forceinline__ uint64_t desc_k_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);      // start address  [0,14)
+  d |= (uint64_t)1 << 16;                         // LBO (ignored)  [16,30)
+  d |= (uint64_t)(512 >> 4) << 32;                // SBO = 512 B    [32,46)
+  d |= (uint64_t)1 << 46;                         // version = 1    [46,48)
+  d |= (uint64_t)4 << 61;                         // SWIZZLE_64B    [61,64)
+  return d;
+}
 // K-major operand without swizzle ("interleaved"): 8-row x 16-byte core
 // matrices; lbo = byte stride between the two K core matrices of a K=16
 // step, sbo = byte stride between 8-row groups.
@@ -173,6 +185,21 @@ __host__ __device__ constexpr uint32_t idesc_u8_s32(int M, int N) {
          | (0u << 7)          // A unsigned
          | (0u << 10)         // B unsigned
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ------------------------------------------------------ host: TMA maps --
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
 }
 
 }  // namespace sm100

@@ -43,18 +43,24 @@ def _dev_tensor(a, device):
 
 
 def plan(N: int, M: int, dim: int, *, kernel: str = "rbf", dtype=np.float32,
-         memory_limit=None, resident_bytes: int | None = None) -> _lib.SgprPlan:
+         memory_limit=None, resident_bytes: int | None = None,
+         engine: str = "auto") -> _lib.SgprPlan:
     """Planner only (CPU): chunk of training points so that resident inputs +
-    Sigma/v + workspace fit ``memory_limit``."""
+    Sigma/v + workspace fit ``memory_limit``.  ``engine``: "i8" (exact Gram of
+    the 24-bit fixed-point Kuf on the INT8 tensor cores; default), "f64"
+    (fp64 DMMA) or "f64_simt" (fp64 CUDA cores)."""
     if kernel not in _lib.KERNELS:
         raise ValueError(f"kernel must be one of {tuple(_lib.KERNELS)}")
+    if engine not in _lib.SGPR_ENGINES:
+        raise ValueError(f"engine must be one of {tuple(_lib.SGPR_ENGINES)}")
     es = np.dtype(dtype).itemsize
     if resident_bytes is None:
         resident_bytes = (N * dim + N + M * dim) * es
     p = _lib.SgprPlan()
     rc = _lib.load().tb_sgpr_plan_create(N, M, dim, _lib.KERNELS[kernel],
                                          _lib.TB_F32 if np.dtype(dtype) == np.float32 else _lib.TB_F64,
-                                         as_limit(memory_limit), resident_bytes, ctypes.byref(p))
+                                         _lib.SGPR_ENGINES[engine], as_limit(memory_limit),
+                                         resident_bytes, ctypes.byref(p))
     _lib.check(rc, f"sgpr_N{N}_M{M}_d{dim}", live=resident_bytes)
     return p
 
@@ -76,11 +82,24 @@ def kernel_matrix(A, B, kind="rbf", variance=1.0, lengthscales=1.0, stream=None)
 
 @dataclass
 class SgprStats:
-    Sigma: object    # torch fp64 [M, M]
+    Sigma: object    # torch fp64, in plan.sigma_layout (full [M, M] or packed lower tiles)
     v: object        # torch fp64 [M]
     yy: float
     N: int
     plan: _lib.SgprPlan
+
+    def full_sigma(self, stream=None):
+        """Sigma as the full symmetric [M, M] fp64 matrix (tail input)."""
+        torch = _torch()
+        if self.plan.sigma_layout == _lib.TB_SIGMA_FULL:
+            return self.Sigma
+        M = self.v.numel()
+        out = torch.empty((M, M), dtype=torch.float64, device=self.Sigma.device)
+        st = stream if stream is not None else torch.cuda.current_stream(self.Sigma.device)
+        rc = _lib.load().tb_sgpr_sigma_unpack(ctypes.byref(self.plan), self.Sigma.data_ptr(),
+                                              out.data_ptr(), st.cuda_stream)
+        _lib.check(rc, "sgpr_sigma_unpack")
+        return out
 
 
 class SGPR:
@@ -94,7 +113,7 @@ class SGPR:
 
     def __init__(self, X, y, Z, kernel: str = "rbf", variance: float = 1.0,
                  lengthscales=1.0, noise_variance: float = 0.01, jitter: float = 1e-6,
-                 memory_limit=None, group=None, device=None):
+                 memory_limit=None, group=None, device=None, engine: str = "auto"):
         torch = _torch()
         if kernel not in _lib.KERNELS:
             raise ValueError(f"kernel must be one of {tuple(_lib.KERNELS)}")
@@ -119,6 +138,9 @@ class SGPR:
         self.jitter = float(jitter)
         self.memory_limit = memory_limit
         self.group = group
+        if engine not in _lib.SGPR_ENGINES:
+            raise ValueError(f"engine must be one of {tuple(_lib.SGPR_ENGINES)}")
+        self.engine = engine
         self._stats = None
         self._w = None
 
@@ -131,8 +153,10 @@ class SGPR:
         p = plan(N, M, dim, kernel=self.kernel,
                  dtype=np.float32 if self.X.dtype == torch.float32 else np.float64,
                  memory_limit=self.memory_limit,
-                 resident_bytes=(N * dim + N + M * dim) * es)
-        Sigma = torch.empty((M, M), dtype=torch.float64, device=self.device)
+                 resident_bytes=(N * dim + N + M * dim) * es, engine=self.engine)
+        Sigma = torch.empty(int(p.sigma_bytes) // 8, dtype=torch.float64, device=self.device)
+        if p.sigma_layout == _lib.TB_SIGMA_FULL:
+            Sigma = Sigma.view(M, M)
         v = torch.empty(M, dtype=torch.float64, device=self.device)
         yy = torch.empty(1, dtype=torch.float64, device=self.device)
         ws = torch.empty(max(int(p.workspace_bytes), 1), dtype=torch.uint8, device=self.device)
@@ -166,7 +190,9 @@ class SGPR:
         Kuu.diagonal().add_(self.jitter)
         L = torch.linalg.cholesky(Kuu)
         del Kuu
-        tmp = torch.linalg.solve_triangular(L, s.Sigma, upper=False)          # L^-1 Sigma
+        Sigma = s.full_sigma()
+        tmp = torch.linalg.solve_triangular(L, Sigma, upper=False)            # L^-1 Sigma
+        del Sigma
         AAT = torch.linalg.solve_triangular(L, tmp.mT, upper=False).mT          # L^-1 Sigma L^-T
         del tmp
         AAT = 0.5 * (AAT + AAT.mT) / s2
@@ -200,14 +226,16 @@ class SGPR:
 
 
 def sgpr_elbo(X, y, Z, kernel="rbf", variance=1.0, lengthscales=1.0,
-              noise_variance=0.01, *, jitter=1e-6, memory_limit=None, group=None) -> float:
+              noise_variance=0.01, *, jitter=1e-6, memory_limit=None, group=None,
+              engine="auto") -> float:
     """Titsias collapsed ELBO of GPflow 2.3.1 SGPR, on the B200 path."""
     return SGPR(X, y, Z, kernel, variance, lengthscales, noise_variance, jitter,
-                memory_limit, group).elbo()
+                memory_limit, group, engine=engine).elbo()
 
 
 def sgpr_predict_mean(Xnew, X, y, Z, kernel="rbf", variance=1.0, lengthscales=1.0,
-                      noise_variance=0.01, *, jitter=1e-6, memory_limit=None, group=None):
+                      noise_variance=0.01, *, jitter=1e-6, memory_limit=None, group=None,
+                      engine="auto"):
     m = SGPR(X, y, Z, kernel, variance, lengthscales, noise_variance, jitter,
-             memory_limit, group)
+             memory_limit, group, engine=engine)
     return m.predict_mean(Xnew)

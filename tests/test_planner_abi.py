@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts_match_c():
     assert ctypes.sizeof(_lib.KnnPlan) == 256
-    assert ctypes.sizeof(_lib.SgprPlan) == 144
+    assert ctypes.sizeof(_lib.SgprPlan) == 168
 
 
 def test_capabilities_and_error_string():
@@ -173,3 +173,41 @@ def test_estimate_peak_memory_is_planner_peak():
     assert est >= (10_000 + 1_000) * 16 * 8
     # far below the reference's naive-graph peak (it materialises [m,n,d])
     assert est < int(golden("budget.npz")["knn_c1_naive_peak"])
+
+
+def test_sgpr_planner_engines_and_c4_budget():
+    """C4 (N=2e6, d=11, M=1e4, f32, 1 GB): the fixed-point engine keeps Sigma
+    as packed lower tiles (414 MB) so a full 10880-point chunk fits; the fp64
+    engine keeps the full 800 MB Sigma and gets a much smaller chunk."""
+    from paper_2206_14148_b200 import sgpr
+    N, M, d = 2_000_000, 10_000, 11
+    resident = (N * d + N + M * d) * 4
+    p = sgpr.plan(N, M, d, kernel="rbf", memory_limit="1GB", resident_bytes=resident)
+    assert p.engine == _lib.SGPR_ENGINES["i8"] and p.sigma_layout == _lib.TB_SIGMA_TILES
+    assert p.M_pad == 10_112
+    assert p.sigma_bytes == (79 * 80 // 2) * 128 * 128 * 8
+    assert p.chunk_n == 10_880 and p.peak_bytes <= 1_000_000_000
+    f = sgpr.plan(N, M, d, kernel="rbf", memory_limit="1GB", resident_bytes=resident,
+                  engine="f64")
+    assert f.sigma_layout == _lib.TB_SIGMA_FULL and f.sigma_bytes == M * M * 8
+    assert f.chunk_n < p.chunk_n and f.peak_bytes <= 1_000_000_000
+    with pytest.raises(ValueError):
+        sgpr.plan(N, M, d, engine="tf32")
+    with pytest.raises(tb.BudgetExceeded):
+        sgpr.plan(N, M, d, memory_limit="500MB", resident_bytes=resident)
+
+
+def test_fixed24_oracle_is_a_small_perturbation():
+    """oracle.sgpr.sufficient_stats_fixed24 (the i8 engine's exact numerics)
+    vs the unquantised fp64 statistics: same ELBO to ~1e-8 on a small case."""
+    import numpy as np
+    from oracle import sgpr as osgpr
+    from paper_2206_14148_b200 import synthetic
+    X, y, Z, _ = synthetic.sgpr_data(3000, 3, 120, seed=3, dtype=np.float64)
+    S, v, yy = osgpr.sufficient_stats(X, y, Z, "matern32", 1.0, 0.6)
+    Sq, vq, yyq = osgpr.sufficient_stats_fixed24(X, y, Z, "matern32", 1.0, 0.6)
+    assert np.abs(Sq - S).max() <= 1e-7 * np.abs(S).max()
+    K = osgpr.kuu(Z, "matern32", 1.0, 0.6)
+    e, _ = osgpr.elbo_from_stats(S, v, yy, 3000, K, 0.01, 1.0)
+    eq, _ = osgpr.elbo_from_stats(Sq, vq, yyq, 3000, K, 0.01, 1.0)
+    assert abs(eq - e) <= 1e-8 * abs(e)

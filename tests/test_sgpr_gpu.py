@@ -28,17 +28,56 @@ def test_sgpr_elbo_and_mean(kind, ls, dtype):
     assert rel_err(mu, mu_ref) <= 1e-4
 
 
-@pytest.mark.parametrize("gram", ["dmma", "simt"])
-def test_sgpr_statistics_exact(gram, monkeypatch):
-    monkeypatch.setenv("TB_SGPR_GRAM", gram)
+@pytest.mark.parametrize("engine", ["f64", "f64_simt"])
+def test_sgpr_statistics_exact(engine):
     X, y, Z, _ = synthetic.sgpr_data(5000, 4, 300, seed=5, dtype=np.float64)
     S, v, yy = osgpr.sufficient_stats(X, y, Z, "rbf", 1.0, [0.7, 1.1, 0.9, 1.3])
-    m = tb.SGPR(X, y, Z, "rbf", 1.0, [0.7, 1.1, 0.9, 1.3], 0.01)
+    m = tb.SGPR(X, y, Z, "rbf", 1.0, [0.7, 1.1, 0.9, 1.3], 0.01, engine=engine)
     st = m.statistics()
     assert rel_err(st.Sigma.cpu().numpy(), S) < 1e-12
     assert rel_err(st.v.cpu().numpy(), v) < 1e-12
     assert abs(st.yy - yy) <= 1e-12 * yy
     assert np.allclose(st.Sigma.cpu().numpy(), st.Sigma.cpu().numpy().T)
+
+
+@pytest.mark.parametrize("N,M,d,kind,dtype", [(5000, 300, 4, "rbf", np.float64),
+                                              (12000, 200, 3, "matern32", np.float32),
+                                              (777, 129, 2, "rbf", np.float32)])
+def test_sgpr_i8_statistics_are_the_exact_fixed_point_gram(N, M, d, kind, dtype):
+    """The INT8 tensor-core engine returns exactly the Gram of the 24-bit
+    fixed-point Kuf (oracle.sgpr.sufficient_stats_fixed24); tolerance covers
+    fp64 level combination order and rare 1-ulp differences of exp() that
+    move one q by 1.  Also within 1e-7 of the unquantised fp64 statistics.
+    N=12000 streams two chunks (ragged last chunk); M=129 pads to 256."""
+    X, y, Z, _ = synthetic.sgpr_data(N, d, M, seed=9, dtype=dtype)
+    ls = [0.7, 1.1, 0.9, 1.3][:d]
+    Sq, vq, yy = osgpr.sufficient_stats_fixed24(X, y, Z, kind, 1.3, ls)
+    S, v, _ = osgpr.sufficient_stats(X, y, Z, kind, 1.3, ls)
+    m = tb.SGPR(X, y, Z, kind, 1.3, ls, 0.01, engine="i8",
+                memory_limit=None if N != 12000 else (N * d + N + M * d) * 4 + 60_000_000)
+    st = m.statistics()
+    if N == 12000:
+        assert st.plan.chunk_n < N
+    Sg = st.full_sigma().cpu().numpy()
+    assert np.array_equal(Sg, Sg.T)
+    assert rel_err(Sg, Sq) < 1e-11
+    assert rel_err(st.v.cpu().numpy(), vq) < 1e-11
+    assert rel_err(Sg, S) < 1e-7
+    assert rel_err(st.v.cpu().numpy(), v) < 1e-7
+    assert abs(st.yy - yy) <= 1e-12 * yy
+
+
+@pytest.mark.parametrize("engine", ["i8", "f64"])
+def test_sgpr_engines_agree_ill_conditioned(engine):
+    """Matern-3/2, l = 0.5, dense inducing set (cond(Kuu) ~ 1e5+): the
+    regime where fp32-class Gram schemes fail."""
+    X, y, Z, Xs = synthetic.sgpr_data(20000, 3, 1500, seed=11, n_test=300, dtype=np.float32)
+    ref, w = osgpr.elbo(X, y, Z, "matern32", 1.0, 0.5, 0.01)
+    mu_ref = osgpr.predict_mean(Xs, Z, w, "matern32", 1.0, 0.5)
+    m = tb.SGPR(X, y, Z, "matern32", 1.0, 0.5, 0.01, engine=engine)
+    e = m.elbo()
+    assert abs(e - ref) <= 1e-4 * abs(ref), (e, ref)
+    assert rel_err(m.predict_mean(Xs), mu_ref) <= 1e-4
 
 
 def test_sgpr_chunking_under_memory_limit():
