@@ -23,7 +23,9 @@
 //   gram_i8     persistent, one CTA per SM, units = lower 128x128 Sigma tiles.
 //     warp 0    TMA producer: per 64-point k-block the plane tiles
 //               (A_p rows of tile a, B_p rows of tile b), 64-B swizzle,
-//               through a 12-stage mbarrier ring (16 KB per stage);
+//               through a 4-stage mbarrier ring (48 KB per stage: one
+//               phase-A k-block, or plane 0 of three k-blocks in phase B);
+//               Units are ordered in 12x12 super-blocks of tiles (L2 reuse);
 //     warp 1    TMEM (512 columns = 4 accumulators x 128) + MMA issuer:
 //               phase A: levels 4..1 (8 products per k-block):
 //                 acc0 = A2B2, acc1 = A2B1 + A1B2, acc2 = A2B0 + A1B1 + A0B2,
@@ -38,6 +40,7 @@
 // 10880-point chunk fits the 1 GB budget of C4.  tb_sgpr_sigma_unpack
 // expands it for the O(M^3) tail.
 #include <cmath>
+#include <cstdlib>
 
 #include "sgpr_internal.h"
 #include "sm100.cuh"
@@ -45,22 +48,22 @@
 namespace tb {
 using namespace sm100;
 
-constexpr int kI8Stages = 12;
+constexpr int kI8Stages = 4;
 constexpr uint32_t kI8TileBytes = kI8Tile * kI8KB;        // 8 KB
-constexpr uint32_t kI8StageBytes = 2 * kI8TileBytes;      // A + B
+constexpr uint32_t kI8StageBytes = 6 * kI8TileBytes;      // 3 x (A + B) = 48 KB
 constexpr int kI8EpiWarps = 8;
 constexpr int kI8Threads = 64 + 32 * kI8EpiWarps;
-constexpr size_t kI8Smem = 1024 + (size_t)kI8Stages * kI8StageBytes + 256;
+constexpr size_t kI8Smem = 1024 + (size_t)kI8Stages * kI8StageBytes + 512;   // + barriers
 
 // ------------------------------------------------------------ kuf_quant --
 // Block: 32 inducing rows x 128 points (256 threads: 128 points x 2 row
 // groups of 16).  Each thread keeps its scaled x in fp64 registers.
-template <typename T>
+template <typename T, int DMAX>
 __global__ void __launch_bounds__(256)
 kuf_quant_kernel(const T* __restrict__ X, const T* __restrict__ y, const T* __restrict__ Z,
                  int64_t n0, int64_t cur, int64_t M, int64_t M_pad, int64_t nc, KernParams p,
                  double qscale, uint8_t* __restrict__ planes, double* __restrict__ vpart) {
-  __shared__ double zs[32][kMaxDim + 1];
+  __shared__ double zs[32][DMAX + 1];
   __shared__ double red[32][4];
   const int i0 = blockIdx.y * 32;
   const int64_t c = (int64_t)blockIdx.x * 128 + (threadIdx.x & 127);
@@ -71,9 +74,9 @@ kuf_quant_kernel(const T* __restrict__ X, const T* __restrict__ y, const T* __re
   }
   __syncthreads();
   const bool valid = c < cur;
-  double xs[kMaxDim];
+  double xs[DMAX];
 #pragma unroll
-  for (int t = 0; t < kMaxDim; ++t)
+  for (int t = 0; t < DMAX; ++t)
     if (t < p.dim) xs[t] = valid ? (double)X[(n0 + c) * p.dim + t] * p.inv_ls[t] : 0.0;
   const double yc = valid ? (double)y[n0 + c] : 0.0;
   const int64_t plane = M_pad * nc;
@@ -84,7 +87,7 @@ kuf_quant_kernel(const T* __restrict__ X, const T* __restrict__ y, const T* __re
     if (valid && i < M) {
       double r2 = 0.0;
 #pragma unroll
-      for (int t = 0; t < kMaxDim; ++t)
+      for (int t = 0; t < DMAX; ++t)
         if (t < p.dim) {
           const double df = zs[r][t] - xs[t];
           r2 = fma(df, df, r2);
@@ -116,17 +119,49 @@ __global__ void v_reduce_kernel(const double* __restrict__ vpart, int nseg, int6
 }
 
 // ------------------------------------------------------------- gram_i8 --
-__device__ __forceinline__ void tile_of_unit(int u, int& ta, int& tb) {
-  int a = (int)((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
+__device__ __forceinline__ void tri_of(int u, int& a, int& b) {
+  a = (int)((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
   while ((a + 1) * (a + 2) / 2 <= u) ++a;
   while (a * (a + 1) / 2 > u) --a;
-  ta = a;
-  tb = u - a * (a + 1) / 2;
+  b = u - a * (a + 1) / 2;
+}
+// Unit u -> lower tile (ta, tb).  Units are grouped in 12 x 12 super-blocks
+// of tiles (lower ones, row-major), so the ~148 units running at once touch
+// ~24 row blocks of the chunk instead of up to nt + 2: far fewer L2 misses
+// (each wave re-streams every row block it touches).
+constexpr int kI8SuperBlock = 12;
+__device__ __forceinline__ void tile_of_unit(int u, int nt, int& ta, int& tb) {
+  const int nsb = (nt + kI8SuperBlock - 1) / kI8SuperBlock;
+  for (int I = 0; I < nsb; ++I) {
+    const int r0 = I * kI8SuperBlock, r1 = min(nt, r0 + kI8SuperBlock);
+    for (int J = 0; J <= I; ++J) {
+      const int c0 = J * kI8SuperBlock, c1 = min(nt, c0 + kI8SuperBlock);
+      const int cnt = I > J ? (r1 - r0) * (c1 - c0) : (r1 - r0) * (r1 - r0 + 1) / 2;
+      if (u < cnt) {
+        if (I > J) {
+          ta = r0 + u / (c1 - c0);
+          tb = c0 + u % (c1 - c0);
+        } else {
+          int a, b;
+          tri_of(u, a, b);
+          ta = r0 + a;
+          tb = c0 + b;
+        }
+        return;
+      }
+      u -= cnt;
+    }
+  }
+  ta = tb = 0;
 }
 
 __global__ void __launch_bounds__(kI8Threads, 1)
 sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, int m_pad,
-                    double scale, double* __restrict__ sig) {
+                    double scale, double* __restrict__ sig, int dbg) {
+  // dbg (TB_I8_DEBUG, A/B timing only): 1 = producer skips the TMA loads
+  // (MMA-issue bound), 2 = issuer skips the MMAs (TMA-feed bound);
+  // results are garbage in both modes
+  const int nt = m_pad / kI8Tile;
   constexpr int S = kI8Stages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -158,25 +193,44 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
+    // phase A stage = one k-block, tiles [A2 B2 A1 B1 A0 B0];
+    // phase B stage = plane 0 of up to 3 k-blocks, tiles [A0 B0] x 3
     if (lane == 0) {
       tma_prefetch(&tm);
       int s = 0;
       uint32_t ph = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int ta, tb;
-        tile_of_unit(u, ta, tb);
+        tile_of_unit(u, nt, ta, tb);
+        const int ra = ta * kI8Tile, rb = tb * kI8Tile;
         for (int phase = 0; phase < 2; ++phase) {
-          for (int kb = 0; kb < nkb; ++kb) {
-            for (int pl = phase ? 0 : 2; pl >= 0; --pl) {
-              mbar_wait(&empty[s], ph ^ 1);
-              mbar_expect_tx(&full[s], kI8StageBytes);
+          const int step = phase ? 3 : 1;
+          for (int kb = 0; kb < nkb; kb += step) {
+            mbar_wait(&empty[s], ph ^ 1);
+            if (dbg == 1) {
+              mbar_arrive(&full[s]);
+            } else {
               uint8_t* st = smem + (size_t)s * kI8StageBytes;
-              tma_load_2d(st, &tm, &full[s], kb * kI8KB, pl * m_pad + ta * kI8Tile);
-              tma_load_2d(st + kI8TileBytes, &tm, &full[s], kb * kI8KB, pl * m_pad + tb * kI8Tile);
-              if (++s == S) {
-                s = 0;
-                ph ^= 1;
+              if (phase == 0) {
+                mbar_expect_tx(&full[s], kI8StageBytes);
+                for (int pl = 2; pl >= 0; --pl) {
+                  uint8_t* t = st + (2 - pl) * 2 * kI8TileBytes;
+                  tma_load_2d(t, &tm, &full[s], kb * kI8KB, pl * m_pad + ra);
+                  tma_load_2d(t + kI8TileBytes, &tm, &full[s], kb * kI8KB, pl * m_pad + rb);
+                }
+              } else {
+                const int nk = min(3, nkb - kb);
+                mbar_expect_tx(&full[s], nk * 2 * kI8TileBytes);
+                for (int j = 0; j < nk; ++j) {
+                  uint8_t* t = st + j * 2 * kI8TileBytes;
+                  tma_load_2d(t, &tm, &full[s], (kb + j) * kI8KB, ra);
+                  tma_load_2d(t + kI8TileBytes, &tm, &full[s], (kb + j) * kI8KB, rb);
+                }
               }
+            }
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
             }
           }
         }
@@ -184,59 +238,74 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
+    // The issuing thread is the bottleneck of this kernel (a UTCIMMA issue
+    // costs about one MMA time, and every barrier wait + commit ~70 cycles
+    // on top), so: descriptors are precomputed (one 64-bit add per MMA) and
+    // each barrier handshake covers 16 MMAs (phase A) or 6 (phase B).
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_u8_s32(kI8Tile, kI8Tile);
       const uint32_t acc0 = tmem, acc1 = tmem + 128, acc2 = tmem + 256, acc3 = tmem + 384;
+      // UMMA descriptor of stage s, tile j: d0 + s * kStageD + j * kTileD
+      // (16-byte units); the second K=32 step of a 64-byte row is +2
+      const uint64_t d0 = desc_k_sw64(smem_u32(smem));
+      constexpr uint64_t kStageD = kI8StageBytes >> 4, kTileD = kI8TileBytes >> 4;
       int s = 0;
       uint32_t ph = 0;
-      auto next = [&](uint32_t& a, uint32_t& b) {
-        mbar_wait(&full[s], ph);
-        a = smem_u32(smem + (size_t)s * kI8StageBytes);
-        b = a + kI8TileBytes;
-        const int cur = s;
-        if (++s == S) {
-          s = 0;
-          ph ^= 1;
-        }
-        return cur;
-      };
       int i = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
         mbar_wait(tempty, (i & 1) ^ 1);
         tc_fence_after();
         for (int kb = 0; kb < nkb; ++kb) {
-          uint32_t a2, b2, a1, b1, a0, b0;
-          const int s2 = next(a2, b2), s1 = next(a1, b1), s0 = next(a0, b0);
+          mbar_wait(&full[s], ph);
           tc_fence_after();
-#pragma unroll
-          for (int ks = 0; ks < kI8KB / 32; ++ks) {
-            const uint32_t o = ks * 32;
-            const uint32_t acc = (kb | ks) ? 1u : 0u;
-            mma_i8(acc0, desc_k_sw64(a2 + o), desc_k_sw64(b2 + o), idesc, acc);
-            mma_i8(acc1, desc_k_sw64(a2 + o), desc_k_sw64(b1 + o), idesc, acc);
-            mma_i8(acc1, desc_k_sw64(a1 + o), desc_k_sw64(b2 + o), idesc, 1);
-            mma_i8(acc2, desc_k_sw64(a2 + o), desc_k_sw64(b0 + o), idesc, acc);
-            mma_i8(acc2, desc_k_sw64(a1 + o), desc_k_sw64(b1 + o), idesc, 1);
-            mma_i8(acc2, desc_k_sw64(a0 + o), desc_k_sw64(b2 + o), idesc, 1);
-            mma_i8(acc3, desc_k_sw64(a1 + o), desc_k_sw64(b0 + o), idesc, acc);
-            mma_i8(acc3, desc_k_sw64(a0 + o), desc_k_sw64(b1 + o), idesc, 1);
+          const uint64_t a2 = d0 + (uint64_t)s * kStageD, b2 = a2 + kTileD;
+          const uint64_t a1 = a2 + 2 * kTileD, b1 = a2 + 3 * kTileD;
+          const uint64_t a0 = a2 + 4 * kTileD, b0 = a2 + 5 * kTileD;
+          if (dbg != 2) {
+            const uint32_t acc = kb ? 1u : 0u;
+            mma_i8(acc0, a2, b2, idesc, acc);
+            mma_i8(acc1, a2, b1, idesc, acc);
+            mma_i8(acc1, a1, b2, idesc, 1);
+            mma_i8(acc2, a2, b0, idesc, acc);
+            mma_i8(acc2, a1, b1, idesc, 1);
+            mma_i8(acc2, a0, b2, idesc, 1);
+            mma_i8(acc3, a1, b0, idesc, acc);
+            mma_i8(acc3, a0, b1, idesc, 1);
+            mma_i8(acc0, a2 + 2, b2 + 2, idesc, 1);
+            mma_i8(acc1, a2 + 2, b1 + 2, idesc, 1);
+            mma_i8(acc1, a1 + 2, b2 + 2, idesc, 1);
+            mma_i8(acc2, a2 + 2, b0 + 2, idesc, 1);
+            mma_i8(acc2, a1 + 2, b1 + 2, idesc, 1);
+            mma_i8(acc2, a0 + 2, b2 + 2, idesc, 1);
+            mma_i8(acc3, a1 + 2, b0 + 2, idesc, 1);
+            mma_i8(acc3, a0 + 2, b1 + 2, idesc, 1);
           }
-          mma_commit(&empty[s2]);
-          mma_commit(&empty[s1]);
-          mma_commit(&empty[s0]);
+          mma_commit(&empty[s]);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         mma_commit(tfull_a);
         mbar_wait(acc0_free, i & 1);
         tc_fence_after();
-        for (int kb = 0; kb < nkb; ++kb) {
-          uint32_t a0, b0;
-          const int s0 = next(a0, b0);
+        for (int kb = 0; kb < nkb; kb += 3) {
+          mbar_wait(&full[s], ph);
           tc_fence_after();
-#pragma unroll
-          for (int ks = 0; ks < kI8KB / 32; ++ks)
-            mma_i8(acc0, desc_k_sw64(a0 + ks * 32), desc_k_sw64(b0 + ks * 32), idesc,
-                   (kb | ks) ? 1u : 0u);
-          mma_commit(&empty[s0]);
+          const uint64_t a = d0 + (uint64_t)s * kStageD;
+          const int nk = min(3, nkb - kb);
+          if (dbg != 2) {
+            for (int j = 0; j < nk; ++j) {
+              const uint64_t aj = a + 2 * j * kTileD, bj = aj + kTileD;
+              mma_i8(acc0, aj, bj, idesc, (kb | j) ? 1u : 0u);
+              mma_i8(acc0, aj + 2, bj + 2, idesc, 1);
+            }
+          }
+          mma_commit(&empty[s]);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         mma_commit(tfull_b);
       }
@@ -252,7 +321,7 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
       double P[64];
       uint32_t r[32];
-      mbar_wait(tfull_a, i & 1);
+      mbar_wait_sleep(tfull_a, i & 1, 256);
       tc_fence_after();
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -273,7 +342,7 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
           for (int j = 0; j < 32; ++j) P[h * 32 + j] = fma(P[h * 32 + j], 256.0, (double)(int)r[j]);
         }
       }
-      mbar_wait(tfull_b, i & 1);
+      mbar_wait_sleep(tfull_b, i & 1, 256);
       tc_fence_after();
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -285,7 +354,10 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
       tc_fence_before();
       mbar_arrive(tempty);
       // column-major tile: lanes (consecutive rows) hit consecutive doubles
-      double* t = sig + (int64_t)u * (kI8Tile * kI8Tile) + (int64_t)(half * 64) * kI8Tile + row;
+      int ta, tb;
+      tile_of_unit(u, nt, ta, tb);
+      const int64_t slot = (int64_t)ta * (ta + 1) / 2 + tb;
+      double* t = sig + slot * (kI8Tile * kI8Tile) + (int64_t)(half * 64) * kI8Tile + row;
 #pragma unroll
       for (int j = 0; j < 64; ++j) t[j * kI8Tile] += P[j] * scale;
     }
@@ -333,14 +405,22 @@ int i8_stats_chunk(const void* X, const void* y, const void* Z, int dtype, int64
   const int64_t ncur = round_up(cur, 128);           // columns written this chunk
   const double qscale = std::ldexp(1.0, kI8FracBits) / kp.variance;
   dim3 g((unsigned)(ncur / 128), (unsigned)(M_pad / 32));
-  if (dtype == TB_F32)
-    kuf_quant_kernel<float><<<g, 256, 0, st>>>((const float*)X, (const float*)y,
-                                               (const float*)Z, n0, cur, M, M_pad, nc, kp,
-                                               qscale, planes, vpart);
-  else
-    kuf_quant_kernel<double><<<g, 256, 0, st>>>((const double*)X, (const double*)y,
-                                                (const double*)Z, n0, cur, M, M_pad, nc, kp,
-                                                qscale, planes, vpart);
+#define TB_KQ(T, D)                                                                      \
+  kuf_quant_kernel<T, D><<<g, 256, 0, st>>>((const T*)X, (const T*)y, (const T*)Z, n0, cur, M, \
+                                            M_pad, nc, kp, qscale, planes, vpart)
+#define TB_KQ_DIM(T)                   \
+  if (kp.dim <= 4) TB_KQ(T, 4);        \
+  else if (kp.dim <= 8) TB_KQ(T, 8);   \
+  else if (kp.dim <= 16) TB_KQ(T, 16); \
+  else if (kp.dim <= 32) TB_KQ(T, 32); \
+  else TB_KQ(T, 64)
+  if (dtype == TB_F32) {
+    TB_KQ_DIM(float);
+  } else {
+    TB_KQ_DIM(double);
+  }
+#undef TB_KQ_DIM
+#undef TB_KQ
   TB_LAUNCH_CHECK("kuf_quant");
   v_reduce_kernel<<<(unsigned)ceil_div(M, 256), 256, 0, st>>>(
       vpart, (int)(ncur / 128), M, M_pad, kp.variance * std::ldexp(1.0, -kI8FracBits), v);
@@ -360,9 +440,11 @@ int i8_stats_chunk(const void* X, const void* y, const void* Z, int dtype, int64
     attr = true;
   }
   const double scale = kp.variance * kp.variance * std::ldexp(1.0, -2 * kI8FracBits);
+  const char* dbg_env = std::getenv("TB_I8_DEBUG");
+  const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   sgpr_gram_i8_kernel<<<std::min(units, sms), kI8Threads, kI8Smem, st>>>(tm, units, nkb,
                                                                          (int)M_pad, scale,
-                                                                         Sigma_tiles);
+                                                                         Sigma_tiles, dbg);
   TB_LAUNCH_CHECK("sgpr_gram_i8");
   return TB_OK;
 }
