@@ -96,6 +96,16 @@ __global__ void sumsq_kernel(const T* __restrict__ y, int64_t n0, int64_t n1,
   }
 }
 
+static int launch_sumsq(const void* y, int dtype, int64_t n0, int64_t n1, double* yy,
+                        cudaStream_t st) {
+  if (dtype == TB_F32)
+    sumsq_kernel<float><<<1, 1024, 0, st>>>((const float*)y, n0, n1, yy);
+  else
+    sumsq_kernel<double><<<1, 1024, 0, st>>>((const double*)y, n0, n1, yy);
+  TB_LAUNCH_CHECK("sumsq");
+  return TB_OK;
+}
+
 // ---------------------------------------------------------------- syrk --
 // Sigma[a, b] += sum_n K[a, n] K[b, n] on lower tile pairs (ta >= tb).
 // 256 threads, 8x8 fp64 micro-tile per thread over a 128x128 tile.
@@ -369,28 +379,53 @@ int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel, int32
   plan->sigma_bytes = i8 ? i8_tiles(M_pad) * kI8Tile * kI8Tile * 8 : M * M * 8;
   plan->output_bytes = plan->sigma_bytes + M * 8 + 8;
   const int64_t limit = memory_limit > 0 ? memory_limit : INT64_MAX;
-  // chunk of training points: as large as the budget allows (amortises the
-  // per-chunk Sigma tile read-modify-write); fp64 engines cap at 8192, the
-  // fixed-point engine at kI8MaxChunk (s32 accumulator range)
-  int64_t nc = i8 ? std::min<int64_t>(kI8MaxChunk, round_up(N, 128))
-                  : std::min<int64_t>(8192, round_up(N, 128));
+  const int64_t fixed = resident_bytes + plan->output_bytes;
+  auto budget_fail = [&](int64_t ws) {
+    return fail(TB_ERR_BUDGET, "sgpr: allocating " + std::to_string(plan->output_bytes + ws) +
+                                   " bytes would exceed the budget (live=" +
+                                   std::to_string(resident_bytes) + ", limit=" +
+                                   std::to_string(memory_limit) + ")");
+  };
+  if (i8) {
+    // chunk buffer = 3 digit planes + v partials; two buffers let chunk c+1's
+    // Kuf generation overlap chunk c's Gram.  Largest chunk (multiple of 128,
+    // <= kI8MaxChunk: s32 range) that fits, double-buffered unless that
+    // would more than halve the chunk.
+    auto buf_bytes = [&](int64_t nc) {
+      return round_up(i8_planes_bytes(M_pad, nc), 256) + round_up(i8_vpart_bytes(M_pad, nc), 256);
+    };
+    const int64_t cap = std::min<int64_t>(kI8MaxChunk, round_up(N, 128));
+    auto largest = [&](int nbuf) -> int64_t {
+      for (int64_t nc = cap; nc >= 128; nc -= 128)
+        if (fixed + nbuf * buf_bytes(nc) <= limit) return nc;
+      return 0;
+    };
+    const int64_t n1 = largest(1), n2 = N > cap ? largest(2) : 0;
+    if (!n1) return budget_fail(buf_bytes(128));
+    const int nbuf = (n2 && 2 * n2 >= n1) ? 2 : 1;
+    const int64_t nc = nbuf == 2 ? n2 : n1;
+    plan->chunk_n = nc;
+    plan->off[0] = 0;
+    plan->off[1] = round_up(i8_planes_bytes(M_pad, nc), 256);
+    plan->off[2] = nbuf == 2 ? buf_bytes(nc) : 0;
+    plan->off[3] = plan->off[2] + plan->off[1];
+    plan->off[4] = nbuf;
+    plan->workspace_bytes = nbuf * buf_bytes(nc);
+    plan->peak_bytes = fixed + plan->workspace_bytes;
+    return TB_OK;
+  }
+  // fp64 engines: one fp64 Kuf chunk [M_pad, nc]; as large as the budget
+  // allows (amortises the per-chunk Sigma tile read-modify-write), <= 8192
+  int64_t nc = std::min<int64_t>(8192, round_up(N, 128));
   for (;;) {
-    const int64_t ws = i8 ? round_up(i8_planes_bytes(M_pad, nc), 256) +
-                                round_up(i8_vpart_bytes(M_pad, nc), 256)
-                          : round_up(M_pad * nc * 8, 256);
-    if (resident_bytes + plan->output_bytes + ws <= limit) {
+    const int64_t ws = round_up(M_pad * nc * 8, 256);
+    if (fixed + ws <= limit) {
       plan->chunk_n = nc;
       plan->workspace_bytes = ws;
-      plan->peak_bytes = resident_bytes + plan->output_bytes + ws;
-      plan->off[0] = 0;
-      plan->off[1] = i8 ? round_up(i8_planes_bytes(M_pad, nc), 256) : 0;   // vpart
+      plan->peak_bytes = fixed + ws;
       return TB_OK;
     }
-    if (nc <= 128)
-      return fail(TB_ERR_BUDGET, "sgpr: allocating " + std::to_string(plan->output_bytes + ws) +
-                                     " bytes would exceed the budget (live=" +
-                                     std::to_string(resident_bytes) + ", limit=" +
-                                     std::to_string(memory_limit) + ")");
+    if (nc <= 128) return budget_fail(ws);
     nc = std::max<int64_t>(128, round_up(nc / 2, 128));
   }
 }
@@ -418,20 +453,44 @@ int tb_sgpr_stats_run(const tb_sgpr_plan* p, const void* X, const void* y, const
     TB_CUDA_TRY(cudaMemsetAsync(yy, 0, 8, st));
   }
   if (p->engine == TB_SGPR_ENGINE_I8) {
-    uint8_t* planes = (uint8_t*)workspace + p->off[0];
-    double* vpart = (double*)((uint8_t*)workspace + p->off[1]);
-    for (int64_t n0 = 0; n0 < N; n0 += nc) {
-      const int64_t cur = std::min(nc, N - n0);
-      rc = i8_stats_chunk(X, y, Z, p->dtype, n0, cur, N, M, M_pad, nc, kp, planes, vpart,
-                          Sigma, v, st);
-      if (rc) return rc;
-      if (p->dtype == TB_F32)
-        sumsq_kernel<float><<<1, 1024, 0, st>>>((const float*)y, n0, n0 + cur, yy);
-      else
-        sumsq_kernel<double><<<1, 1024, 0, st>>>((const double*)y, n0, n0 + cur, yy);
-      TB_LAUNCH_CHECK("sumsq");
+    // Two chunk buffers: chunk c+1's Kuf generation (fp64 CUDA cores, side
+    // stream) runs while chunk c's Gram (INT8 tensor cores) runs on `st`.
+    const int nbuf = (int)p->off[4];
+    uint8_t* planes[2] = {(uint8_t*)workspace + p->off[0], (uint8_t*)workspace + p->off[2]};
+    double* vpart[2] = {(double*)((uint8_t*)workspace + p->off[1]),
+                        (double*)((uint8_t*)workspace + p->off[3])};
+    cudaStream_t gen = st;
+    cudaEvent_t ev[5] = {};   // start, gen done (buf 0/1), gram done (buf 0/1)
+    if (nbuf == 2) {
+      TB_CUDA_TRY(cudaStreamCreateWithFlags(&gen, cudaStreamNonBlocking));
+      for (auto& e : ev) TB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      TB_CUDA_TRY(cudaEventRecord(ev[0], st));
+      TB_CUDA_TRY(cudaStreamWaitEvent(gen, ev[0], 0));
     }
-    return TB_OK;
+    int64_t c = 0;
+    for (int64_t n0 = 0; n0 < N && rc == TB_OK; n0 += nc, ++c) {
+      const int64_t cur = std::min(nc, N - n0);
+      const int b = nbuf == 2 ? (int)(c & 1) : 0;
+      if (nbuf == 2 && c >= 2) TB_CUDA_TRY(cudaStreamWaitEvent(gen, ev[3 + b], 0));
+      rc = i8_gen_chunk(X, y, Z, p->dtype, n0, cur, M, M_pad, nc, kp, planes[b], vpart[b], v, gen);
+      if (rc) break;
+      rc = launch_sumsq(y, p->dtype, n0, n0 + cur, yy, gen);
+      if (rc) break;
+      if (nbuf == 2) {
+        TB_CUDA_TRY(cudaEventRecord(ev[1 + b], gen));
+        TB_CUDA_TRY(cudaStreamWaitEvent(st, ev[1 + b], 0));
+      }
+      rc = i8_gram_chunk(cur, M_pad, nc, kp.variance, planes[b], Sigma, st);
+      if (nbuf == 2 && rc == TB_OK) TB_CUDA_TRY(cudaEventRecord(ev[3 + b], st));
+    }
+    if (nbuf == 2) {
+      // v / yy (side stream) complete before anything later on `st`
+      cudaEventRecord(ev[0], gen);
+      cudaStreamWaitEvent(st, ev[0], 0);
+      for (auto& e : ev) cudaEventDestroy(e);
+      cudaStreamDestroy(gen);
+    }
+    return rc;
   }
   double* K = (double*)workspace;
   const int ntiles = (int)(M_pad / kSyrkTile);

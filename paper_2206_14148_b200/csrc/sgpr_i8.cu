@@ -56,10 +56,13 @@ constexpr int kI8Threads = 64 + 32 * kI8EpiWarps;
 constexpr size_t kI8Smem = 1024 + (size_t)kI8Stages * kI8StageBytes + 512;   // + barriers
 
 // ------------------------------------------------------------ kuf_quant --
-// Block: 32 inducing rows x 128 points (256 threads: 128 points x 2 row
-// groups of 16).  Each thread keeps its scaled x in fp64 registers.
+// Block: 32 inducing rows x 128 points, 128 threads (one point each, all 32
+// rows); small enough to co-reside with the persistent Gram CTA of the
+// previous chunk (which leaves ~11k registers and ~30 KB of shared memory
+// per SM), so the fp64 generation overlaps the tensor-core Gram.
+constexpr int kI8QuantThreads = 128;
 template <typename T, int DMAX>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kI8QuantThreads)
 kuf_quant_kernel(const T* __restrict__ X, const T* __restrict__ y, const T* __restrict__ Z,
                  int64_t n0, int64_t cur, int64_t M, int64_t M_pad, int64_t nc, KernParams p,
                  double qscale, uint8_t* __restrict__ planes, double* __restrict__ vpart) {
@@ -67,7 +70,6 @@ kuf_quant_kernel(const T* __restrict__ X, const T* __restrict__ y, const T* __re
   __shared__ double red[32][4];
   const int i0 = blockIdx.y * 32;
   const int64_t c = (int64_t)blockIdx.x * 128 + (threadIdx.x & 127);
-  const int ty = threadIdx.x >> 7;
   for (int e = threadIdx.x; e < 32 * p.dim; e += blockDim.x) {
     const int r = e / p.dim, t = e % p.dim;
     zs[r][t] = (i0 + r < M) ? (double)Z[(int64_t)(i0 + r) * p.dim + t] * p.inv_ls[t] : 0.0;
@@ -81,7 +83,7 @@ kuf_quant_kernel(const T* __restrict__ X, const T* __restrict__ y, const T* __re
   const double yc = valid ? (double)y[n0 + c] : 0.0;
   const int64_t plane = M_pad * nc;
   const int lane = threadIdx.x & 31, wq = (threadIdx.x & 127) >> 5;
-  for (int r = ty; r < 32; r += 2) {
+  for (int r = 0; r < 32; ++r) {
     const int64_t i = i0 + r;
     uint32_t q = 0;
     if (valid && i < M) {
@@ -397,17 +399,16 @@ static int make_plane_map(CUtensorMap* map, const uint8_t* base, int64_t M_pad, 
   return TB_OK;
 }
 
-int i8_stats_chunk(const void* X, const void* y, const void* Z, int dtype, int64_t n0,
-                   int64_t cur, int64_t N, int64_t M, int64_t M_pad, int64_t nc,
-                   const KernParams& kp, uint8_t* planes, double* vpart, double* Sigma_tiles,
-                   double* v, cudaStream_t st) {
-  (void)N;
+int i8_gen_chunk(const void* X, const void* y, const void* Z, int dtype, int64_t n0,
+                 int64_t cur, int64_t M, int64_t M_pad, int64_t nc, const KernParams& kp,
+                 uint8_t* planes, double* vpart, double* v, cudaStream_t st) {
   const int64_t ncur = round_up(cur, 128);           // columns written this chunk
   const double qscale = std::ldexp(1.0, kI8FracBits) / kp.variance;
   dim3 g((unsigned)(ncur / 128), (unsigned)(M_pad / 32));
-#define TB_KQ(T, D)                                                                      \
-  kuf_quant_kernel<T, D><<<g, 256, 0, st>>>((const T*)X, (const T*)y, (const T*)Z, n0, cur, M, \
-                                            M_pad, nc, kp, qscale, planes, vpart)
+#define TB_KQ(T, D)                                                                        \
+  kuf_quant_kernel<T, D><<<g, kI8QuantThreads, 0, st>>>((const T*)X, (const T*)y, (const T*)Z, \
+                                                        n0, cur, M, M_pad, nc, kp, qscale,    \
+                                                        planes, vpart)
 #define TB_KQ_DIM(T)                   \
   if (kp.dim <= 4) TB_KQ(T, 4);        \
   else if (kp.dim <= 8) TB_KQ(T, 8);   \
@@ -425,6 +426,11 @@ int i8_stats_chunk(const void* X, const void* y, const void* Z, int dtype, int64
   v_reduce_kernel<<<(unsigned)ceil_div(M, 256), 256, 0, st>>>(
       vpart, (int)(ncur / 128), M, M_pad, kp.variance * std::ldexp(1.0, -kI8FracBits), v);
   TB_LAUNCH_CHECK("v_reduce");
+  return TB_OK;
+}
+
+int i8_gram_chunk(int64_t cur, int64_t M_pad, int64_t nc, double variance, const uint8_t* planes,
+                  double* Sigma_tiles, cudaStream_t st) {
   CUtensorMap tm;
   int rc = make_plane_map(&tm, planes, M_pad, nc);
   if (rc) return rc;
@@ -433,13 +439,9 @@ int i8_stats_chunk(const void* X, const void* y, const void* Z, int dtype, int64
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int units = (int)i8_tiles(M_pad);
   const int nkb = (int)ceil_div(cur, kI8KB);
-  static bool attr = false;
-  if (!attr) {
-    TB_CUDA_TRY(cudaFuncSetAttribute(sgpr_gram_i8_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem));
-    attr = true;
-  }
-  const double scale = kp.variance * kp.variance * std::ldexp(1.0, -2 * kI8FracBits);
+  TB_CUDA_TRY(cudaFuncSetAttribute(sgpr_gram_i8_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem));
+  const double scale = variance * variance * std::ldexp(1.0, -2 * kI8FracBits);
   const char* dbg_env = std::getenv("TB_I8_DEBUG");
   const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
   sgpr_gram_i8_kernel<<<std::min(units, sms), kI8Threads, kI8Smem, st>>>(tm, units, nkb,

@@ -42,10 +42,13 @@ inline int64_t i8_tiles(int64_t M_pad) {
 inline int64_t i8_planes_bytes(int64_t M_pad, int64_t nc) { return 3 * M_pad * nc; }
 inline int64_t i8_vpart_bytes(int64_t M_pad, int64_t nc) { return (nc / 128) * M_pad * 8; }
 
-int i8_stats_chunk(const void* X, const void* y, const void* Z, int dtype, int64_t n0,
-                   int64_t cur, int64_t N, int64_t M, int64_t M_pad, int64_t nc,
-                   const KernParams& kp, uint8_t* planes, double* vpart, double* Sigma_tiles,
-                   double* v, cudaStream_t st);
+// Kuf chunk -> digit planes + v partials (+ v update), on `st`
+int i8_gen_chunk(const void* X, const void* y, const void* Z, int dtype, int64_t n0,
+                 int64_t cur, int64_t M, int64_t M_pad, int64_t nc, const KernParams& kp,
+                 uint8_t* planes, double* vpart, double* v, cudaStream_t st);
+// Sigma tiles += Gram of the chunk's planes, on `st`
+int i8_gram_chunk(int64_t cur, int64_t M_pad, int64_t nc, double variance, const uint8_t* planes,
+                  double* Sigma_tiles, cudaStream_t st);
 int i8_unpack(const double* tiles, int64_t M, int64_t M_pad, double* full, cudaStream_t st);
 
 }  // namespace tb

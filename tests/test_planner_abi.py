@@ -177,8 +177,9 @@ def test_estimate_peak_memory_is_planner_peak():
 
 def test_sgpr_planner_engines_and_c4_budget():
     """C4 (N=2e6, d=11, M=1e4, f32, 1 GB): the fixed-point engine keeps Sigma
-    as packed lower tiles (414 MB) so a full 10880-point chunk fits; the fp64
-    engine keeps the full 800 MB Sigma and gets a much smaller chunk."""
+    as packed lower tiles (414 MB), so two 7808-point chunk buffers fit (Kuf
+    generation of chunk c+1 overlaps the Gram of chunk c); the fp64 engine
+    keeps the full 800 MB Sigma and gets a much smaller chunk."""
     from paper_2206_14148_b200 import sgpr
     N, M, d = 2_000_000, 10_000, 11
     resident = (N * d + N + M * d) * 4
@@ -186,7 +187,11 @@ def test_sgpr_planner_engines_and_c4_budget():
     assert p.engine == _lib.SGPR_ENGINES["i8"] and p.sigma_layout == _lib.TB_SIGMA_TILES
     assert p.M_pad == 10_112
     assert p.sigma_bytes == (79 * 80 // 2) * 128 * 128 * 8
-    assert p.chunk_n == 10_880 and p.peak_bytes <= 1_000_000_000
+    assert p.off[4] == 2 and p.chunk_n == 7808 and p.peak_bytes <= 1_000_000_000
+    one = sgpr.plan(N, M, d, kernel="rbf", memory_limit="700MB", resident_bytes=resident)
+    assert one.off[4] == 1 and one.chunk_n < 7808 and one.peak_bytes <= 700_000_000
+    small = sgpr.plan(5000, 300, 4, kernel="rbf")
+    assert small.off[4] == 1 and small.chunk_n == 5120          # one chunk: no overlap
     f = sgpr.plan(N, M, d, kernel="rbf", memory_limit="1GB", resident_bytes=resident,
                   engine="f64")
     assert f.sigma_layout == _lib.TB_SIGMA_FULL and f.sigma_bytes == M * M * 8
