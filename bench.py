@@ -41,6 +41,17 @@ UNIT = "queries/s"
 WORKLOAD = "knn_c2_1e6x128_q1e4_k10_fp32_1GB"
 
 
+def _traffic(kernel: str):
+    """roofline.traffic: DRAM bytes per launch of `kernel` from the committed
+    ncu --set full capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)[kernel]
+        return t["traffic"], t["algorithmic_bytes"], t["ncu_rep"]
+    except (OSError, KeyError):
+        return None, None, None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -195,20 +206,35 @@ def run_sgpr(args, dev, world, rank, dist):
         stats_ms, total_ms = (float(v) for v in t.tolist())
     useful = SG_N * SG_M * (SG_M + 1)
     achieved = useful / (stats_ms / 1e3) / 1e12
+    # denominator: INT8 dense MMA rate = 2x bf16 on sm_100 (tcgen05 kind::i8
+    # K=32 vs kind::f16 K=16 per instruction, verified by tools/probes/
+    # mma_probe.cu) of the measured bf16 sustained figure, / 9 u8 x u8 slice
+    # products per useful MAC (exact 24-bit fixed-point Gram)
+    peaks, peak_src = _peaks()
+    peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / 9.0
+    traffic, alg_bytes, rep = _traffic("sgpr_gram_i8")
     out = {"metric": "sgpr_elbo_evals_per_s", "value": 1e3 / total_ms, "unit": "elbo_evals/s",
            "ms_per_eval": total_ms, "stats_ms": stats_ms, "tail_ms": total_ms - stats_ms,
-           "elbo": elbo, "dtype": "f32 inputs, fp64 statistics and tail",
+           "elbo": elbo, "dtype": "f32 inputs; Kuf rounded once to 24-bit fixed point, exact "
+                                   "integer Gram (u8 slices, s32 TMEM); fp64 accumulation and tail",
            "config": {"workload": "sgpr_c4_rbf_N2e6_d11_M1e4_1GB", "N": SG_N, "d": SG_D,
                       "M": SG_M, "kernel": "rbf", "lengthscale": 1.0, "noise": 0.01,
                       "memory_limit": LIMIT, "chunk_n": int(st.plan.chunk_n),
+                      "engine": "i8", "chunk_buffers": int(st.plan.off[4]),
+                      "Z": "M points drawn from the X distribution (same seed on every rank)",
                       "parallelism": f"N-shard{world}", "timed": "1 evaluation after a "
                       "small-problem warm-up (one C4 evaluation takes seconds)"},
            "peak_stats_mb": peak_stats / 1e6, "planned_peak_mb": st.plan.peak_bytes / 1e6,
-           "roofline": {"bound": "tensor", "achieved": achieved, "peak": 40.0, "unit": "TFLOP/s",
-                        "frac": achieved / 40.0, "traffic": None,
-                        "kernel": "syrk_dmma (fp64 tensor-core exact Gram)",
-                        "peak_source": "nominal B200 FP64 tensor 40 TF/s (not in "
-                                       "MEASURED_PEAKS.json)",
+           "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "frac": achieved / peak, "traffic": traffic,
+                        "traffic_note": None if traffic is None else
+                        f"DRAM bytes per 7808-point chunk launch from {rep}; algorithmic "
+                        f"{alg_bytes} B",
+                        "kernel": "sgpr_gram_i8 (exact fixed-point Gram on INT8 tcgen05) + "
+                                  "overlapped kuf_quant; time = whole statistics pass",
+                        "peak_source": f"2 x {peak_src} bf16 sustained (INT8 rate) / 9 slice "
+                                       "products per useful MAC",
+                        "frac_of_nominal": achieved / (4500.0 / 9.0),
                         "useful_flops": useful}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = sgpr_cpu_baseline(args.sgpr_cpu_n, host_cores())
@@ -337,18 +363,21 @@ def run_ours(args):
     # results copied out, every step
     e2e = None
     if not args.no_e2e and world == 1:
+        # the reference-facing call with HOST buffers (tb_knn_run_host): pinned
+        # x, q copied in (database chunk by chunk, overlapped with compute)
+        # and dist, idx copied out, every step.  Its plan caps chunks at n/4
+        # so three of the four database copies overlap compute.
         xh = x.cpu().pin_memory()
         qh = q.cpu().pin_memory()
+        op_h = neighbors.KnnOperator(rows, M_Q, DIM, K, dtype=np.float32, out_dtype=out_dtype,
+                                     engine=args.engine, memory_limit=LIMIT, device=dev,
+                                     max_chunk_rows=-(-rows // 4))
+        staging = (x, q, out[0], out[1])      # device buffers refilled every step
         dh = torch.empty(out[0].shape, dtype=out[0].dtype).pin_memory()
         ih = torch.empty(out[1].shape, dtype=out[1].dtype).pin_memory()
-        xd, qd = x, q          # the same device buffers are refilled each step
 
         def e2e_step():
-            xd.copy_(xh, non_blocking=True)
-            qd.copy_(qh, non_blocking=True)
-            d, i = op.run(xd, qd, out)
-            dh.copy_(d, non_blocking=True)
-            ih.copy_(i, non_blocking=True)
+            op_h.run_host(xh, qh, (dh, ih), staging=staging)
 
         for _ in range(max(1, args.warmup)):
             e2e_step()
@@ -365,7 +394,10 @@ def run_ours(args):
                "h2d_bytes_per_step": int(x.numel() * 4 + q.numel() * 4),
                "d2h_bytes_per_step": int(dh.numel() * dh.element_size() + ih.numel() * 8),
                "ms_per_step": ems / args.steps,
-               "path": "KnnOperator.run with pinned host x,q copied in and dist,idx copied out"}
+               "chunks": int(op_h.plan.n_chunks),
+               "path": "KnnOperator.run_host -> tb_knn_run_host: pinned host x,q in "
+                       "(per-chunk H2D overlapped with compute), dist,idx out"}
+        del op_h
 
     peaks, peak_src = _peaks()
     roof = None
@@ -375,8 +407,11 @@ def run_ours(args):
         passes = {"tc3": 3, "tc1": 1, "simt": 1}[engine]
         achieved = useful / (eng_ms / 1000.0) / 1e12
         peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / passes
+        traffic, alg_bytes, rep = _traffic("knn_tc") if engine == "tc3" else (None, None, None)
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_note": None if traffic is None else
+                f"DRAM bytes per chunk launch from {rep}; algorithmic {alg_bytes} B",
                 "kernel": f"knn candidate engine ({engine})",
                 "kernel_ms": eng_ms, "kernel_share_of_step": eng_ms / (ms / args.steps),
                 "peak_source": f"{peak_src} bf16 sustained / {passes} MMA passes per useful MAC"}

@@ -101,6 +101,14 @@ TB_API int tb_knn_plan_create(int64_t n, int64_t m, int64_t d, int64_t k, int32_
                 int64_t memory_limit, int64_t resident_bytes,
                 tb_knn_plan* plan);
 
+/* tb_knn_plan_create with an upper bound on the database rows staged per
+ * chunk (max_chunk_rows <= 0: none).  Smaller chunks let tb_knn_run_host
+ * overlap more of the host->device copy with compute. */
+TB_API int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int32_t metric,
+                int32_t dtype, int32_t out_dtype, int32_t engine,
+                int64_t memory_limit, int64_t resident_bytes,
+                int64_t max_chunk_rows, tb_knn_plan* plan);
+
 /* Replaces evaluate(knn_graph, [x, q], budget) (interpreter.py:522-551) for
  * the kNN graph family: x[n,d], q[m,d] (plan dtype) -> out_dist[m,k]
  * (plan out_dtype, squared L2 as the reference's rewritten graph computes,
@@ -118,6 +126,18 @@ TB_API int tb_knn_run_ex(const tb_knn_plan* plan, const void* x, const void* q,
                          int64_t index_base, void* out_dist, int64_t* out_idx,
                          void* workspace, int64_t workspace_bytes, void* stream,
                          void** events, int32_t n_events);
+
+/* The same call with HOST inputs/outputs (the reference's evaluate() takes
+ * host numpy arrays, interpreter.py:522-551): x_host[n,d], q_host[m,d] are
+ * copied into the caller's device buffers x_dev / q_dev (database chunk by
+ * chunk on a side stream, so chunk c+1's copy overlaps chunk c's compute),
+ * results land in dist_dev / idx_dev and are copied to dist_host /
+ * idx_host.  Host buffers should be pinned for the copies to be
+ * asynchronous.  Completes asynchronously on `stream`. */
+TB_API int tb_knn_run_host(const tb_knn_plan* plan, const void* x_host, const void* q_host,
+                           int64_t index_base, void* dist_host, int64_t* idx_host,
+                           void* x_dev, void* q_dev, void* dist_dev, int64_t* idx_dev,
+                           void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Merge L per-shard result lists (each [m,k], ascending, dtype `dtype`) into
  * the global top-k with ties -> lower global index.  No reference

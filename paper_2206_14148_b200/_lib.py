@@ -58,6 +58,10 @@ class SgprPlan(ctypes.Structure):
 _SIGS = {
     "tb_knn_plan_create": (ctypes.c_int, [_i64, _i64, _i64, _i64, _i32, _i32, _i32, _i32,
                                           _i64, _i64, ctypes.POINTER(KnnPlan)]),
+    "tb_knn_plan_create_ex": (ctypes.c_int, [_i64, _i64, _i64, _i64, _i32, _i32, _i32, _i32,
+                                             _i64, _i64, _i64, ctypes.POINTER(KnnPlan)]),
+    "tb_knn_run_host": (ctypes.c_int, [ctypes.POINTER(KnnPlan), _vp, _vp, _i64, _vp, _vp,
+                                       _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "tb_knn_run": (ctypes.c_int, [ctypes.POINTER(KnnPlan), _vp, _vp, _i64, _vp, _vp,
                                   _vp, _i64, _vp]),
     "tb_knn_run_ex": (ctypes.c_int, [ctypes.POINTER(KnnPlan), _vp, _vp, _i64, _vp, _vp,

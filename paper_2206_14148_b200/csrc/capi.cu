@@ -7,6 +7,7 @@
 #include <string>
 #include <mutex>
 #include <cstdlib>
+#include <vector>
 
 #include "tb_common.cuh"
 #include "knn_internal.h"
@@ -80,6 +81,12 @@ static bool device_is_sm100(std::string* why) {
 
 using namespace tb;
 
+// tb_knn_run_ex body; `ready[c]` (if given) gates database chunk c
+static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
+                        int64_t index_base, void* out_dist, int64_t* out_idx,
+                        void* workspace, int64_t workspace_bytes, cudaStream_t st,
+                        void** events, int32_t n_events, void** ready, int32_t n_ready);
+
 extern "C" {
 
 const char* tb_last_error(void) { return g_last_error.c_str(); }
@@ -92,6 +99,14 @@ int tb_knn_plan_create(int64_t n, int64_t m, int64_t d, int64_t k, int32_t metri
                 int32_t dtype, int32_t out_dtype, int32_t engine,
                 int64_t memory_limit, int64_t resident_bytes,
                 tb_knn_plan* plan) {
+  return tb_knn_plan_create_ex(n, m, d, k, metric, dtype, out_dtype, engine, memory_limit,
+                               resident_bytes, 0, plan);
+}
+
+int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int32_t metric,
+                          int32_t dtype, int32_t out_dtype, int32_t engine,
+                          int64_t memory_limit, int64_t resident_bytes,
+                          int64_t max_chunk_rows, tb_knn_plan* plan) {
   if (!plan) return fail(TB_ERR_ARG, "plan pointer is null");
   std::memset(plan, 0, sizeof(*plan));
   if (n < 1 || d < 1 || m < 0)
@@ -132,6 +147,8 @@ int tb_knn_plan_create(int64_t n, int64_t m, int64_t d, int64_t k, int32_t metri
   plan->m_pad = qt * 128;
   plan->d_pad = tc ? round_up(d, 64) : d;
   plan->output_bytes = m * k * (elem_size(out_dtype) + 8);
+  // what the caller's allocator charges: dist and idx are two buffers
+  const int64_t out_charged = alloc_bytes(m * k * elem_size(out_dtype)) + alloc_bytes(m * k * 8);
 
   const int tile_rows = tc ? 256 : 128;
   const int ctas_per_sm = 1;
@@ -166,25 +183,27 @@ int tb_knn_plan_create(int64_t n, int64_t m, int64_t d, int64_t k, int32_t metri
   const int64_t limit = memory_limit > 0 ? memory_limit : INT64_MAX;
   int64_t chunk = tc ? std::min<int64_t>(n, (int64_t)1 << 22) : n;
   int64_t min_chunk = std::min<int64_t>(n, tile_rows);
+  if (max_chunk_rows > 0)
+    chunk = std::max(min_chunk, std::min(chunk, round_up(max_chunk_rows, tile_rows)));
   for (;;) {
     const int64_t tiles = ceil_div(chunk, tile_rows);
     int slices = tc ? 1 : choose_slices(qt, tiles, ctas_per_sm, 512);
     int64_t ws = layout(chunk, slices);
     // shrink the candidate fan-out before the chunk if that is what breaks the limit
-    while (resident_bytes + ws + plan->output_bytes > limit && slices > 1) {
+    while (resident_bytes + alloc_bytes(ws) + out_charged > limit && slices > 1) {
       slices = std::max(1, slices / 2);
       ws = layout(chunk, slices);
     }
-    if (resident_bytes + ws + plan->output_bytes <= limit) {
+    if (resident_bytes + alloc_bytes(ws) + out_charged <= limit) {
       plan->chunk_rows = chunk;
       plan->n_chunks = ceil_div(n, chunk);
       plan->slices = slices;
       plan->workspace_bytes = ws;
-      plan->peak_bytes = resident_bytes + ws + plan->output_bytes;
+      plan->peak_bytes = resident_bytes + alloc_bytes(ws) + out_charged;
       return TB_OK;
     }
     if (chunk <= min_chunk) {
-      const int64_t need = resident_bytes + ws + plan->output_bytes;
+      const int64_t need = resident_bytes + alloc_bytes(ws) + out_charged;
       return fail(TB_ERR_BUDGET,
                   "knn: allocating " + std::to_string(ws + plan->output_bytes) +
                       " bytes would exceed the budget (live=" +
@@ -207,6 +226,69 @@ int tb_knn_run_ex(const tb_knn_plan* p, const void* x, const void* q,
                   int64_t index_base, void* out_dist, int64_t* out_idx,
                   void* workspace, int64_t workspace_bytes, void* stream,
                   void** events, int32_t n_events) {
+  return knn_run_impl(p, x, q, index_base, out_dist, out_idx, workspace, workspace_bytes,
+                      (cudaStream_t)stream, events, n_events, nullptr, 0);
+}
+
+int tb_knn_run_host(const tb_knn_plan* p, const void* x_host, const void* q_host,
+                    int64_t index_base, void* dist_host, int64_t* idx_host, void* x_dev,
+                    void* q_dev, void* dist_dev, int64_t* idx_dev, void* workspace,
+                    int64_t workspace_bytes, void* stream) {
+  if (!p) return fail(TB_ERR_ARG, "plan pointer is null");
+  if (!x_host || !q_host || !dist_host || !idx_host || !x_dev || !q_dev || !dist_dev || !idx_dev)
+    return fail(TB_ERR_ARG, "null buffer passed to tb_knn_run_host");
+  if (p->m == 0) return TB_OK;
+  std::string why;
+  if (!device_is_sm100(&why)) return fail(TB_ERR_NO_DEVICE, why);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t es = elem_size(p->dtype);
+  // database chunk c is copied on a side stream; chunk c's compute waits only
+  // for its own rows, so chunk c+1's host->device copy overlaps chunk c
+  cudaStream_t cp;
+  TB_CUDA_TRY(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> ready((size_t)p->n_chunks + 1);
+  int rc = TB_OK;
+  for (auto& e : ready) {
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      rc = fail(TB_ERR_CUDA, "cudaEventCreate failed");
+      break;
+    }
+  }
+  if (rc == TB_OK) {
+    // the copy stream starts after the caller's prior work on `stream`
+    cudaEventRecord(ready[p->n_chunks], st);
+    cudaStreamWaitEvent(cp, ready[p->n_chunks], 0);
+    cudaMemcpyAsync(q_dev, q_host, p->m * p->d * es, cudaMemcpyHostToDevice, st);
+    for (int64_t c = 0; c < p->n_chunks; ++c) {
+      const int64_t c0 = c * p->chunk_rows, rows = std::min(p->chunk_rows, p->n - c0);
+      cudaMemcpyAsync((char*)x_dev + c0 * p->d * es, (const char*)x_host + c0 * p->d * es,
+                      rows * p->d * es, cudaMemcpyHostToDevice, cp);
+      cudaEventRecord(ready[c], cp);
+    }
+    std::vector<void*> rv(ready.begin(), ready.end());
+    rc = knn_run_impl(p, x_dev, q_dev, index_base, dist_dev, idx_dev, workspace,
+                      workspace_bytes, st, nullptr, 0, rv.data(), (int32_t)p->n_chunks);
+    if (rc == TB_OK) {
+      cudaMemcpyAsync(dist_host, dist_dev, p->m * p->k * elem_size(p->out_dtype),
+                      cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(idx_host, idx_dev, p->m * p->k * 8, cudaMemcpyDeviceToHost, st);
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) rc = fail(TB_ERR_CUDA, std::string("tb_knn_run_host: ") +
+                                                       cudaGetErrorString(e));
+    }
+  }
+  for (auto& e : ready)
+    if (e) cudaEventDestroy(e);
+  cudaStreamDestroy(cp);
+  return rc;
+}
+
+}  // extern "C"
+
+static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
+                        int64_t index_base, void* out_dist, int64_t* out_idx,
+                        void* workspace, int64_t workspace_bytes, cudaStream_t st,
+                        void** events, int32_t n_events, void** ready, int32_t n_ready) {
   if (!p) return fail(TB_ERR_ARG, "plan pointer is null");
   if (p->m == 0) return TB_OK;
   if (!x || !q || !out_dist || !out_idx || !workspace)
@@ -215,7 +297,6 @@ int tb_knn_run_ex(const tb_knn_plan* p, const void* x, const void* q,
     return fail(TB_ERR_ARG, "workspace smaller than plan->workspace_bytes");
   std::string why;
   if (!device_is_sm100(&why)) return fail(TB_ERR_NO_DEVICE, why);
-  cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)workspace;
   auto at = [&](int slot) { return ws + p->off[slot]; };
   double* qn64 = (double*)at(kQn64);
@@ -251,6 +332,7 @@ int tb_knn_run_ex(const tb_knn_plan* p, const void* x, const void* q,
     const int64_t rows = std::min(p->chunk_rows, p->n - c0);
     const int64_t rows_pad = round_up(rows, tile_rows);
     const char* xc = (const char*)x + c0 * p->d * es;
+    if (ready && c < n_ready) TB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)ready[c], 0));
     rc = launch_db_prep(p->dtype, xc, rows, p->d, xn, stats, xhi, xlo,
                         rows_pad, p->d_pad, xext, st);
     if (rc) return rc;
@@ -297,6 +379,8 @@ int tb_knn_run_ex(const tb_knn_plan* p, const void* x, const void* q,
   return launch_knn_fallback(p->dtype, p->out_dtype, x, q, p->n, p->m, p->d,
                              p->k, stats, fb, out_dist, out_idx, index_base, st);
 }
+
+extern "C" {
 
 int tb_knn_fallback_count(const tb_knn_plan* p, const void* workspace,
                           void* stream, int64_t* count) {

@@ -379,7 +379,9 @@ int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel, int32
   plan->sigma_bytes = i8 ? i8_tiles(M_pad) * kI8Tile * kI8Tile * 8 : M * M * 8;
   plan->output_bytes = plan->sigma_bytes + M * 8 + 8;
   const int64_t limit = memory_limit > 0 ? memory_limit : INT64_MAX;
-  const int64_t fixed = resident_bytes + plan->output_bytes;
+  // outputs as the caller's allocator charges them (Sigma, v, yy buffers)
+  const int64_t fixed = resident_bytes + alloc_bytes(plan->sigma_bytes) + alloc_bytes(M * 8) +
+                        alloc_bytes(8);
   auto budget_fail = [&](int64_t ws) {
     return fail(TB_ERR_BUDGET, "sgpr: allocating " + std::to_string(plan->output_bytes + ws) +
                                    " bytes would exceed the budget (live=" +
@@ -397,7 +399,7 @@ int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel, int32
     const int64_t cap = std::min<int64_t>(kI8MaxChunk, round_up(N, 128));
     auto largest = [&](int nbuf) -> int64_t {
       for (int64_t nc = cap; nc >= 128; nc -= 128)
-        if (fixed + nbuf * buf_bytes(nc) <= limit) return nc;
+        if (fixed + alloc_bytes(nbuf * buf_bytes(nc)) <= limit) return nc;
       return 0;
     };
     const int64_t n1 = largest(1), n2 = N > cap ? largest(2) : 0;
@@ -411,7 +413,7 @@ int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel, int32
     plan->off[3] = plan->off[2] + plan->off[1];
     plan->off[4] = nbuf;
     plan->workspace_bytes = nbuf * buf_bytes(nc);
-    plan->peak_bytes = fixed + plan->workspace_bytes;
+    plan->peak_bytes = fixed + alloc_bytes(plan->workspace_bytes);
     return TB_OK;
   }
   // fp64 engines: one fp64 Kuf chunk [M_pad, nc]; as large as the budget
@@ -419,10 +421,10 @@ int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel, int32
   int64_t nc = std::min<int64_t>(8192, round_up(N, 128));
   for (;;) {
     const int64_t ws = round_up(M_pad * nc * 8, 256);
-    if (fixed + ws <= limit) {
+    if (fixed + alloc_bytes(ws) <= limit) {
       plan->chunk_n = nc;
       plan->workspace_bytes = ws;
-      plan->peak_bytes = fixed + ws;
+      plan->peak_bytes = fixed + alloc_bytes(ws);
       return TB_OK;
     }
     if (nc <= 128) return budget_fail(ws);

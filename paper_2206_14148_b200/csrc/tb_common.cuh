@@ -154,5 +154,11 @@ __device__ __forceinline__ double to_f64(T v) { return (double)v; }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+// Device bytes the caller's caching allocator charges for one b-byte buffer
+// (PyTorch: 512-B granules up to 1 MiB, 2 MiB granules above).  Planners
+// count buffers this way so measured max_memory_allocated <= peak_bytes.
+inline int64_t alloc_bytes(int64_t b) {
+  return b <= ((int64_t)1 << 20) ? round_up(b, 512) : round_up(b, (int64_t)2 << 20);
+}
 
 }  // namespace tb

@@ -55,11 +55,12 @@ def _raise(exc):
 
 def plan(n: int, m: int, d: int, k: int, *, metric: str = "l2", dtype=np.float32,
          out_dtype=None, engine: str = "auto", memory_limit=None,
-         resident_bytes: int | None = None) -> _lib.KnnPlan:
+         resident_bytes: int | None = None, max_chunk_rows: int = 0) -> _lib.KnnPlan:
     """Run the planner alone (CPU only, no device needed).
 
     ``resident_bytes`` defaults to the bytes of x and q themselves, which the
     reference also counts against its budget (interpreter.py:543-546).
+    ``max_chunk_rows`` caps the database rows per chunk (0: memory decides).
     """
     if metric not in _lib.METRICS:
         raise ValueError(f"metric must be one of {tuple(_lib.METRICS)}")
@@ -72,10 +73,10 @@ def plan(n: int, m: int, d: int, k: int, *, metric: str = "l2", dtype=np.float32
         resident_bytes = (n + m) * d * es
     p = _lib.KnnPlan()
     lib = _lib.load()
-    rc = lib.tb_knn_plan_create(n, m, d, k, _lib.METRICS[metric], _tb_dtype(dtype),
-                                _tb_dtype(out_dtype or dtype), _lib.ENGINES[engine],
-                                as_limit(memory_limit), resident_bytes,
-                                ctypes.byref(p))
+    rc = lib.tb_knn_plan_create_ex(n, m, d, k, _lib.METRICS[metric], _tb_dtype(dtype),
+                                   _tb_dtype(out_dtype or dtype), _lib.ENGINES[engine],
+                                   as_limit(memory_limit), resident_bytes, int(max_chunk_rows),
+                                   ctypes.byref(p))
     _lib.check(rc, f"knn_n{n}_m{m}_d{d}_k{k}", requested=0, live=resident_bytes)
     return p
 
@@ -97,11 +98,12 @@ class KnnOperator:
     """
 
     def __init__(self, n, m, d, k, *, metric="l2", dtype=np.float32, out_dtype=None,
-                 engine="auto", memory_limit=None, device=None, resident_bytes=None):
+                 engine="auto", memory_limit=None, device=None, resident_bytes=None,
+                 max_chunk_rows: int = 0):
         torch = _torch()
         self.plan = plan(n, m, d, k, metric=metric, dtype=dtype, out_dtype=out_dtype,
                          engine=engine, memory_limit=memory_limit,
-                         resident_bytes=resident_bytes)
+                         resident_bytes=resident_bytes, max_chunk_rows=max_chunk_rows)
         self.device = torch.device(device or "cuda")
         self.dtype = np.dtype(dtype)
         self.out_dtype = np.dtype(out_dtype or dtype)
@@ -143,6 +145,43 @@ class KnnOperator:
                                        st.cuda_stream, ev_arr, n_ev)
         _lib.check(rc, "knn")
         return dist, idx
+
+    def run_host(self, xh, qh, out_host=None, *, index_base: int = 0, stream=None,
+                 staging=None):
+        """Host (CPU) x[n,d], q[m,d] in -> host (dist, idx) out, through
+        tb_knn_run_host: database chunk c+1 is copied to the device while
+        chunk c computes.  ``xh``/``qh`` are torch CPU tensors (pin them for
+        asynchronous copies); ``staging`` = (x_dev, q_dev, dist_dev, idx_dev)
+        device buffers to reuse (allocated on first use otherwise).  Returns
+        host tensors after synchronising the stream."""
+        torch = _torch()
+        p = self.plan
+        for name, t, rows in (("x", xh, p.n), ("q", qh, p.m)):
+            if tuple(t.shape) != (rows, p.d) or t.is_cuda or not t.is_contiguous():
+                raise EvaluationError(f"{name} must be a contiguous host tensor of shape "
+                                      f"{(int(rows), int(p.d))}")
+            if t.dtype != self._torch_dtype(self.dtype):
+                raise EvaluationError(f"{name} dtype {t.dtype} != planned {self.dtype}")
+        if staging is None:
+            if getattr(self, "_staging", None) is None:
+                td = self._torch_dtype(self.dtype)
+                self._staging = (torch.empty((int(p.n), int(p.d)), dtype=td, device=self.device),
+                                 torch.empty((int(p.m), int(p.d)), dtype=td, device=self.device),
+                                 *self.alloc_outputs())
+            staging = self._staging
+        xd, qd, dd, idd = staging
+        if out_host is None:
+            out_host = (torch.empty(tuple(dd.shape), dtype=dd.dtype).pin_memory(),
+                        torch.empty(tuple(idd.shape), dtype=torch.int64).pin_memory())
+        dh, ih = out_host
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = _lib.load().tb_knn_run_host(ctypes.byref(p), xh.data_ptr(), qh.data_ptr(),
+                                         int(index_base), dh.data_ptr(), ih.data_ptr(),
+                                         xd.data_ptr(), qd.data_ptr(), dd.data_ptr(),
+                                         idd.data_ptr(), self.workspace.data_ptr(),
+                                         self.workspace.numel(), st.cuda_stream)
+        _lib.check(rc, "knn_host")
+        return dh, ih
 
     def fallback_count(self, stream=None) -> int:
         torch = _torch()

@@ -230,3 +230,24 @@ def test_topk_merge_abi():
                                     torch.from_numpy(np.stack(il)).cuda())
     assert np.array_equal(oi.cpu().numpy(), ref_i)
     assert rel_err(od.cpu().numpy(), ref_d) < 1e-12
+
+
+@pytest.mark.parametrize("chunk", [0, 2048, 777])
+def test_run_host_pipelined_matches_device_run(chunk):
+    """tb_knn_run_host (host buffers, per-chunk H2D overlapped with compute)
+    returns exactly what the device-resident call returns, and the oracle's
+    answer, for 1 and several database chunks (ragged last chunk)."""
+    import torch
+    x, q = synthetic.gaussian_knn(9000, 300, 64, seed=21)
+    op = neighbors.KnnOperator(9000, 300, 64, 10, max_chunk_rows=chunk)
+    if chunk:
+        assert op.plan.n_chunks > 1
+    xh = torch.from_numpy(x).pin_memory()
+    qh = torch.from_numpy(q).pin_memory()
+    dh, ih = op.run_host(xh, qh)
+    torch.cuda.synchronize()
+    dd, idd = op.run(torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda())
+    assert np.array_equal(dh.numpy(), dd.cpu().numpy())
+    assert np.array_equal(ih.numpy(), idd.cpu().numpy())
+    ref_d, ref_i = oknn.exact(x, q, 10)
+    assert oknn.compare(dh.numpy(), ih.numpy(), ref_d, ref_i, x, q)["ok"]

@@ -72,7 +72,10 @@ def test_c2_plan_fits_one_gb(engine):
     p = tknn.plan(**C2, dtype=np.float32, memory_limit="1GB", engine=engine)
     assert p.peak_bytes <= 10**9
     assert p.resident_bytes == (C2["n"] + C2["m"]) * C2["d"] * 4
-    assert p.peak_bytes == p.resident_bytes + p.workspace_bytes + p.output_bytes
+    # peak = resident + buffers as a caching allocator charges them
+    # (512-B granules up to 1 MiB, 2 MiB above): never below the exact sum
+    exact = p.resident_bytes + p.workspace_bytes + p.output_bytes
+    assert exact <= p.peak_bytes <= exact + 3 * (2 << 20)
     assert p.n_chunks * p.chunk_rows >= C2["n"]
     assert p.cand >= C2["k"]
 
