@@ -128,10 +128,13 @@ int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int32_t me
     return fail(TB_ERR_ARG, "unknown engine");
   const bool tc = engine != TB_ENGINE_SIMT;
   if (tc && round_up(d, 64) > tc_max_dpad())
-    return fail(TB_ERR_UNSUPPORTED, "tcgen05 engines keep the query tile resident: need d <= " +
+    return fail(TB_ERR_UNSUPPORTED, "tcgen05 engines support d <= " +
                                         std::to_string(tc_max_dpad()));
 
-  const int64_t margin = engine == TB_ENGINE_TC1 ? std::max<int64_t>(22, k) : 6;
+  // candidates kept beyond k: the single-pass engine and long (d > 128)
+  // contractions have wider certified error bounds, so they keep more
+  const int64_t margin =
+      engine == TB_ENGINE_TC1 ? std::max<int64_t>(22, k) : (round_up(d, 64) > 128 ? 22 : 6);
   const int64_t want = k + margin;
   int cand = want <= 16 ? 16 : want <= 32 ? 32 : want <= 64 ? 64 : 0;
   if (!cand) {
@@ -376,8 +379,11 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
                          qn64, qnorm, stats, p->n, p->m, p->d, p->k, c1, c2,
                          out_dist, out_idx, index_base, fb, st);
   if (rc) return rc;
-  return launch_knn_fallback(p->dtype, p->out_dtype, x, q, p->n, p->m, p->d,
-                             p->k, stats, fb, out_dist, out_idx, index_base, st);
+  // the per-chunk candidate lists (kCandS, kCandI) are dead after the last
+  // merge: the fallback uses them as scratch
+  return launch_knn_fallback(p->dtype, p->out_dtype, x, q, p->n, p->m, p->d, p->k, stats, fb,
+                             at(kCandS), p->off[kRunS] - p->off[kCandS], out_dist, out_idx,
+                             index_base, st);
 }
 
 extern "C" {

@@ -70,9 +70,9 @@ int launch_knn_refine(int dtype, int out_dtype, int cand, const float* cs,
                       cudaStream_t st);
 int launch_knn_fallback(int dtype, int out_dtype, const void* x, const void* q,
                         int64_t n, int64_t m, int64_t d, int64_t k,
-                        const unsigned* stats, const int* fb_list,
-                        void* out_dist, int64_t* out_idx, int64_t index_base,
-                        cudaStream_t st);
+                        const unsigned* stats, const int* fb_list, void* scratch,
+                        int64_t scratch_bytes, void* out_dist, int64_t* out_idx,
+                        int64_t index_base, cudaStream_t st);
 int launch_topk_merge(const void* dist_lists, const int64_t* idx_lists,
                       int n_lists, int64_t m, int64_t k, int dtype,
                       void* out_dist, int64_t* out_idx, cudaStream_t st);

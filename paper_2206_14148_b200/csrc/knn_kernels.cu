@@ -61,9 +61,10 @@ __global__ void rows_prep_kernel(const T* __restrict__ src, int64_t rows,
   if (max_bits && lane == 0 && wmax > 0.f) atomicMax(max_bits, __float_as_uint(wmax));
 }
 
-// Tensor-core operand prep, G = d_pad / 8 threads per row, 8 elements per
-// thread: 16-byte loads/stores of the bf16 hi/lo split, fp64 norms reduced
-// over the row's lanes, and one max-norm atomic per block (not per row).
+// Tensor-core operand prep, G threads per row (G = d_pad / 8 for d_pad 64 /
+// 128, a full warp looping over 8-element segments beyond), 8 elements per
+// thread and step: 16-byte loads/stores of the bf16 hi/lo split, fp64 norms
+// reduced over the row's lanes, and one max-norm atomic per block.
 template <typename T, int G>
 __global__ void __launch_bounds__(256)
 rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
@@ -77,9 +78,8 @@ rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
   const int64_t r = gt / G;
   const int seg = (int)(gt % G);
   double acc = 0.0;
-  if (r < rows_pad) {
+  for (int64_t c0 = (int64_t)seg * 8; r < rows_pad && c0 < d_pad; c0 += 8 * G) {
     double v[8];
-    const int64_t c0 = (int64_t)seg * 8;
     if (r < rows && c0 + 8 <= d && sizeof(T) == 4 && (d & 3) == 0) {
       const float4 a = __ldg(reinterpret_cast<const float4*>(src + r * d + c0));
       const float4 b = __ldg(reinterpret_cast<const float4*>(src + r * d + c0 + 4));
@@ -154,15 +154,20 @@ static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
                      uint8_t* ext = nullptr) {
   const int64_t limit = hi ? rows_pad : rows;
   if (limit <= 0) return TB_OK;
-  if (hi && (d_pad == 64 || d_pad == 128)) {
-    const int64_t threads = rows_pad * (d_pad / 8);
+  if (hi && d_pad % 64 == 0) {
+    const int G = d_pad == 64 ? 8 : d_pad == 128 ? 16 : 32;
+    const int64_t threads = rows_pad * G;
     const unsigned blocks = (unsigned)ceil_div(threads, 256);
-    if (d_pad == 64)
+    if (G == 8)
       rows_split_kernel<T, 8><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32, norm32,
                                                       max_bits, hi, lo, rows_pad, d_pad, scale,
                                                       ext);
-    else
+    else if (G == 16)
       rows_split_kernel<T, 16><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32, norm32,
+                                                       max_bits, hi, lo, rows_pad, d_pad, scale,
+                                                       ext);
+    else
+      rows_split_kernel<T, 32><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32, norm32,
                                                        max_bits, hi, lo, rows_pad, d_pad, scale,
                                                        ext);
     TB_LAUNCH_CHECK("rows_split");
@@ -529,86 +534,146 @@ int launch_knn_refine(int dtype, int out_dtype, int cand, const float* cs,
 }
 
 // ------------------------------------------------- exact fp64 fallback --
-// Persistent: each CTA takes flagged queries p = blockIdx.x, +gridDim.x, ...
-// and brute-forces the whole shard in fp64 (direct differences).
-template <typename T, typename OT, int KC>
+// Uncertified queries (count = stats[1], normally 0) are brute-forced in
+// fp64 with direct differences.  The grid is sized on the host without
+// knowing count: each of the G blocks derives S = max(1, G / count) database
+// slices per query and takes units u = slice * count + p (slice-major, so
+// concurrently running blocks scan the same rows for different queries and
+// share them through L2).  One warp per database row (lane-strided over d,
+// coalesced), a per-warp top-KC, merged per block into scratch[u]; then
+// knn_fallback_merge combines the S lists of each query.
+template <typename T, int KC>
 __global__ void __launch_bounds__(256)
-knn_fallback_kernel(const T* __restrict__ x, const T* __restrict__ q, int64_t n,
-                    int64_t d, int k, const unsigned* __restrict__ stats,
-                    const int* __restrict__ fb_list, OT* __restrict__ out_dist,
-                    int64_t* __restrict__ out_idx, int64_t index_base) {
+knn_fallback_partial_kernel(const T* __restrict__ x, const T* __restrict__ q, int64_t n,
+                            int64_t d, const unsigned* __restrict__ stats,
+                            const int* __restrict__ fb_list, double* __restrict__ sc_d,
+                            int* __restrict__ sc_i) {
   __shared__ double sd[8][KC];
   __shared__ int si[8][KC];
   const int count = *reinterpret_cast<const volatile int*>(&stats[1]);
+  if (count == 0) return;
+  const int S = max(1, (int)gridDim.x / count);
+  const int units = count * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int p = blockIdx.x; p < count; p += gridDim.x) {
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int slice = u / count, p = u - slice * count;
     const int64_t r = fb_list[p];
     const T* qr = q + r * d;
+    const int64_t j0 = n * slice / S, j1 = n * (slice + 1) / S;
     TopList<double, KC> L;
     L.init();
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    for (int64_t j = j0 + warp; j < j1; j += 8) {
       const T* xr = x + j * d;
       double acc = 0.0;
-      for (int64_t t = 0; t < d; ++t) {
+      for (int64_t t = lane; t < d; t += 32) {
         const double df = (double)qr[t] - (double)xr[t];
         acc = fma(df, df, acc);
       }
-      L.offer(acc, (int)j);
+      acc = warp_sum(acc);
+      L.offer(acc, (int)j);      // identical in every lane
     }
-    warp_drain(L, KC, [&](int t, double v, int j) {
-      sd[warp][t] = v;
-      si[warp][t] = j;
-    });
+    if (lane == 0)
+      for (int t = 0; t < KC; ++t) {
+        sd[warp][t] = L.s[t];
+        si[warp][t] = L.i[t];
+      }
     __syncthreads();
     if (warp == 0) {
       TopList<double, KC> M;
       M.init();
       if (lane < 8)
         for (int t = 0; t < KC; ++t) M.offer(sd[lane][t], si[lane][t]);
-      warp_drain(M, k, [&](int t, double v, int j) {
-        out_dist[r * k + t] = (OT)v;
-        out_idx[r * k + t] = (int64_t)j + index_base;
+      warp_drain(M, KC, [&](int t, double v, int j) {
+        sc_d[(int64_t)u * KC + t] = v;
+        sc_i[(int64_t)u * KC + t] = j;
       });
     }
     __syncthreads();
   }
 }
 
-template <typename T, typename OT>
-static int fallback_dispatch(const void* x, const void* q, int64_t n,
-                             int64_t d, int64_t k, const unsigned* stats,
-                             const int* fb, void* od, int64_t* oi,
-                             int64_t base, cudaStream_t st) {
+template <typename OT, int KC>
+__global__ void knn_fallback_merge_kernel(const unsigned* __restrict__ stats,
+                                          const int* __restrict__ fb_list, int G, int k,
+                                          const double* __restrict__ sc_d,
+                                          const int* __restrict__ sc_i,
+                                          OT* __restrict__ out_dist,
+                                          int64_t* __restrict__ out_idx, int64_t index_base) {
+  const int count = *reinterpret_cast<const volatile int*>(&stats[1]);
+  const int S = count ? max(1, G / count) : 1;
+  const int lane = threadIdx.x & 31;
+  for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < count;
+       p += gridDim.x * (blockDim.x >> 5)) {
+    const int64_t r = fb_list[p];
+    TopList<double, KC> M;
+    M.init();
+    for (int sl = lane; sl < S; sl += 32) {
+      const int64_t u = (int64_t)sl * count + p;
+      for (int t = 0; t < KC; ++t) M.offer(sc_d[u * KC + t], sc_i[u * KC + t]);
+    }
+    warp_drain(M, k, [&](int t, double v, int j) {
+      out_dist[r * k + t] = (OT)v;
+      out_idx[r * k + t] = (int64_t)j + index_base;
+    });
+  }
+}
+
+template <typename T, typename OT, int KC>
+static int fallback_launch(const void* x, const void* q, int64_t n, int64_t d, int64_t k,
+                           const unsigned* stats, const int* fb, void* scratch,
+                           int64_t scratch_bytes, int64_t m, void* od, int64_t* oi,
+                           int64_t base, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned blocks = (unsigned)(2 * sms);
-  if (k <= 16)
-    knn_fallback_kernel<T, OT, 16><<<blocks, 256, 0, st>>>((const T*)x, (const T*)q, n, d, (int)k, stats, fb, (OT*)od, oi, base);
-  else if (k <= 32)
-    knn_fallback_kernel<T, OT, 32><<<blocks, 256, 0, st>>>((const T*)x, (const T*)q, n, d, (int)k, stats, fb, (OT*)od, oi, base);
-  else if (k <= 64)
-    knn_fallback_kernel<T, OT, 64><<<blocks, 256, 0, st>>>((const T*)x, (const T*)q, n, d, (int)k, stats, fb, (OT*)od, oi, base);
-  else
-    return fail(TB_ERR_UNSUPPORTED, "fallback: k > 64");
-  TB_LAUNCH_CHECK("knn_fallback");
+  // scratch holds max(G, count) lists of KC (double, int); count <= m
+  const int64_t cap = scratch_bytes / (12 * KC);
+  if (cap < m) return fail(TB_ERR_ARG, "fallback scratch too small");
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(4 * sms, cap));
+  double* sc_d = (double*)scratch;
+  int* sc_i = (int*)(sc_d + cap * KC);
+  knn_fallback_partial_kernel<T, KC><<<G, 256, 0, st>>>((const T*)x, (const T*)q, n, d, stats,
+                                                        fb, sc_d, sc_i);
+  TB_LAUNCH_CHECK("knn_fallback_partial");
+  knn_fallback_merge_kernel<OT, KC><<<(unsigned)ceil_div(m, 8), 256, 0, st>>>(
+      stats, fb, G, (int)k, sc_d, sc_i, (OT*)od, oi, base);
+  TB_LAUNCH_CHECK("knn_fallback_merge");
   return TB_OK;
+}
+
+template <typename T, typename OT>
+static int fallback_dispatch(const void* x, const void* q, int64_t n, int64_t d, int64_t k,
+                             const unsigned* stats, const int* fb, void* scratch,
+                             int64_t scratch_bytes, int64_t m, void* od, int64_t* oi,
+                             int64_t base, cudaStream_t st) {
+  if (k <= 16)
+    return fallback_launch<T, OT, 16>(x, q, n, d, k, stats, fb, scratch, scratch_bytes, m, od,
+                                      oi, base, st);
+  if (k <= 32)
+    return fallback_launch<T, OT, 32>(x, q, n, d, k, stats, fb, scratch, scratch_bytes, m, od,
+                                      oi, base, st);
+  if (k <= 64)
+    return fallback_launch<T, OT, 64>(x, q, n, d, k, stats, fb, scratch, scratch_bytes, m, od,
+                                      oi, base, st);
+  return fail(TB_ERR_UNSUPPORTED, "fallback: k > 64");
 }
 
 int launch_knn_fallback(int dtype, int out_dtype, const void* x, const void* q,
                         int64_t n, int64_t m, int64_t d, int64_t k,
-                        const unsigned* stats, const int* fb_list,
-                        void* out_dist, int64_t* out_idx, int64_t index_base,
-                        cudaStream_t st) {
+                        const unsigned* stats, const int* fb_list, void* scratch,
+                        int64_t scratch_bytes, void* out_dist, int64_t* out_idx,
+                        int64_t index_base, cudaStream_t st) {
   if (m <= 0) return TB_OK;
+#define TB_FB(T, OT)                                                                           \
+  return fallback_dispatch<T, OT>(x, q, n, d, k, stats, fb_list, scratch, scratch_bytes, m,    \
+                                  out_dist, out_idx, index_base, st)
   if (dtype == TB_F32) {
-    if (out_dtype == TB_F32)
-      return fallback_dispatch<float, float>(x, q, n, d, k, stats, fb_list, out_dist, out_idx, index_base, st);
-    return fallback_dispatch<float, double>(x, q, n, d, k, stats, fb_list, out_dist, out_idx, index_base, st);
+    if (out_dtype == TB_F32) TB_FB(float, float);
+    TB_FB(float, double);
   }
-  if (out_dtype == TB_F32)
-    return fallback_dispatch<double, float>(x, q, n, d, k, stats, fb_list, out_dist, out_idx, index_base, st);
-  return fallback_dispatch<double, double>(x, q, n, d, k, stats, fb_list, out_dist, out_idx, index_base, st);
+  if (out_dtype == TB_F32) TB_FB(double, float);
+  TB_FB(double, double);
+#undef TB_FB
 }
 
 // ------------------------------------------------ cross-shard top-k merge --

@@ -37,20 +37,25 @@ constexpr int kTcN = 256;        // database rows per tile (UMMA N)
 constexpr int kTcKB = 64;        // bf16 per 128-B swizzle row
 constexpr int kTcEpiWarps = 8;
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
-constexpr int kTcMaxDpad = 128;  // query tile stays resident in shared memory
+constexpr int kTcMaxDpad = 128;  // up to here the query tile stays resident in smem
+constexpr int kTcMaxDpadSQ = 1024;  // beyond: query k-blocks streamed with the database
 constexpr int kTcStages = 4;     // 32 KB database k-blocks in flight
+constexpr int kTcStagesSQ = 6;   // streamed-query ring: [q hi|lo], [x hi], [x lo] per k-block
 constexpr int kTcExtK = 16;      // augmented K block carrying -||x||^2
 constexpr uint32_t kTcAExt = kTcM * kTcExtK * 2;   // 4 KB  [128 x 16] bf16
 constexpr uint32_t kTcBExt = kTcN * kTcExtK * 2;   // 8 KB  [256 x 16] bf16
 
-template <int PASSES>
+// SQ = streamed queries (d_pad > 128): the query k-block (hi, lo) rides in
+// the ring in front of the database k-blocks instead of staying resident.
+template <int PASSES, bool SQ>
 struct TcCfg {
   static constexpr int kMats = PASSES == 3 ? 2 : 1;            // hi (+ lo)
   static constexpr uint32_t kABlock = kTcM * 128;               // 16 KB
-  static constexpr uint32_t kBBlock = kTcN * 128;               // 32 KB
+  static constexpr uint32_t kBBlock = kTcN * 128;               // 32 KB (one ring stage)
+  static constexpr int kStages = SQ ? kTcStagesSQ : kTcStages;
   static size_t smem_bytes(int nkb) {
-    return 1024 + (size_t)kMats * nkb * kABlock + kTcAExt + (size_t)kTcStages * kBBlock +
-           2 * kTcBExt + (2 * kTcStages + 10) * 8 + 16;
+    return 1024 + (SQ ? 0 : (size_t)kMats * nkb * kABlock) + kTcAExt +
+           (size_t)kStages * kBBlock + 2 * kTcBExt + (2 * kStages + 10) * 8 + 16;
   }
 };
 
@@ -79,7 +84,7 @@ struct TcWork {
 // extra K=16 MMA per tile (A_ext rows = [1,1,1,0...], B_ext rows =
 // -(h,m,l), the bf16 triple split of ||x||^2; SWIZZLE_NONE K-major core
 // matrices).  The selection score is s = -acc' = ||x||^2 - 2 q.x.
-template <int PASSES, int KC>
+template <int PASSES, int KC, bool SQ>
 __global__ void __launch_bounds__(kTcThreads, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               const __grid_constant__ CUtensorMap tm_qlo,
@@ -88,12 +93,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               const uint8_t* __restrict__ xext, TcWork work, int m, int nkb,
               int idx_base, float* __restrict__ cand_s, int* __restrict__ cand_i,
               unsigned* __restrict__ gthr) {
-  using Cfg = TcCfg<PASSES>;
-  constexpr int S = kTcStages;
+  using Cfg = TcCfg<PASSES, SQ>;
+  constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_base = smem;
-  uint8_t* b_base = a_base + (size_t)Cfg::kMats * nkb * Cfg::kABlock;
+  uint8_t* b_base = a_base + (SQ ? 0 : (size_t)Cfg::kMats * nkb * Cfg::kABlock);
   uint8_t* bext = b_base + (size_t)S * Cfg::kBBlock;          // 2 x 8 KB
   uint8_t* aext = bext + 2 * kTcBExt;                          // 4 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(aext + kTcAExt);
@@ -154,14 +159,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++seg) {
         const int slice = u / work.qtiles, qt = u - slice * work.qtiles;
         const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
-        mbar_wait(a_empty, (seg & 1) ^ 1);           // previous query tile retired
-        mbar_expect_tx(a_full, Cfg::kMats * nkb * Cfg::kABlock);
-        for (int kb = 0; kb < nkb; ++kb) {
-          tma_load_2d(a_base + (size_t)kb * Cfg::kABlock, &tm_qhi, a_full, kb * kTcKB,
-                      qt * kTcM);
-          if (Cfg::kMats == 2)
-            tma_load_2d(a_base + (size_t)(nkb + kb) * Cfg::kABlock, &tm_qlo, a_full,
-                        kb * kTcKB, qt * kTcM);
+        if (!SQ) {
+          mbar_wait(a_empty, (seg & 1) ^ 1);           // previous query tile retired
+          mbar_expect_tx(a_full, Cfg::kMats * nkb * Cfg::kABlock);
+          for (int kb = 0; kb < nkb; ++kb) {
+            tma_load_2d(a_base + (size_t)kb * Cfg::kABlock, &tm_qhi, a_full, kb * kTcKB,
+                        qt * kTcM);
+            if (Cfg::kMats == 2)
+              tma_load_2d(a_base + (size_t)(nkb + kb) * Cfg::kABlock, &tm_qlo, a_full,
+                          kb * kTcKB, qt * kTcM);
+          }
         }
         for (int t = t0; t < t1; ++t, ++i) {
           const int e = i & 1;
@@ -169,6 +176,19 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           mbar_expect_tx(&efull[e], kTcBExt);
           bulk_load(bext + e * kTcBExt, xext + (size_t)t * kTcBExt, kTcBExt, &efull[e]);
           for (int kb = 0; kb < nkb; ++kb) {
+            if (SQ) {
+              // query k-block (hi, lo) into one ring stage
+              mbar_wait(&empty[s], ph ^ 1);
+              mbar_expect_tx(&full[s], Cfg::kMats * Cfg::kABlock);
+              uint8_t* qs = b_base + (size_t)s * Cfg::kBBlock;
+              tma_load_2d(qs, &tm_qhi, &full[s], kb * kTcKB, qt * kTcM);
+              if (Cfg::kMats == 2)
+                tma_load_2d(qs + Cfg::kABlock, &tm_qlo, &full[s], kb * kTcKB, qt * kTcM);
+              if (++s == S) {
+                s = 0;
+                ph ^= 1;
+              }
+            }
 #pragma unroll
             for (int mat = 0; mat < Cfg::kMats; ++mat) {
               mbar_wait(&empty[s], ph ^ 1);
@@ -194,8 +214,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++seg) {
         const int slice = u / work.qtiles;
         const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
-        mbar_wait(a_full, seg & 1);
-        tc_fence_after();
+        if (!SQ) {
+          mbar_wait(a_full, seg & 1);
+          tc_fence_after();
+        }
         for (int t = t0; t < t1; ++t, ++i) {
           const int buf = i & 1;
           mbar_wait(&tempty[buf], ((i >> 1) & 1) ^ 1);
@@ -206,8 +228,19 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           mma_bf16(d, desc_k_inter(aext_a, 128, 256), desc_k_inter(smem_u32(bext + buf * kTcBExt), 128, 256),
                    idesc, 0);
           for (int kb = 0; kb < nkb; ++kb) {
-            const uint32_t ahi = smem_u32(a_base + (size_t)kb * Cfg::kABlock);
-            const uint32_t alo = smem_u32(a_base + (size_t)(nkb + kb) * Cfg::kABlock);
+            uint32_t ahi = smem_u32(a_base + (size_t)kb * Cfg::kABlock);
+            uint32_t alo = smem_u32(a_base + (size_t)(nkb + kb) * Cfg::kABlock);
+            int qstage = -1;
+            if (SQ) {
+              mbar_wait(&full[s], ph);
+              ahi = smem_u32(b_base + (size_t)s * Cfg::kBBlock);
+              alo = ahi + Cfg::kABlock;
+              qstage = s;
+              if (++s == S) {
+                s = 0;
+                ph ^= 1;
+              }
+            }
             // stage x_hi: q_hi.x_hi (+ q_lo.x_hi)
             mbar_wait(&full[s], ph);
             tc_fence_after();
@@ -238,11 +271,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
                 ph ^= 1;
               }
             }
+            if (SQ) mma_commit(&empty[qstage]);   // query k-block consumed
           }
           mma_commit(&eempty[buf]);  // norm block may be replaced
           mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
         }
-        mma_commit(a_empty);         // query tile may be replaced
+        if (!SQ) mma_commit(a_empty);         // query tile may be replaced
       }
     }
   } else {
@@ -362,7 +396,7 @@ static int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
   return TB_OK;
 }
 
-int tc_max_dpad() { return kTcMaxDpad; }
+int tc_max_dpad() { return kTcMaxDpadSQ; }
 
 // Schedule of one database chunk of T tiles: a short seed launch over the
 // first kTcSeedTiles tiles (one unit per query tile) publishes per-query
@@ -403,15 +437,15 @@ int tc_lists(int64_t m, int64_t rows_pad, int sms) {
   return 2 + 2 * b.slices;
 }
 
-template <int PASSES, int KC>
+template <int PASSES, int KC, bool SQ>
 static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtensorMap& xh,
                      const CUtensorMap& xl, const uint8_t* xext, TcWork work,
                      int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
                      unsigned* gthr, cudaStream_t st) {
-  const size_t smem = TcCfg<PASSES>::smem_bytes(nkb);
-  TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<PASSES, KC>,
+  const size_t smem = TcCfg<PASSES, SQ>::smem_bytes(nkb);
+  TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<PASSES, KC, SQ>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  knn_tc_kernel<PASSES, KC><<<grid, kTcThreads, smem, st>>>(qh, ql, xh, xl, xext, work,
+  knn_tc_kernel<PASSES, KC, SQ><<<grid, kTcThreads, smem, st>>>(qh, ql, xh, xl, xext, work,
                                                             (int)m, nkb, idx_base, cs, ci, gthr);
   TB_LAUNCH_CHECK("knn_tc");
   return TB_OK;
@@ -427,8 +461,8 @@ int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfl
                   int64_t rows, int64_t rows_pad, int64_t m, int64_t m_pad, int64_t d_pad,
                   int lists, int idx_base, float* cs, int* ci, unsigned* gthr,
                   cudaStream_t st) {
-  if (d_pad > kTcMaxDpad || d_pad % kTcKB)
-    return fail(TB_ERR_UNSUPPORTED, "tcgen05 engine: d_pad must be 64 or 128");
+  if (d_pad > kTcMaxDpadSQ || d_pad % kTcKB)
+    return fail(TB_ERR_UNSUPPORTED, "tcgen05 engine: d_pad must be a multiple of 64, <= 1024");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -455,9 +489,12 @@ int tc_dispatch(int passes, int cand, const CUtensorMap& mqh, const CUtensorMap&
                 const CUtensorMap& mxh, const CUtensorMap& mxl, const uint8_t* xext,
                 TcWork work, int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
                 unsigned* gthr, cudaStream_t st) {
-#define TB_TC(P, KC)                                                                      \
-  return tc_launch<P, KC>(mqh, mql, mxh, mxl, xext, work, grid, m, nkb, idx_base, cs, \
-                          ci, gthr, st)
+#define TB_TC(P, KC)                                                                       \
+  return nkb * kTcKB > kTcMaxDpad                                                          \
+             ? tc_launch<P, KC, true>(mqh, mql, mxh, mxl, xext, work, grid, m, nkb, idx_base, \
+                                      cs, ci, gthr, st)                                      \
+             : tc_launch<P, KC, false>(mqh, mql, mxh, mxl, xext, work, grid, m, nkb, idx_base, \
+                                       cs, ci, gthr, st)
   if (passes == 3) {
     if (cand == 16) TB_TC(3, 16);
     if (cand == 32) TB_TC(3, 32);
