@@ -71,25 +71,42 @@ def reference_port(x: np.ndarray, q: np.ndarray, k: int,
 # fast exact checker
 
 
-def exact(x: np.ndarray, q: np.ndarray, k: int, chunk: int = 256,
-          ) -> tuple[np.ndarray, np.ndarray]:
-    """fp64 expanded-form squared L2, stable-argsort semantics.
+def _dist_block(qc, x64, xn, metric):
+    """fp64 [rows(qc), n] distances in the reference graph's formulas:
+    l2 expanded (match_replace.py:149-155), l1 = sum |q - x|
+    (frontend.py:57-63), cosine = 1 - q.x / (|q| |x|) (frontend.py:66-73)."""
+    if metric == "l2":
+        qn = np.sum(np.square(qc), axis=1)
+        return (qn[:, None] + xn[None, :]) + (-2.0 * (qc @ x64.T))
+    if metric == "l1":
+        step = max(1, int(2e7 // max(1, x64.shape[0] * x64.shape[1])))
+        return np.concatenate([np.sum(np.abs(qc[a:a + step, None, :] - x64[None, :, :]), axis=2)
+                               for a in range(0, qc.shape[0], step)])
+    if metric == "cosine":
+        qn = np.sqrt(np.sum(np.square(qc), axis=1))
+        return 1.0 - (qc @ x64.T) / (qn[:, None] * xn[None, :])
+    raise ValueError(f"unknown metric {metric!r}")
 
-    Returns (dist f64[m,k], idx int64[m,k]).
-    """
+
+def exact(x: np.ndarray, q: np.ndarray, k: int, chunk: int = 256, metric: str = "l2",
+          ) -> tuple[np.ndarray, np.ndarray]:
+    """fp64 distances of the reference graph for ``metric``, stable-argsort
+    semantics.  Returns (dist f64[m,k], idx int64[m,k])."""
     x64 = np.asarray(x, dtype=np.float64)
     q64 = np.asarray(q, dtype=np.float64)
     n = x64.shape[0]
     m = q64.shape[0]
     if not 1 <= k <= n:
         raise ValueError(f"k={k} must satisfy 1 <= k <= n={n}")
-    xn = np.sum(np.square(x64), axis=1)
+    if metric == "cosine":
+        xn = np.sqrt(np.sum(np.square(x64), axis=1))
+    else:
+        xn = np.sum(np.square(x64), axis=1)
     out_d = np.empty((m, k), np.float64)
     out_i = np.empty((m, k), np.int64)
     for s in range(0, m, chunk):
         qc = q64[s:s + chunk]
-        qn = np.sum(np.square(qc), axis=1)
-        dist = (qn[:, None] + xn[None, :]) + (-2.0 * (qc @ x64.T))
+        dist = _dist_block(qc, x64, xn, metric)
         if k < n:
             part = np.argpartition(dist, k - 1, axis=1)[:, :k]
             kth = np.max(np.take_along_axis(dist, part, axis=1), axis=1)
@@ -104,11 +121,18 @@ def exact(x: np.ndarray, q: np.ndarray, k: int, chunk: int = 256,
 
 
 def direct_dist(x: np.ndarray, q: np.ndarray, rows: np.ndarray,
-                idx: np.ndarray) -> np.ndarray:
-    """Exact fp64 sum((q - x)^2) for the given (query row, data index) pairs."""
+                idx: np.ndarray, metric: str = "l2") -> np.ndarray:
+    """Exact fp64 distance for the given (query row, data index) pairs:
+    sum((q - x)^2), sum |q - x|, or 1 - cos."""
     x64 = np.asarray(x, dtype=np.float64)
     q64 = np.asarray(q, dtype=np.float64)
-    diff = q64[rows] - x64[idx]
+    a, b = q64[rows], x64[idx]
+    if metric == "l1":
+        return np.sum(np.abs(a - b), axis=-1)
+    if metric == "cosine":
+        return 1.0 - np.sum(a * b, axis=-1) / (np.sqrt(np.sum(a * a, axis=-1)) *
+                                                np.sqrt(np.sum(b * b, axis=-1)))
+    diff = a - b
     return np.sum(diff * diff, axis=-1)
 
 
@@ -128,7 +152,7 @@ def rel_err(a, b) -> float:
 
 
 def compare(got_dist, got_idx, ref_dist, ref_idx, x, q,
-            tie_rtol: float = 1e-5, dist_rtol: float = 1e-4) -> dict:
+            tie_rtol: float = 1e-5, dist_rtol: float = 1e-4, metric: str = "l2") -> dict:
     """Tie-aware kNN parity report.
 
     A position whose index differs from the reference counts as a tie (and
@@ -159,7 +183,7 @@ def compare(got_dist, got_idx, ref_dist, ref_idx, x, q,
             report["identical"] += 1
             continue
         diff = np.nonzero(gi != ri)[0]
-        dg = direct_dist(x, q, np.full(diff.shape, r), gi[diff])
+        dg = direct_dist(x, q, np.full(diff.shape, r), gi[diff], metric)
         scale = np.maximum(np.abs(ref_dist[r, diff]), 1e-30)
         if np.all(np.abs(dg - ref_dist[r, diff]) <= tie_rtol * scale + 1e-12):
             report["tie_swaps"] += 1

@@ -116,16 +116,22 @@ int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int32_t me
                                 " must satisfy 1 <= k <= n=" + std::to_string(n));
   if (metric != TB_METRIC_L2 && metric != TB_METRIC_L1 && metric != TB_METRIC_COSINE)
     return fail(TB_ERR_ARG, "metric must be one of ('l2', 'l1', 'cosine')");
-  if (metric != TB_METRIC_L2)
-    return fail(TB_ERR_UNSUPPORTED, "only the l2 metric has a CUDA engine in this build");
   if ((dtype != TB_F32 && dtype != TB_F64) || (out_dtype != TB_F32 && out_dtype != TB_F64))
     return fail(TB_ERR_ARG, "unsupported dtype; only f32/f64 tensors exist");
   if (n >= (int64_t)INT_MAX - 1 || m >= (int64_t)INT_MAX)
     return fail(TB_ERR_UNSUPPORTED, "shard extents must be < 2^31 rows");
+  // l1 has no tensor-core form (CUDA-core engine); cosine runs on the
+  // tensor-core engines over unit-normalised rows
   if (engine == TB_ENGINE_AUTO)
-    engine = round_up(d, 64) <= tc_max_dpad() ? kAutoEngine : TB_ENGINE_SIMT;
+    engine = metric == TB_METRIC_L1 ? TB_ENGINE_SIMT
+             : round_up(d, 64) <= tc_max_dpad() || metric == TB_METRIC_COSINE ? kAutoEngine
+                                                                            : TB_ENGINE_SIMT;
   if (engine != TB_ENGINE_TC3 && engine != TB_ENGINE_SIMT && engine != TB_ENGINE_TC1)
     return fail(TB_ERR_ARG, "unknown engine");
+  if (metric == TB_METRIC_L1 && engine != TB_ENGINE_SIMT)
+    return fail(TB_ERR_UNSUPPORTED, "l1 has no tensor-core form: use engine 'simt' or 'auto'");
+  if (metric == TB_METRIC_COSINE && engine == TB_ENGINE_SIMT)
+    return fail(TB_ERR_UNSUPPORTED, "cosine runs on the tensor-core engines ('tc3', 'tc1')");
   const bool tc = engine != TB_ENGINE_SIMT;
   if (tc && round_up(d, 64) > tc_max_dpad())
     return fail(TB_ERR_UNSUPPORTED, "tcgen05 engines support d <= " +
@@ -323,7 +329,7 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
 
   TB_CUDA_TRY(cudaMemsetAsync(stats, 0, 256, st));
   if (tc) TB_CUDA_TRY(cudaMemsetAsync(gthr, 0xFF, p->m * 4, st));
-  int rc = launch_query_prep(p->dtype, q, p->m, p->d, qn64, qnorm, qhi, qlo,
+  int rc = launch_query_prep(p->dtype, p->metric, q, p->m, p->d, qn64, qnorm, qhi, qlo,
                              p->m_pad, p->d_pad, st);
   if (rc) return rc;
 
@@ -336,7 +342,7 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
     const int64_t rows_pad = round_up(rows, tile_rows);
     const char* xc = (const char*)x + c0 * p->d * es;
     if (ready && c < n_ready) TB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)ready[c], 0));
-    rc = launch_db_prep(p->dtype, xc, rows, p->d, xn, stats, xhi, xlo,
+    rc = launch_db_prep(p->dtype, p->metric, xc, rows, p->d, xn, stats, xhi, xlo,
                         rows_pad, p->d_pad, xext, st);
     if (rc) return rc;
     const int slices = (int)std::min<int64_t>(p->slices, ceil_div(rows, tile_rows));
@@ -348,7 +354,7 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
                          qhi, qlo, xext, rows, rows_pad, p->m, p->m_pad, p->d_pad,
                          lists, (int)c0, cs, ci, gthr, st);
     } else {
-      rc = launch_knn_simt(p->dtype, p->cand, xc, q, xn, rows, p->m, p->d,
+      rc = launch_knn_simt(p->dtype, p->metric, p->cand, xc, q, xn, rows, p->m, p->d,
                            slices, (int)c0, cs, ci, st);
     }
     if (rc) return rc;
@@ -372,16 +378,22 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
     dot_rel = 2.0 * std::ldexp(1.0, -8) + std::ldexp(1.0, -15) + (double)(p->d_pad + 16) * 2 * u24;
   double c1 = 2.0 * 2.0 * dot_rel;   // 2x safety, 2 for the -2 q.x
   double c2 = 2.0 * 4.0 * u24;        // ||x||^2 rounding + final FMA
+  if (p->metric == TB_METRIC_L1) {
+    // fp32 sum of d non-negative |q-x| terms: relative (d+2)u, plus the
+    // rounding of f64 inputs to fp32, u (|q|_1 + |x|_1); 2x safety
+    c1 = 2.0 * (double)(p->d + 2) * u24;
+    c2 = p->dtype == TB_F64 ? 2.0 * u24 : 0.0;
+  }
   // test hook: make every query uncertified to exercise the exact fallback
   if (const char* f = std::getenv("TB_FORCE_FALLBACK"))
     if (f[0] == '1') c1 = c2 = 1e300;
-  rc = launch_knn_refine(p->dtype, p->out_dtype, p->cand, prev_s, prev_i, x, q,
+  rc = launch_knn_refine(p->dtype, p->out_dtype, p->metric, p->cand, prev_s, prev_i, x, q,
                          qn64, qnorm, stats, p->n, p->m, p->d, p->k, c1, c2,
                          out_dist, out_idx, index_base, fb, st);
   if (rc) return rc;
   // the per-chunk candidate lists (kCandS, kCandI) are dead after the last
   // merge: the fallback uses them as scratch
-  return launch_knn_fallback(p->dtype, p->out_dtype, x, q, p->n, p->m, p->d, p->k, stats, fb,
+  return launch_knn_fallback(p->dtype, p->out_dtype, p->metric, x, q, p->n, p->m, p->d, p->k, stats, fb,
                              at(kCandS), p->off[kRunS] - p->off[kCandS], out_dist, out_idx,
                              index_base, st);
 }

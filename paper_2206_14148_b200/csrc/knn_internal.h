@@ -33,16 +33,16 @@ struct KnnDims {
 };
 
 // prep
-int launch_query_prep(int dtype, const void* q, int64_t m, int64_t d,
+int launch_query_prep(int dtype, int metric, const void* q, int64_t m, int64_t d,
                       double* qn64, float* qnorm, __nv_bfloat16* qhi,
                       __nv_bfloat16* qlo, int64_t m_pad, int64_t d_pad,
                       cudaStream_t st);
-int launch_db_prep(int dtype, const void* x, int64_t rows, int64_t d,
+int launch_db_prep(int dtype, int metric, const void* x, int64_t rows, int64_t d,
                    float* xn, unsigned* xmax_bits, __nv_bfloat16* xhi,
                    __nv_bfloat16* xlo, int64_t rows_pad, int64_t d_pad,
                    uint8_t* xext, cudaStream_t st);
 // SIMT candidate engine: writes lists [2*slices][m][cand]
-int launch_knn_simt(int dtype, int cand, const void* x_chunk, const void* q,
+int launch_knn_simt(int dtype, int metric, int cand, const void* x_chunk, const void* q,
                     const float* xn, int64_t rows, int64_t m, int64_t d,
                     int slices, int idx_base, float* cand_s, int* cand_i,
                     cudaStream_t st);
@@ -61,14 +61,14 @@ int launch_knn_merge(int cand, const float* in_s, const int* in_i, int lists,
                      const float* prev_s, const int* prev_i, int64_t m,
                      float* out_s, int* out_i, cudaStream_t st);
 // exact fp64 re-rank + certification
-int launch_knn_refine(int dtype, int out_dtype, int cand, const float* cs,
+int launch_knn_refine(int dtype, int out_dtype, int metric, int cand, const float* cs,
                       const int* ci, const void* x, const void* q,
                       const double* qn64, const float* qnorm,
                       const unsigned* stats, int64_t n, int64_t m, int64_t d,
                       int64_t k, double c1, double c2, void* out_dist,
                       int64_t* out_idx, int64_t index_base, int* fb_list,
                       cudaStream_t st);
-int launch_knn_fallback(int dtype, int out_dtype, const void* x, const void* q,
+int launch_knn_fallback(int dtype, int out_dtype, int metric, const void* x, const void* q,
                         int64_t n, int64_t m, int64_t d, int64_t k,
                         const unsigned* stats, const int* fb_list, void* scratch,
                         int64_t scratch_bytes, void* out_dist, int64_t* out_idx,

@@ -21,6 +21,8 @@ namespace tb {
 
 // One warp per row: ||row||^2 in fp64 and optional bf16 hi/lo split with
 // zero padding to [rows_pad, d_pad] (tensor-core operand layout, K-major).
+// L1 (metric == TB_METRIC_L1): acc = sum |v| and norm32 = ||row||_1 (for
+// the L1 error bound) instead of the squared L2 norm.
 template <typename T>
 __global__ void rows_prep_kernel(const T* __restrict__ src, int64_t rows,
                                  int64_t d, double* __restrict__ n64,
@@ -29,7 +31,7 @@ __global__ void rows_prep_kernel(const T* __restrict__ src, int64_t rows,
                                  unsigned* __restrict__ max_bits,
                                  __nv_bfloat16* __restrict__ hi,
                                  __nv_bfloat16* __restrict__ lo,
-                                 int64_t rows_pad, int64_t d_pad) {
+                                 int64_t rows_pad, int64_t d_pad, int metric) {
   const int lane = threadIdx.x & 31;
   const int64_t limit = hi ? rows_pad : rows;
   const int64_t cols = hi ? d_pad : d;
@@ -40,7 +42,7 @@ __global__ void rows_prep_kernel(const T* __restrict__ src, int64_t rows,
     double acc = 0.0;
     for (int64_t j = lane; j < cols; j += 32) {
       const double v = (r < rows && j < d) ? (double)src[r * d + j] : 0.0;
-      acc += v * v;
+      acc += metric == TB_METRIC_L1 ? fabs(v) : v * v;
       if (hi) {
         const __nv_bfloat16 h = __double2bfloat16(v);
         const __nv_bfloat16 l = __double2bfloat16(v - (double)__bfloat162float(h));
@@ -52,7 +54,7 @@ __global__ void rows_prep_kernel(const T* __restrict__ src, int64_t rows,
     if (lane == 0 && r < rows) {
       if (n64) n64[r] = acc;
       if (n32) n32[r] = (float)acc;
-      const float nrm = (float)sqrt(acc) * (1.0f + 1e-6f);
+      const float nrm = (float)(metric == TB_METRIC_L1 ? acc : sqrt(acc)) * (1.0f + 1e-6f);
       if (norm32) norm32[r] = nrm;
       wmax = fmaxf(wmax, nrm);
     }
@@ -65,7 +67,9 @@ __global__ void rows_prep_kernel(const T* __restrict__ src, int64_t rows,
 // 128, a full warp looping over 8-element segments beyond), 8 elements per
 // thread and step: 16-byte loads/stores of the bf16 hi/lo split, fp64 norms
 // reduced over the row's lanes, and one max-norm atomic per block.
-template <typename T, int G>
+// NORM (cosine): rows are first scaled to unit L2 norm (a pre-pass over the
+// row computes it), so the engine's ||x||^2 - 2 q.x ranks by cosine.
+template <typename T, int G, bool NORM>
 __global__ void __launch_bounds__(256)
 rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
                   double* __restrict__ n64, float* __restrict__ n32,
@@ -77,6 +81,17 @@ rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t r = gt / G;
   const int seg = (int)(gt % G);
+  double inv = 1.0;
+  if (NORM) {
+    double nn = 0.0;
+    for (int64_t c = (int64_t)seg; r < rows && c < d; c += G) {
+      const double v = (double)src[r * d + c];
+      nn = fma(v, v, nn);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+    inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+  }
   double acc = 0.0;
   for (int64_t c0 = (int64_t)seg * 8; r < rows_pad && c0 < d_pad; c0 += 8 * G) {
     double v[8];
@@ -94,8 +109,9 @@ rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
     __align__(16) __nv_bfloat16 l[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      acc = fma(v[j], v[j], acc);
-      const double sv = scale * v[j];          // exact (power-of-two scale)
+      const double u = NORM ? v[j] * inv : v[j];
+      acc = fma(u, u, acc);
+      const double sv = scale * u;             // scale: exact power of two
       h[j] = __double2bfloat16(sv);
       l[j] = __double2bfloat16(sv - (double)__bfloat162float(h[j]));
     }
@@ -150,7 +166,7 @@ template <typename T>
 static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
                      float* n32, float* norm32, unsigned* max_bits,
                      __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t rows_pad,
-                     int64_t d_pad, cudaStream_t st, double scale = 1.0,
+                     int64_t d_pad, cudaStream_t st, int metric, double scale = 1.0,
                      uint8_t* ext = nullptr) {
   const int64_t limit = hi ? rows_pad : rows;
   if (limit <= 0) return TB_OK;
@@ -158,48 +174,52 @@ static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
     const int G = d_pad == 64 ? 8 : d_pad == 128 ? 16 : 32;
     const int64_t threads = rows_pad * G;
     const unsigned blocks = (unsigned)ceil_div(threads, 256);
-    if (G == 8)
-      rows_split_kernel<T, 8><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32, norm32,
-                                                      max_bits, hi, lo, rows_pad, d_pad, scale,
-                                                      ext);
-    else if (G == 16)
-      rows_split_kernel<T, 16><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32, norm32,
-                                                       max_bits, hi, lo, rows_pad, d_pad, scale,
-                                                       ext);
-    else
-      rows_split_kernel<T, 32><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32, norm32,
-                                                       max_bits, hi, lo, rows_pad, d_pad, scale,
-                                                       ext);
+    const bool norm = metric == TB_METRIC_COSINE;
+#define TB_SPLIT(GG, NN)                                                                     \
+  rows_split_kernel<T, GG, NN><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32,     \
+                                                       norm32, max_bits, hi, lo, rows_pad,   \
+                                                       d_pad, scale, ext)
+    if (G == 8) {
+      if (norm) TB_SPLIT(8, true); else TB_SPLIT(8, false);
+    } else if (G == 16) {
+      if (norm) TB_SPLIT(16, true); else TB_SPLIT(16, false);
+    } else {
+      if (norm) TB_SPLIT(32, true); else TB_SPLIT(32, false);
+    }
+#undef TB_SPLIT
     TB_LAUNCH_CHECK("rows_split");
     return TB_OK;
   }
+  if (hi) return fail(TB_ERR_UNSUPPORTED, "tensor-core prep needs d_pad % 64 == 0");
   const int warps = 8;
   const int64_t blocks = std::min<int64_t>(ceil_div(limit, warps), 148 * 16);
   rows_prep_kernel<T><<<(unsigned)blocks, warps * 32, 0, st>>>(
-      (const T*)src, rows, d, n64, n32, norm32, max_bits, hi, lo, rows_pad, d_pad);
+      (const T*)src, rows, d, n64, n32, norm32, max_bits, hi, lo, rows_pad, d_pad, metric);
   TB_LAUNCH_CHECK("rows_prep");
   return TB_OK;
 }
 
-int launch_query_prep(int dtype, const void* q, int64_t m, int64_t d,
+int launch_query_prep(int dtype, int metric, const void* q, int64_t m, int64_t d,
                       double* qn64, float* qnorm, __nv_bfloat16* qhi,
                       __nv_bfloat16* qlo, int64_t m_pad, int64_t d_pad,
                       cudaStream_t st) {
   // the tensor-core engines use 2q (exact) so that acc' = 2 q.x - ||x||^2
   if (dtype == TB_F32)
-    return rows_prep<float>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st, 2.0);
-  return rows_prep<double>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st, 2.0);
+    return rows_prep<float>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st,
+                            metric, 2.0);
+  return rows_prep<double>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st,
+                           metric, 2.0);
 }
 
-int launch_db_prep(int dtype, const void* x, int64_t rows, int64_t d,
+int launch_db_prep(int dtype, int metric, const void* x, int64_t rows, int64_t d,
                    float* xn, unsigned* xmax_bits, __nv_bfloat16* xhi,
                    __nv_bfloat16* xlo, int64_t rows_pad, int64_t d_pad,
                    uint8_t* xext, cudaStream_t st) {
   if (dtype == TB_F32)
     return rows_prep<float>(x, rows, d, nullptr, xn, nullptr, xmax_bits, xhi, xlo, rows_pad, d_pad,
-                            st, 1.0, xext);
+                            st, metric, 1.0, xext);
   return rows_prep<double>(x, rows, d, nullptr, xn, nullptr, xmax_bits, xhi, xlo, rows_pad, d_pad,
-                           st, 1.0, xext);
+                           st, metric, 1.0, xext);
 }
 
 // ------------------------------------------------- SIMT candidate engine --
@@ -212,7 +232,9 @@ constexpr int kSimtLd = 132;   // padded k-major operand rows
 constexpr int kSimtSt = 129;   // padded score rows
 constexpr size_t kSimtSmem = (2 * 16 * kSimtLd + kSimtTile * kSimtSt) * sizeof(float);
 
-template <typename T, int KC>
+// L1 = true: the tile accumulates sum |q - x| (no tensor-core form) and the
+// score is that sum; otherwise the L2 cross term and ||x||^2 - 2 q.x.
+template <typename T, int KC, bool L1>
 __global__ void __launch_bounds__(256, 1)
 knn_simt_kernel(const T* __restrict__ x, const T* __restrict__ q,
                 const float* __restrict__ xn, int64_t rows, int m, int d,
@@ -274,7 +296,8 @@ knn_simt_kernel(const T* __restrict__ x, const T* __restrict__ q,
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < 8; ++j)
+            acc[i][j] = L1 ? acc[i][j] + fabsf(a[i] - b[j]) : fmaf(a[i], b[j], acc[i][j]);
       }
     }
     // epilogue: score = ||x||^2 - 2 q.x, staged for the scan
@@ -285,7 +308,7 @@ knn_simt_kernel(const T* __restrict__ x, const T* __restrict__ q,
         const int col = j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4);
         const int64_t g = t0 + col;
         St[(ty * 8 + i) * kSimtSt + col] =
-            g < r_end ? fmaf(-2.f, acc[i][j], xn[g]) : INFINITY;
+            g < r_end ? (L1 ? acc[i][j] : fmaf(-2.f, acc[i][j], xn[g])) : INFINITY;
       }
     __syncthreads();
     if (q0 + srow < m) {
@@ -315,34 +338,35 @@ knn_simt_kernel(const T* __restrict__ x, const T* __restrict__ q,
   }
 }
 
-template <typename T, int KC>
+template <typename T, int KC, bool L1>
 static int simt_launch(const void* x, const void* q, const float* xn,
                        int64_t rows, int64_t m, int64_t d, int slices,
                        int idx_base, float* cs, int* ci, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    TB_CUDA_TRY(cudaFuncSetAttribute(knn_simt_kernel<T, KC>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kSimtSmem));
-    configured = true;
-  }
+  TB_CUDA_TRY(cudaFuncSetAttribute(knn_simt_kernel<T, KC, L1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kSimtSmem));
   const int64_t rps = round_up(ceil_div(rows, slices), kSimtTile);
   dim3 grid((unsigned)ceil_div(m, kSimtTile), (unsigned)slices);
-  knn_simt_kernel<T, KC><<<grid, 256, kSimtSmem, st>>>(
+  knn_simt_kernel<T, KC, L1><<<grid, 256, kSimtSmem, st>>>(
       (const T*)x, (const T*)q, xn, rows, (int)m, (int)d, rps, idx_base, cs, ci);
   TB_LAUNCH_CHECK("knn_simt");
   return TB_OK;
 }
 
-int launch_knn_simt(int dtype, int cand, const void* x, const void* q,
+int launch_knn_simt(int dtype, int metric, int cand, const void* x, const void* q,
                     const float* xn, int64_t rows, int64_t m, int64_t d,
                     int slices, int idx_base, float* cs, int* ci,
                     cudaStream_t st) {
-#define TB_SIMT_CASE(KC)                                                       \
-  case KC:                                                                     \
-    return dtype == TB_F32                                                     \
-               ? simt_launch<float, KC>(x, q, xn, rows, m, d, slices, idx_base, cs, ci, st) \
-               : simt_launch<double, KC>(x, q, xn, rows, m, d, slices, idx_base, cs, ci, st);
+  if (metric == TB_METRIC_COSINE)
+    return fail(TB_ERR_UNSUPPORTED, "SIMT engine: cosine runs on the tensor-core engine");
+  const bool l1 = metric == TB_METRIC_L1;
+#define TB_SIMT_CASE(KC)                                                                     \
+  case KC:                                                                                   \
+    if (dtype == TB_F32)                                                                     \
+      return l1 ? simt_launch<float, KC, true>(x, q, xn, rows, m, d, slices, idx_base, cs, ci, st) \
+                : simt_launch<float, KC, false>(x, q, xn, rows, m, d, slices, idx_base, cs, ci, st); \
+    return l1 ? simt_launch<double, KC, true>(x, q, xn, rows, m, d, slices, idx_base, cs, ci, st) \
+              : simt_launch<double, KC, false>(x, q, xn, rows, m, d, slices, idx_base, cs, ci, st);
   switch (cand) {
     TB_SIMT_CASE(16)
     TB_SIMT_CASE(32)
@@ -399,6 +423,35 @@ int launch_knn_merge(int cand, const float* in_s, const int* in_i, int lists,
   return TB_OK;
 }
 
+// Exact fp64 distance of one (query row, data row) pair in the reference
+// graph's formula (frontend.py:57-73): sum (q-x)^2, sum |q-x|, or
+// 1 - q.x / (|q| |x|).  Warp-cooperative (lane-strided over d); every lane
+// returns the same value.
+template <typename T, int MET>
+__device__ __forceinline__ double exact_dist_warp(const T* __restrict__ qr,
+                                                  const T* __restrict__ xr, int64_t d,
+                                                  int lane) {
+  if (MET == TB_METRIC_COSINE) {
+    double dot = 0.0, qq = 0.0, xx = 0.0;
+    for (int64_t t = lane; t < d; t += 32) {
+      const double a = (double)qr[t], b = (double)xr[t];
+      dot = fma(a, b, dot);
+      qq = fma(a, a, qq);
+      xx = fma(b, b, xx);
+    }
+    dot = warp_sum(dot);
+    qq = warp_sum(qq);
+    xx = warp_sum(xx);
+    return 1.0 - dot / (sqrt(qq) * sqrt(xx));
+  }
+  double acc = 0.0;
+  for (int64_t t = lane; t < d; t += 32) {
+    const double df = (double)qr[t] - (double)xr[t];
+    acc = MET == TB_METRIC_L1 ? acc + fabs(df) : fma(df, df, acc);
+  }
+  return warp_sum(acc);
+}
+
 // --------------------------------------------- exact re-rank + certify --
 // One warp per query.  Exact fp64 sum((q - x)^2) for the K' candidates,
 // sorted by (distance, index); the k best are the answer.  Certified when
@@ -406,8 +459,11 @@ int launch_knn_merge(int cand, const float* in_s, const int* in_i, int lists,
 //   approx(j) >= T* (K'-th merged approx score)   and
 //   |approx - exact| <= E = c1 ||q|| max||x|| + c2 max||x||^2
 // => need T* - E > exact_score(k-th).  Otherwise the query goes to the
-// exact fallback.
-template <typename T, typename OT, int KC>
+// exact fallback.  Per metric (engine score s~ vs exact distance):
+//   l2:     s~ = ||x||^2 - 2q.x,        E = c1 |q| X + c2 X^2, score_k = kth - ||q||^2
+//   cosine: s~ = 1 - 2 q^.x^ (unit rows), same E with |q| = X = 1, score_k = 2 kth - 1
+//   l1:     s~ = fp32 sum |q-x| (SIMT):  outside s >= s~/(1+c1) - c2 (|q|_1 + X_1)
+template <typename T, typename OT, int KC, int MET>
 __global__ void knn_refine_kernel(const float* __restrict__ cs,
                                   const int* __restrict__ ci,
                                   const T* __restrict__ x, const T* __restrict__ q,
@@ -433,14 +489,7 @@ __global__ void knn_refine_kernel(const float* __restrict__ cs,
   for (int c = 0; c < KC; ++c) {
     const int j = ci[r * KC + c];
     double acc = 0.0;
-    if (j != kInvalidIdx) {
-      const T* xr = x + (int64_t)j * d;
-      for (int64_t t = lane; t < d; t += 32) {
-        const double df = (double)qr[t] - (double)xr[t];
-        acc = fma(df, df, acc);
-      }
-    }
-    acc = warp_sum(acc);
+    if (j != kInvalidIdx) acc = exact_dist_warp<T, MET>(qr, x + (int64_t)j * d, d, lane);
     if ((c & 31) == lane) {
 #pragma unroll
       for (int p = 0; p < PER; ++p)
@@ -477,9 +526,15 @@ __global__ void knn_refine_kernel(const float* __restrict__ cs,
     const float tstar = cs[r * KC + KC - 1];
     if (isfinite(tstar)) {
       const double X = (double)__uint_as_float(stats[0]);
-      const double E = c1 * (double)qnorm[r] * X + c2 * X * X;
-      const double exact_score_k = kth - qn64[r];
-      if (!((double)tstar - E > exact_score_k)) {
+      bool ok;
+      if (MET == TB_METRIC_L1) {
+        ok = (double)tstar / (1.0 + c1) - c2 * ((double)qnorm[r] + X) > kth;
+      } else {
+        const double E = c1 * (double)qnorm[r] * X + c2 * X * X;
+        const double exact_score_k = MET == TB_METRIC_COSINE ? 2.0 * kth - 1.0 : kth - qn64[r];
+        ok = (double)tstar - E > exact_score_k;
+      }
+      if (!ok) {
         const int pos = atomicAdd(reinterpret_cast<int*>(&stats[1]), 1);
         fb_list[pos] = (int)r;
       }
@@ -487,7 +542,7 @@ __global__ void knn_refine_kernel(const float* __restrict__ cs,
   }
 }
 
-template <typename T, typename OT>
+template <typename T, typename OT, int MET>
 static int refine_dispatch(int cand, const float* cs, const int* ci,
                            const void* x, const void* q, const double* qn64,
                            const float* qnorm, unsigned* stats, int64_t m,
@@ -498,7 +553,7 @@ static int refine_dispatch(int cand, const float* cs, const int* ci,
   const unsigned blocks = (unsigned)ceil_div(m, warps);
 #define TB_REFINE_CASE(KC)                                                   \
   case KC:                                                                   \
-    knn_refine_kernel<T, OT, KC><<<blocks, warps * 32, 0, st>>>(             \
+    knn_refine_kernel<T, OT, KC, MET><<<blocks, warps * 32, 0, st>>>(        \
         cs, ci, (const T*)x, (const T*)q, qn64, qnorm, stats, m, d, (int)k,  \
         c1, c2, (OT*)od, oi, base, fb);                                      \
     break;
@@ -513,7 +568,7 @@ static int refine_dispatch(int cand, const float* cs, const int* ci,
   return TB_OK;
 }
 
-int launch_knn_refine(int dtype, int out_dtype, int cand, const float* cs,
+int launch_knn_refine(int dtype, int out_dtype, int metric, int cand, const float* cs,
                       const int* ci, const void* x, const void* q,
                       const double* qn64, const float* qnorm,
                       const unsigned* stats, int64_t n, int64_t m, int64_t d,
@@ -523,14 +578,21 @@ int launch_knn_refine(int dtype, int out_dtype, int cand, const float* cs,
   (void)n;
   if (m <= 0) return TB_OK;
   unsigned* s = const_cast<unsigned*>(stats);
+#define TB_REF(T, OT, MET)                                                                  \
+  return refine_dispatch<T, OT, MET>(cand, cs, ci, x, q, qn64, qnorm, s, m, d, k, c1, c2,   \
+                                     out_dist, out_idx, index_base, fb_list, st)
+#define TB_REF_MET(T, OT)                                        \
+  if (metric == TB_METRIC_L1) TB_REF(T, OT, TB_METRIC_L1);       \
+  if (metric == TB_METRIC_COSINE) TB_REF(T, OT, TB_METRIC_COSINE); \
+  TB_REF(T, OT, TB_METRIC_L2)
   if (dtype == TB_F32) {
-    if (out_dtype == TB_F32)
-      return refine_dispatch<float, float>(cand, cs, ci, x, q, qn64, qnorm, s, m, d, k, c1, c2, out_dist, out_idx, index_base, fb_list, st);
-    return refine_dispatch<float, double>(cand, cs, ci, x, q, qn64, qnorm, s, m, d, k, c1, c2, out_dist, out_idx, index_base, fb_list, st);
+    if (out_dtype == TB_F32) { TB_REF_MET(float, float); }
+    TB_REF_MET(float, double);
   }
-  if (out_dtype == TB_F32)
-    return refine_dispatch<double, float>(cand, cs, ci, x, q, qn64, qnorm, s, m, d, k, c1, c2, out_dist, out_idx, index_base, fb_list, st);
-  return refine_dispatch<double, double>(cand, cs, ci, x, q, qn64, qnorm, s, m, d, k, c1, c2, out_dist, out_idx, index_base, fb_list, st);
+  if (out_dtype == TB_F32) { TB_REF_MET(double, float); }
+  TB_REF_MET(double, double);
+#undef TB_REF_MET
+#undef TB_REF
 }
 
 // ------------------------------------------------- exact fp64 fallback --
@@ -542,7 +604,7 @@ int launch_knn_refine(int dtype, int out_dtype, int cand, const float* cs,
 // share them through L2).  One warp per database row (lane-strided over d,
 // coalesced), a per-warp top-KC, merged per block into scratch[u]; then
 // knn_fallback_merge combines the S lists of each query.
-template <typename T, int KC>
+template <typename T, int KC, int MET>
 __global__ void __launch_bounds__(256)
 knn_fallback_partial_kernel(const T* __restrict__ x, const T* __restrict__ q, int64_t n,
                             int64_t d, const unsigned* __restrict__ stats,
@@ -562,16 +624,8 @@ knn_fallback_partial_kernel(const T* __restrict__ x, const T* __restrict__ q, in
     const int64_t j0 = n * slice / S, j1 = n * (slice + 1) / S;
     TopList<double, KC> L;
     L.init();
-    for (int64_t j = j0 + warp; j < j1; j += 8) {
-      const T* xr = x + j * d;
-      double acc = 0.0;
-      for (int64_t t = lane; t < d; t += 32) {
-        const double df = (double)qr[t] - (double)xr[t];
-        acc = fma(df, df, acc);
-      }
-      acc = warp_sum(acc);
-      L.offer(acc, (int)j);      // identical in every lane
-    }
+    for (int64_t j = j0 + warp; j < j1; j += 8)
+      L.offer(exact_dist_warp<T, MET>(qr, x + j * d, d, lane), (int)j);   // same in every lane
     if (lane == 0)
       for (int t = 0; t < KC; ++t) {
         sd[warp][t] = L.s[t];
@@ -618,7 +672,7 @@ __global__ void knn_fallback_merge_kernel(const unsigned* __restrict__ stats,
   }
 }
 
-template <typename T, typename OT, int KC>
+template <typename T, typename OT, int KC, int MET>
 static int fallback_launch(const void* x, const void* q, int64_t n, int64_t d, int64_t k,
                            const unsigned* stats, const int* fb, void* scratch,
                            int64_t scratch_bytes, int64_t m, void* od, int64_t* oi,
@@ -632,7 +686,7 @@ static int fallback_launch(const void* x, const void* q, int64_t n, int64_t d, i
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(4 * sms, cap));
   double* sc_d = (double*)scratch;
   int* sc_i = (int*)(sc_d + cap * KC);
-  knn_fallback_partial_kernel<T, KC><<<G, 256, 0, st>>>((const T*)x, (const T*)q, n, d, stats,
+  knn_fallback_partial_kernel<T, KC, MET><<<G, 256, 0, st>>>((const T*)x, (const T*)q, n, d, stats,
                                                         fb, sc_d, sc_i);
   TB_LAUNCH_CHECK("knn_fallback_partial");
   knn_fallback_merge_kernel<OT, KC><<<(unsigned)ceil_div(m, 8), 256, 0, st>>>(
@@ -641,38 +695,43 @@ static int fallback_launch(const void* x, const void* q, int64_t n, int64_t d, i
   return TB_OK;
 }
 
-template <typename T, typename OT>
+template <typename T, typename OT, int MET>
 static int fallback_dispatch(const void* x, const void* q, int64_t n, int64_t d, int64_t k,
                              const unsigned* stats, const int* fb, void* scratch,
                              int64_t scratch_bytes, int64_t m, void* od, int64_t* oi,
                              int64_t base, cudaStream_t st) {
   if (k <= 16)
-    return fallback_launch<T, OT, 16>(x, q, n, d, k, stats, fb, scratch, scratch_bytes, m, od,
-                                      oi, base, st);
+    return fallback_launch<T, OT, 16, MET>(x, q, n, d, k, stats, fb, scratch, scratch_bytes, m,
+                                           od, oi, base, st);
   if (k <= 32)
-    return fallback_launch<T, OT, 32>(x, q, n, d, k, stats, fb, scratch, scratch_bytes, m, od,
-                                      oi, base, st);
+    return fallback_launch<T, OT, 32, MET>(x, q, n, d, k, stats, fb, scratch, scratch_bytes, m,
+                                           od, oi, base, st);
   if (k <= 64)
-    return fallback_launch<T, OT, 64>(x, q, n, d, k, stats, fb, scratch, scratch_bytes, m, od,
-                                      oi, base, st);
+    return fallback_launch<T, OT, 64, MET>(x, q, n, d, k, stats, fb, scratch, scratch_bytes, m,
+                                           od, oi, base, st);
   return fail(TB_ERR_UNSUPPORTED, "fallback: k > 64");
 }
 
-int launch_knn_fallback(int dtype, int out_dtype, const void* x, const void* q,
+int launch_knn_fallback(int dtype, int out_dtype, int metric, const void* x, const void* q,
                         int64_t n, int64_t m, int64_t d, int64_t k,
                         const unsigned* stats, const int* fb_list, void* scratch,
                         int64_t scratch_bytes, void* out_dist, int64_t* out_idx,
                         int64_t index_base, cudaStream_t st) {
   if (m <= 0) return TB_OK;
-#define TB_FB(T, OT)                                                                           \
-  return fallback_dispatch<T, OT>(x, q, n, d, k, stats, fb_list, scratch, scratch_bytes, m,    \
-                                  out_dist, out_idx, index_base, st)
+#define TB_FB(T, OT, MET)                                                                     \
+  return fallback_dispatch<T, OT, MET>(x, q, n, d, k, stats, fb_list, scratch, scratch_bytes, \
+                                       m, out_dist, out_idx, index_base, st)
+#define TB_FB_MET(T, OT)                                          \
+  if (metric == TB_METRIC_L1) TB_FB(T, OT, TB_METRIC_L1);         \
+  if (metric == TB_METRIC_COSINE) TB_FB(T, OT, TB_METRIC_COSINE); \
+  TB_FB(T, OT, TB_METRIC_L2)
   if (dtype == TB_F32) {
-    if (out_dtype == TB_F32) TB_FB(float, float);
-    TB_FB(float, double);
+    if (out_dtype == TB_F32) { TB_FB_MET(float, float); }
+    TB_FB_MET(float, double);
   }
-  if (out_dtype == TB_F32) TB_FB(double, float);
-  TB_FB(double, double);
+  if (out_dtype == TB_F32) { TB_FB_MET(double, float); }
+  TB_FB_MET(double, double);
+#undef TB_FB_MET
 #undef TB_FB
 }
 

@@ -105,6 +105,7 @@ class KnnOperator:
                          engine=engine, memory_limit=memory_limit,
                          resident_bytes=resident_bytes, max_chunk_rows=max_chunk_rows)
         self.device = torch.device(device or "cuda")
+        self.metric = metric
         self.dtype = np.dtype(dtype)
         self.out_dtype = np.dtype(out_dtype or dtype)
         self.workspace = torch.empty(max(int(self.plan.workspace_bytes), 1),
@@ -113,6 +114,15 @@ class KnnOperator:
     def _torch_dtype(self, dt):
         torch = _torch()
         return torch.float32 if np.dtype(dt) == np.float32 else torch.float64
+
+    def _check_cosine(self, x, q):
+        """Cosine distance is undefined for all-zero rows: the reference
+        rejects them with ValueError (frontend.py:126-135)."""
+        if self.metric != "cosine":
+            return
+        for t in (x, q):
+            if bool((t.abs().amax(dim=1) == 0).any()):
+                raise ValueError("cosine distance is undefined for zero rows")
 
     def alloc_outputs(self):
         torch = _torch()
@@ -133,6 +143,7 @@ class KnnOperator:
                 raise EvaluationError(f"{name} dtype {t.dtype} != planned {self.dtype}")
             if not t.is_cuda or not t.is_contiguous():
                 raise EvaluationError(f"{name} must be a contiguous CUDA tensor")
+        self._check_cosine(x, q)
         dist, idx = out if out is not None else self.alloc_outputs()
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         ev_arr, n_ev = None, 0
@@ -162,6 +173,7 @@ class KnnOperator:
                                       f"{(int(rows), int(p.d))}")
             if t.dtype != self._torch_dtype(self.dtype):
                 raise EvaluationError(f"{name} dtype {t.dtype} != planned {self.dtype}")
+        self._check_cosine(xh, qh)
         if staging is None:
             if getattr(self, "_staging", None) is None:
                 td = self._torch_dtype(self.dtype)
@@ -196,7 +208,9 @@ class KnnOperator:
 
 def knn(x, q, k: int, *, metric: str = "l2", memory_limit=None, engine: str = "auto",
         index_base: int = 0, out_dtype=None, return_result: bool = False):
-    """k nearest database rows of every query row, smallest squared L2 first.
+    """k nearest database rows of every query row, smallest distance first
+    (``metric``: "l2" squared Euclidean, "l1", or "cosine" = 1 - cos, the
+    reference's three metrics, frontend.py:19,57-73).
 
     x[n, d] database, q[m, d] queries (f32 or f64; numpy arrays or CUDA
     tensors).  Returns (dist[m, k], idx[m, k] int64) in the input's kind

@@ -39,10 +39,10 @@ def sha(*arrays) -> str:
     return h.hexdigest()
 
 
-def ref_knn(x, q, k, threshold=None):
+def ref_knn(x, q, k, threshold=None, metric="l2"):
     x = np.asarray(x, np.float64)
     q = np.asarray(q, np.float64)
-    g = tb.build_knn(x.shape[0], q.shape[0], x.shape[1], k, "l2", tb.DType.F64)
+    g = tb.build_knn(x.shape[0], q.shape[0], x.shape[1], k, metric, tb.DType.F64)
     if threshold is not None:
         g = tb.run_pipeline(g, tb.PassConfig(tensor_size_threshold=threshold))
     t0 = time.perf_counter()
@@ -136,5 +136,35 @@ def main():
     save("budget.npz", naive_requested=requested, knn_c1_naive_peak=est)
 
 
+def metrics():
+    """L1 and cosine kNN (frontend.py:57-73 naive forms, TopK of
+    interpreter.py:371-390) on the reference, naive and query-split."""
+    out = {}
+    # reference random_inputs style U[-1, 1]
+    x, q = synthetic.uniform_inputs([(3000, 16), (100, 16)], seed=4)
+    for metric in ("l1", "cosine"):
+        d, i, _, _ = ref_knn(x, q, 10, metric=metric)
+        dp, ip, _, _ = ref_knn(x, q, 10, threshold=2 * 10**6, metric=metric)
+        assert np.array_equal(i, ip)
+        out[f"{metric}_uniform_dist"], out[f"{metric}_uniform_idx"] = d, i
+    out["uniform_x"], out["uniform_q"] = x, q
+    # ties: small integer lattice (L1) and scaled copies of directions (cosine)
+    rng = np.random.default_rng(6)
+    x = rng.integers(0, 4, (2000, 3)).astype(np.float64)
+    q = rng.integers(0, 4, (50, 3)).astype(np.float64)
+    d, i, _, _ = ref_knn(x, q, 10, metric="l1")
+    out["l1_ties_x"], out["l1_ties_q"], out["l1_ties_dist"], out["l1_ties_idx"] = x, q, d, i
+    base = rng.integers(1, 4, (400, 3)).astype(np.float64)
+    x = np.concatenate([base, 2.0 * base, 3.0 * base])[rng.permutation(1200)]
+    q = rng.integers(1, 4, (40, 3)).astype(np.float64)
+    d, i, _, _ = ref_knn(x, q, 10, metric="cosine")
+    out["cos_ties_x"], out["cos_ties_q"], out["cos_ties_dist"], out["cos_ties_idx"] = x, q, d, i
+    save("knn_metrics.npz", **out)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["metrics"]:
+        metrics()
+    else:
+        main()
+        metrics()

@@ -264,3 +264,72 @@ def test_run_host_pipelined_matches_device_run(chunk):
     assert np.array_equal(ih.numpy(), idd.cpu().numpy())
     ref_d, ref_i = oknn.exact(x, q, 10)
     assert oknn.compare(dh.numpy(), ih.numpy(), ref_d, ref_i, x, q)["ok"]
+
+
+# ---------------------------------------------------------------- metrics --
+# L1 (CUDA-core engine: no tensor-core form) and cosine (tensor cores over
+# unit-normalised rows), the reference's other two metrics
+# (frontend.py:19,57-73), exact against the reference's own answers.
+
+def mcheck(dist, idx, ref_d, ref_i, x, q, metric):
+    rep = oknn.compare(dist, idx, ref_d, ref_i, x, q, metric=metric)
+    assert rep["ok"], rep
+    return rep
+
+
+@pytest.mark.parametrize("metric,case", [("l1", "uniform"), ("cosine", "uniform"),
+                                         ("l1", "l1_ties"), ("cosine", "cos_ties")])
+def test_metric_reference_goldens(metric, case):
+    g = golden("knn_metrics.npz")
+    if case == "uniform":
+        x, q = g["uniform_x"], g["uniform_q"]
+        rd, ri = g[f"{metric}_uniform_dist"], g[f"{metric}_uniform_idx"]
+    else:
+        x, q, rd, ri = g[f"{case}_x"], g[f"{case}_q"], g[f"{case}_dist"], g[f"{case}_idx"]
+    for dt in (np.float64, np.float32):
+        dist, idx = tb.knn(x.astype(dt), q.astype(dt), 10, metric=metric)
+        if dt == np.float64:
+            assert np.array_equal(idx, ri)          # ties resolve exactly as the reference
+            assert rel_err(dist, rd) < 1e-12
+        else:
+            rd32, ri32 = oknn.exact(x.astype(dt), q.astype(dt), 10, metric=metric)
+            mcheck(dist, idx, rd32, ri32, x.astype(dt), q.astype(dt), metric)
+
+
+@pytest.mark.parametrize("metric,n,m,d", [("l1", 30000, 200, 64), ("cosine", 30000, 200, 64),
+                                          ("cosine", 20000, 130, 300), ("l1", 6000, 70, 300)])
+def test_metric_random_vs_oracle(metric, n, m, d):
+    x, q = synthetic.gaussian_knn(n, m, d, seed=n + d)
+    ref_d, ref_i = oknn.exact(x, q, 10, metric=metric)
+    res = tb.knn(x, q, 10, metric=metric, return_result=True)
+    mcheck(res.dist, res.idx, ref_d, ref_i, x, q, metric)
+    assert res.fallback_queries == 0
+
+
+@pytest.mark.parametrize("metric", ["l1", "cosine"])
+def test_metric_fallback_and_chunking_exact(metric, monkeypatch):
+    x, q = synthetic.gaussian_knn(9000, 90, 24, seed=5)
+    ref_d, ref_i = oknn.exact(x, q, 7, metric=metric)
+    resident = (9000 + 90) * 24 * 4
+    d1, i1 = tb.knn(x, q, 7, metric=metric, memory_limit=resident + 3_000_000)
+    mcheck(d1, i1, ref_d, ref_i, x, q, metric)
+    monkeypatch.setenv("TB_FORCE_FALLBACK", "1")
+    res = tb.knn(x, q, 7, metric=metric, return_result=True)
+    assert res.fallback_queries == 90
+    mcheck(res.dist, res.idx, ref_d, ref_i, x, q, metric)
+
+
+def test_metric_engine_rules_and_zero_rows():
+    x, q = synthetic.gaussian_knn(500, 5, 8, seed=1)
+    with pytest.raises(tb.KernelUnavailable):
+        tb.knn(x, q, 3, metric="l1", engine="tc3")
+    with pytest.raises(tb.KernelUnavailable):
+        tb.knn(x, q, 3, metric="cosine", engine="simt")
+    x[7] = 0.0
+    with pytest.raises(ValueError, match="zero rows"):
+        tb.knn(x, q, 3, metric="cosine")
+    graph = tb.build_knn(500, 5, 8, 3, metric="l1")
+    x, q = x.astype(np.float64), q.astype(np.float64)
+    (vals, idx), _ = tb.evaluate(graph, [x, q])
+    rd, ri = oknn.exact(x, q, 3, metric="l1")
+    assert np.array_equal(np.asarray(idx.array).astype(np.int64), ri)
