@@ -372,9 +372,12 @@ int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel, int32
   plan->N = N; plan->M = M; plan->dim = dim; plan->kernel = kernel; plan->dtype = dtype;
   plan->memory_limit = memory_limit; plan->resident_bytes = resident_bytes;
   plan->engine = engine;
-  const int64_t M_pad = round_up(M, kSyrkTile);
-  plan->M_pad = M_pad;
   const bool i8 = engine == TB_SGPR_ENGINE_I8;
+  // TB_I8_PAIR=1 (opt-in CTA-pair Gram) needs 256-row pair tiles
+  const char* pair_env = std::getenv("TB_I8_PAIR");
+  const bool pair = i8 && pair_env && pair_env[0] == '1';
+  const int64_t M_pad = round_up(M, pair ? 2 * kI8Tile : kSyrkTile);
+  plan->M_pad = M_pad;
   plan->sigma_layout = i8 ? TB_SIGMA_TILES : TB_SIGMA_FULL;
   plan->sigma_bytes = i8 ? i8_tiles(M_pad) * kI8Tile * kI8Tile * 8 : M * M * 8;
   plan->output_bytes = plan->sigma_bytes + M * 8 + 8;

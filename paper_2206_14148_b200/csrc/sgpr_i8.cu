@@ -370,6 +370,258 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ------------------------------------------------- gram_i8, CTA pairs --
+// The same statistics with tcgen05.mma.cta_group::2: a cluster of two CTAs
+// on one TPC computes a 256 x 128 pair tile (rows 256 I + 128 rank, cols
+// 128 J); the leader (rank 0) issues M256.N128.K32 MMAs that use both SMs'
+// tensor cores, each CTA holding its 128 rows of A and half (64 rows) of B.
+// Per SM this halves the MMA instructions the single issuing thread must
+// push (the 1-SM kernel's limiter) and cuts TMA bytes per k-block from 48 to
+// 36 KB.  TMEM per CTA is unchanged: 4 s32 accumulators x 128 columns.
+// Protocol: "full" barriers live in the leader and receive the tx bytes of
+// both CTAs' loads (leader arms expect_tx for both); "empty" and the
+// accumulator-ready barriers are arrived in both CTAs by multicast commits;
+// the epilogue warps of both CTAs arrive on the leader's acc0_free / tempty.
+constexpr int kP2Stages = 6;
+constexpr uint32_t kP2ATile = kI8Tile * kI8KB;             // 8 KB: 128 rows x 64 B
+constexpr uint32_t kP2BTile = (kI8Tile / 2) * kI8KB;       // 4 KB: 64 rows x 64 B
+constexpr uint32_t kP2Stage = 3 * (kP2ATile + kP2BTile);   // 36 KB
+constexpr size_t kP2Smem = 1024 + (size_t)kP2Stages * kP2Stage + 512;
+constexpr int kP2SbI = 6, kP2SbJ = 12;                     // super-block of pair tiles
+
+// pair unit u -> (I, J), J <= 2I + 1, grouped in 6 x 12 super-blocks
+__device__ __forceinline__ void pair_of_unit(int u, int nI, int& I, int& J) {
+  for (int I0 = 0; I0 < nI; I0 += kP2SbI) {
+    const int I1 = min(nI, I0 + kP2SbI);
+    for (int J0 = 0; J0 <= 2 * (I1 - 1) + 1; J0 += kP2SbJ) {
+      const int J1 = min(2 * nI, J0 + kP2SbJ);
+      for (int i = I0; i < I1; ++i) {
+        const int c = max(0, min(J1, 2 * i + 2) - J0);
+        if (u < c) {
+          I = i;
+          J = J0 + u;
+          return;
+        }
+        u -= c;
+      }
+    }
+  }
+  I = J = 0;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
+sgpr_gram_i8_pair_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
+                         int units, int nkb, int m_pad, double scale, double* __restrict__ sig,
+                         int dbg) {
+  constexpr int S = kP2Stages;
+  const int nt = m_pad / kI8Tile, nI = m_pad / (2 * kI8Tile);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * kP2Stage);
+  uint64_t* empty = full + S;
+  uint64_t* tfull_a = empty + S;
+  uint64_t* acc0_free = tfull_a + 1;
+  uint64_t* tfull_b = acc0_free + 1;
+  uint64_t* tempty = tfull_b + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull_a, 1);
+    mbar_init(acc0_free, 2 * kI8EpiWarps);   // one arrive per epilogue warp, both CTAs
+    mbar_init(tfull_b, 1);
+    mbar_init(tempty, 2 * kI8EpiWarps);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();               // barriers of both CTAs initialised before any remote use
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      tma_prefetch(&tma);
+      tma_prefetch(&tmb);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = pair; u < units; u += npairs) {
+        int I, J;
+        pair_of_unit(u, nI, I, J);
+        const int ra = I * 2 * kI8Tile + rank * kI8Tile;
+        const int rb = J * kI8Tile + rank * (kI8Tile / 2);
+        for (int phase = 0; phase < 2; ++phase) {
+          const int step = phase ? 3 : 1;
+          for (int kb = 0; kb < nkb; kb += step) {
+            mbar_wait(&empty[s], ph ^ 1);
+            const uint32_t fb = mapa_shared(&full[s], 0);     // the leader's barrier
+            uint8_t* st = smem + (size_t)s * kP2Stage;
+            const int nk = phase ? min(3, nkb - kb) : 1;
+            if (dbg == 1) {
+              if (rank == 0) mbar_arrive(&full[s]);
+            } else {
+            // the leader arms its own barrier for both CTAs' bytes
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * (phase ? nk * (kP2ATile + kP2BTile) : kP2Stage));
+            if (phase == 0) {
+              for (int pl = 2; pl >= 0; --pl) {
+                uint8_t* t = st + (2 - pl) * (kP2ATile + kP2BTile);
+                tma_load_2d_2sm(t, &tma, fb, kb * kI8KB, pl * m_pad + ra);
+                tma_load_2d_2sm(t + kP2ATile, &tmb, fb, kb * kI8KB, pl * m_pad + rb);
+              }
+            } else {
+              for (int j = 0; j < nk; ++j) {
+                uint8_t* t = st + j * (kP2ATile + kP2BTile);
+                tma_load_2d_2sm(t, &tma, fb, (kb + j) * kI8KB, ra);
+                tma_load_2d_2sm(t + kP2ATile, &tmb, fb, (kb + j) * kI8KB, rb);
+              }
+            }
+            }
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_u8_s32(2 * kI8Tile, kI8Tile);   // M256 N128
+      const uint32_t acc0 = tmem, acc1 = tmem + 128, acc2 = tmem + 256, acc3 = tmem + 384;
+      const uint64_t d0 = desc_k_sw64(smem_u32(smem));
+      constexpr uint64_t kStageD = kP2Stage >> 4, kAD = kP2ATile >> 4, kPairD = (kP2ATile + kP2BTile) >> 4;
+      int s = 0;
+      uint32_t ph = 0;
+      int i = 0;
+      for (int u = pair; u < units; u += npairs, ++i) {
+        mbar_wait(tempty, (i & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t a2 = d0 + (uint64_t)s * kStageD, b2 = a2 + kAD;
+          const uint64_t a1 = a2 + kPairD, b1 = a1 + kAD;
+          const uint64_t a0 = a1 + kPairD, b0 = a0 + kAD;
+          const uint32_t acc = kb ? 1u : 0u;
+          if (dbg != 2) {
+          mma_i8_2sm(acc0, a2, b2, idesc, acc);
+          mma_i8_2sm(acc1, a2, b1, idesc, acc);
+          mma_i8_2sm(acc1, a1, b2, idesc, 1);
+          mma_i8_2sm(acc2, a2, b0, idesc, acc);
+          mma_i8_2sm(acc2, a1, b1, idesc, 1);
+          mma_i8_2sm(acc2, a0, b2, idesc, 1);
+          mma_i8_2sm(acc3, a1, b0, idesc, acc);
+          mma_i8_2sm(acc3, a0, b1, idesc, 1);
+          mma_i8_2sm(acc0, a2 + 2, b2 + 2, idesc, 1);
+          mma_i8_2sm(acc1, a2 + 2, b1 + 2, idesc, 1);
+          mma_i8_2sm(acc1, a1 + 2, b2 + 2, idesc, 1);
+          mma_i8_2sm(acc2, a2 + 2, b0 + 2, idesc, 1);
+          mma_i8_2sm(acc2, a1 + 2, b1 + 2, idesc, 1);
+          mma_i8_2sm(acc2, a0 + 2, b2 + 2, idesc, 1);
+          mma_i8_2sm(acc3, a1 + 2, b0 + 2, idesc, 1);
+          mma_i8_2sm(acc3, a0 + 2, b1 + 2, idesc, 1);
+          }
+          mma_commit_2sm(&empty[s], 3);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit_2sm(tfull_a, 3);
+        mbar_wait(acc0_free, i & 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; kb += 3) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t a = d0 + (uint64_t)s * kStageD;
+          const int nk = min(3, nkb - kb);
+          for (int j = 0; j < nk && dbg != 2; ++j) {
+            const uint64_t aj = a + j * kPairD, bj = aj + kAD;
+            mma_i8_2sm(acc0, aj, bj, idesc, (kb | j) ? 1u : 0u);
+            mma_i8_2sm(acc0, aj + 2, bj + 2, idesc, 1);
+          }
+          mma_commit_2sm(&empty[s], 3);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit_2sm(tfull_b, 3);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int ew = warp - 2;
+    const int quad = warp & 3;
+    const int half = ew >> 2;
+    const int row = quad * 32 + lane;
+    const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + half * 64;
+    const uint32_t acc0_free_l = mapa_shared(acc0_free, 0), tempty_l = mapa_shared(tempty, 0);
+    int i = 0;
+    for (int u = pair; u < units; u += npairs, ++i) {
+      double P[64];
+      uint32_t r[32];
+      mbar_wait_sleep(tfull_a, i & 1, 256);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        tmem_ld32(tbase + h * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) P[h * 32 + j] = (double)(int)r[j];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc0_free_l);
+#pragma unroll
+      for (int a = 1; a < 4; ++a) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          tmem_ld32(tbase + a * 128 + h * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) P[h * 32 + j] = fma(P[h * 32 + j], 256.0, (double)(int)r[j]);
+        }
+      }
+      mbar_wait_sleep(tfull_b, i & 1, 256);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        tmem_ld32(tbase + h * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) P[h * 32 + j] = fma(P[h * 32 + j], 256.0, (double)(int)r[j]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_l);
+      int I, J;
+      pair_of_unit(u, nI, I, J);
+      const int ta = 2 * I + (int)rank, tb = J;
+      if (ta >= tb && ta < nt) {     // rank 0 of J = 2I + 1 lies above the diagonal
+        const int64_t slot = (int64_t)ta * (ta + 1) / 2 + tb;
+        double* t = sig + slot * (kI8Tile * kI8Tile) + (int64_t)(half * 64) * kI8Tile + row;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) t[j * kI8Tile] += P[j] * scale;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_2sm(tmem, 512);
+}
+
 // ------------------------------------------------------------ unpack --
 // full[r, c] (M x M, symmetric) from the packed lower tiles.
 __global__ void sigma_unpack_kernel(const double* __restrict__ tiles, int64_t M,
@@ -384,12 +636,13 @@ __global__ void sigma_unpack_kernel(const double* __restrict__ tiles, int64_t M,
 }
 
 // --------------------------------------------------------------- host --
-static int make_plane_map(CUtensorMap* map, const uint8_t* base, int64_t M_pad, int64_t nc) {
+static int make_plane_map(CUtensorMap* map, const uint8_t* base, int64_t M_pad, int64_t nc,
+                          uint32_t box_rows = kI8Tile) {
   auto fn = tensor_map_encoder();
   if (!fn) return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)nc, (cuuint64_t)(3 * M_pad)};
   cuuint64_t strides[1] = {(cuuint64_t)nc};
-  cuuint32_t box[2] = {(cuuint32_t)kI8KB, (cuuint32_t)kI8Tile};
+  cuuint32_t box[2] = {(cuuint32_t)kI8KB, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims,
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -437,13 +690,32 @@ int i8_gram_chunk(int64_t cur, int64_t M_pad, int64_t nc, double variance, const
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int units = (int)i8_tiles(M_pad);
   const int nkb = (int)ceil_div(cur, kI8KB);
-  TB_CUDA_TRY(cudaFuncSetAttribute(sgpr_gram_i8_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem));
   const double scale = variance * variance * std::ldexp(1.0, -2 * kI8FracBits);
   const char* dbg_env = std::getenv("TB_I8_DEBUG");
   const int dbg = dbg_env ? std::atoi(dbg_env) : 0;
+  // CTA-pair engine: opt-in (TB_I8_PAIR=1, needs M_pad % 256 == 0).  Both
+  // kernels run into the 1 kW power cap (sw_power_cap, SM ~1.7 GHz) on C4;
+  // there the 1-SM kernel is ~7% faster (no 256-row padding, 22 vs 23
+  // rounds), so it stays the default.
+  const char* pair_env = std::getenv("TB_I8_PAIR");
+  if (M_pad % (2 * kI8Tile) == 0 && pair_env && pair_env[0] == '1') {
+    CUtensorMap tmb;
+    if ((rc = make_plane_map(&tmb, planes, M_pad, nc, kI8Tile / 2))) return rc;
+    const int nI = (int)(M_pad / (2 * kI8Tile));
+    const int units = nI * (nI + 1);
+    TB_CUDA_TRY(cudaFuncSetAttribute(sgpr_gram_i8_pair_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP2Smem));
+    const int pairs = std::min(units, sms / 2);
+    sgpr_gram_i8_pair_kernel<<<2 * pairs, kI8Threads, kP2Smem, st>>>(tm, tmb, units, nkb,
+                                                                     (int)M_pad, scale,
+                                                                     Sigma_tiles, dbg);
+    TB_LAUNCH_CHECK("sgpr_gram_i8_pair");
+    return TB_OK;
+  }
+  const int units = (int)i8_tiles(M_pad);
+  TB_CUDA_TRY(cudaFuncSetAttribute(sgpr_gram_i8_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem));
   sgpr_gram_i8_kernel<<<std::min(units, sms), kI8Threads, kI8Smem, st>>>(tm, units, nkb,
                                                                          (int)M_pad, scale,
                                                                          Sigma_tiles, dbg);

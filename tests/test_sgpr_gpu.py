@@ -116,3 +116,18 @@ def test_kernel_mvm_ard(kind):
     ref = omvm.kernel_mvm(X, Z, w, kind, 1.7, ls)
     out = tb.kernel_mvm(X, Z, w, kind, 1.7, ls)
     assert rel_err(out, ref) < 1e-13
+
+
+@pytest.mark.parametrize("N,M", [(9000, 300), (777, 129)])
+def test_sgpr_i8_cta_pair_kernel_same_statistics(N, M, monkeypatch):
+    """Opt-in CTA-pair Gram (tcgen05.mma.cta_group::2, TB_I8_PAIR=1) returns
+    the same exact fixed-point statistics as the 1-SM kernel."""
+    X, y, Z, _ = synthetic.sgpr_data(N, 3, M, seed=13, dtype=np.float32)
+    Sq, vq, _ = osgpr.sufficient_stats_fixed24(X, y, Z, "matern32", 1.1, 0.6)
+    ref = tb.SGPR(X, y, Z, "matern32", 1.1, 0.6, 0.01).statistics()
+    monkeypatch.setenv("TB_I8_PAIR", "1")
+    st = tb.SGPR(X, y, Z, "matern32", 1.1, 0.6, 0.01).statistics()
+    assert st.plan.M_pad % 256 == 0
+    Sg = st.full_sigma().cpu().numpy()
+    assert rel_err(Sg, Sq) < 1e-11
+    assert np.allclose(Sg, ref.full_sigma().cpu().numpy(), rtol=1e-13, atol=0)
