@@ -77,7 +77,9 @@ struct TcWork {
   int t0, T;       // database tile range [t0, T) of this launch
   int slices, tps; // slices of the range, tiles per slice
   int list0;       // first candidate list index written by this launch
-  int drain_only;  // debug (TB_TC_DRAIN_ONLY=1): epilogue only drains TMEM
+  int drain_only;  // debug bits (TB_TC_DEBUG, A/B timing only, results garbage):
+                   // 1 = epilogue only drains TMEM, 2 = no database TMA loads,
+                   // 4 = no MMAs, 8 = max-tree but no top-K' insertions
 };
 
 // The accumulator holds acc' = (2q).x - ||x||^2: the norm enters through one
@@ -192,9 +194,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
 #pragma unroll
             for (int mat = 0; mat < Cfg::kMats; ++mat) {
               mbar_wait(&empty[s], ph ^ 1);
-              mbar_expect_tx(&full[s], Cfg::kBBlock);
-              tma_load_2d(b_base + (size_t)s * Cfg::kBBlock, mat ? &tm_xlo : &tm_xhi,
-                          &full[s], kb * kTcKB, t * kTcN);
+              if (work.drain_only & 2) {
+                mbar_arrive(&full[s]);
+              } else {
+                mbar_expect_tx(&full[s], Cfg::kBBlock);
+                tma_load_2d(b_base + (size_t)s * Cfg::kBBlock, mat ? &tm_xlo : &tm_xhi,
+                            &full[s], kb * kTcKB, t * kTcN);
+              }
               if (++s == S) {
                 s = 0;
                 ph ^= 1;
@@ -248,6 +254,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
 #pragma unroll
             for (int kk = 0; kk < kTcKB / 16; ++kk) {
               const uint32_t ko = kk * 32;  // 16 bf16 = 32 bytes along the swizzled row
+              if (work.drain_only & 4) continue;
               mma_bf16(d, desc_k_sw128(ahi + ko), desc_k_sw128(b0 + ko), idesc, 1);
               if (PASSES == 3)
                 mma_bf16(d, desc_k_sw128(alo + ko), desc_k_sw128(b0 + ko), idesc, 1);
@@ -264,7 +271,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               b0 = smem_u32(b_base + (size_t)s * Cfg::kBBlock);
 #pragma unroll
               for (int kk = 0; kk < kTcKB / 16; ++kk)
-                mma_bf16(d, desc_k_sw128(ahi + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, 1);
+                if (!(work.drain_only & 4))
+                  mma_bf16(d, desc_k_sw128(ahi + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, 1);
               mma_commit(&empty[s]);
               if (++s == S) {
                 s = 0;
@@ -320,7 +328,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           tmem_ld32(taddr + c * 32, ra);
           tmem_ld32(taddr + (c + 1) * 32, rb);
           tmem_ld_wait();
-          if (work.drain_only) continue;
+          if (work.drain_only & 1) continue;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint32_t(&r)[32] = h ? rb : ra;
@@ -331,7 +339,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             float hi = __uint_as_float(r[0]);
 #pragma unroll
             for (int j = 1; j < 32; ++j) hi = fmaxf(hi, __uint_as_float(r[j]));
-            if (-hi < thr) {
+            if (-hi < thr && !(work.drain_only & 8)) {
               float sc[32];
               uint32_t mask = 0;
 #pragma unroll
@@ -408,8 +416,8 @@ static void tc_schedule(int64_t m, int64_t rows_pad, int sms, TcWork* seed, TcWo
   const int qtiles = (int)ceil_div(std::max<int64_t>(m, 1), kTcM);
   const int T = (int)(rows_pad / kTcN);
   const int S = std::min(T, kTcSeedTiles);
-  const char* dbg = std::getenv("TB_TC_DRAIN_ONLY");
-  const int drain = dbg && dbg[0] == '1';
+  const char* dbg = std::getenv("TB_TC_DEBUG");
+  const int drain = dbg ? std::atoi(dbg) : 0;
   *seed = TcWork{qtiles, 0, S, 1, S, 0, drain};
   const int R = T - S;
   int best_k = 0;

@@ -15,4 +15,4 @@ t = []
 for _ in range(5):
     op.run(x, q, events=evs); torch.cuda.synchronize()
     t.append([evs[2*c].elapsed_time(evs[2*c+1]) for c in range(int(op.plan.n_chunks))])
-print(json.dumps({"drain_only": os.environ.get("TB_TC_DRAIN_ONLY", "0"), "chunk_ms": t[-1], "total_ms": min(sum(r) for r in t)}))
+print(json.dumps({"TB_TC_DEBUG": os.environ.get("TB_TC_DEBUG", "0"), "chunk_ms": t[-1], "total_ms": min(sum(r) for r in t)}))
