@@ -39,7 +39,8 @@ constexpr int kInvalidIdx = INT_MAX;
 // (the reference TopK's stable argsort, interpreter.py:379-381).
 template <typename S>
 __device__ __forceinline__ bool lex_less(S a, int ia, S b, int ib) {
-  return a < b || (a == b && ia < ib);
+  // non-short-circuit: compiles to compares + one predicate op, no branches
+  return (a < b) | ((a == b) & (ia < ib));
 }
 
 // Sorted top-K list held in registers (fully unrolled -> no local memory).
@@ -59,20 +60,22 @@ struct TopList {
   __device__ __forceinline__ int worst_idx() const { return i[K - 1]; }
 
   // Insert (v, j); caller guarantees (v, j) < (s[K-1], i[K-1]).
+  // Branch-free parallel network on the OLD list: c[p] = (v,j) < entry p;
+  // slot p takes entry p-1 if c[p-1] (shift down), else (v,j) if c[p],
+  // else keeps its entry.  All K compares are independent (ILP, no
+  // divergence-serialised branch chain).
   __device__ __forceinline__ void insert(S v, int j) {
-    bool done = false;
+    bool c[K];
+#pragma unroll
+    for (int p = 0; p < K; ++p) c[p] = lex_less(v, j, s[p], i[p]);
 #pragma unroll
     for (int p = K - 1; p > 0; --p) {
-      const bool lt = lex_less(v, j, s[p - 1], i[p - 1]);
-      const S ns = lt ? s[p - 1] : v;
-      const int ni = lt ? i[p - 1] : j;
-      if (!done) {
-        s[p] = ns;
-        i[p] = ni;
-      }
-      done = done || !lt;
+      const S ns = c[p - 1] ? s[p - 1] : (c[p] ? v : s[p]);
+      const int ni = c[p - 1] ? i[p - 1] : (c[p] ? j : i[p]);
+      s[p] = ns;
+      i[p] = ni;
     }
-    if (!done) {
+    if (c[0]) {
       s[0] = v;
       i[0] = j;
     }
