@@ -365,13 +365,14 @@ def run_ours(args):
     if not args.no_e2e and world == 1:
         # the reference-facing call with HOST buffers (tb_knn_run_host): pinned
         # x, q copied in (database chunk by chunk, overlapped with compute)
-        # and dist, idx copied out, every step.  Its plan caps chunks at n/4
-        # so three of the four database copies overlap compute.
+        # and dist, idx copied out, every step.  Its plan caps chunks at n/8
+        # so seven of the eight database copies overlap compute (tools/
+        # e2e_chunks.py: 2/4/8/16 chunks -> 771k/844k/913k/813k q/s).
         xh = x.cpu().pin_memory()
         qh = q.cpu().pin_memory()
         op_h = neighbors.KnnOperator(rows, M_Q, DIM, K, dtype=np.float32, out_dtype=out_dtype,
                                      engine=args.engine, memory_limit=LIMIT, device=dev,
-                                     max_chunk_rows=-(-rows // 4))
+                                     max_chunk_rows=-(-rows // 8))
         staging = (x, q, out[0], out[1])      # device buffers refilled every step
         dh = torch.empty(out[0].shape, dtype=out[0].dtype).pin_memory()
         ih = torch.empty(out[1].shape, dtype=out[1].dtype).pin_memory()
