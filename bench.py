@@ -478,7 +478,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--engine", default="auto")
     ap.add_argument("--cpu-queries", type=int, default=384)
-    ap.add_argument("--ref-queries", type=int, default=64)
+    ap.add_argument("--ref-queries", type=int, default=384)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sgpr", action="store_true")
