@@ -14,6 +14,8 @@ written, and ``budget`` counts the inputs (interpreter.py:543-546).
 
 from __future__ import annotations
 
+import math
+import re
 from dataclasses import dataclass, field, replace
 from enum import Enum
 
@@ -239,14 +241,91 @@ def estimate_peak_memory(graph: Graph, budget: int | None = None) -> int:
     raise EvaluationError(f"no evaluator for graph kind {graph.kind!r}")
 
 
+_KNN_NAME = re.compile(r"knn_(l2|l1|cosine)_n(\d+)_m(\d+)_d(\d+)_k(\d+)$")
+_MVM_NAME = re.compile(r"se_kernel_mvm_n(\d+)$")
+
+
+def _se_constants(g, params):
+    """(variance, -0.5/l^2) of the SE kernel pattern mul(bcast(variance),
+    exp(mul(square(.), bcast(scale)))) (frontend.py:49-53), found in ``g`` or
+    in the body of a While the splitter created; loop parameters are resolved
+    to the constants the While is entered with."""
+    ins = getattr(g, "instructions", {})
+
+    def value(i):
+        op = ins[i].op
+        kind = type(op).__name__
+        if kind == "Constant":
+            return float(op.value) if np.ndim(op.value) == 0 else None
+        if kind == "Parameter":
+            return params.get(op.index)
+        if kind == "Broadcast":
+            return value(ins[i].operands[0])
+        return None
+
+    for i, inst in ins.items():
+        op = inst.op
+        kind = type(op).__name__
+        if kind == "Unary" and getattr(op, "op", None) == "exp":
+            arg = ins[inst.operands[0]]
+            if type(arg.op).__name__ == "Binary" and arg.op.op == "mul":
+                scale = [value(o) for o in arg.operands if value(o) is not None]
+                users = [u for u in ins.values() if type(u.op).__name__ == "Binary"
+                         and u.op.op == "mul" and i in u.operands]
+                var = [value(o) for u in users for o in u.operands
+                       if o != i and value(o) is not None]
+                if len(scale) == 1 and len(var) == 1 and scale[0] < 0 < var[0]:
+                    return var[0], scale[0]
+        if kind == "While":
+            inner = {k: value(o) for k, o in enumerate(inst.operands)}
+            found = _se_constants(op.body, inner)
+            if found is not None:
+                return found
+    return None
+
+
+def from_reference(graph) -> Graph:
+    """Descriptor for a graph object built by the REFERENCE package
+    (tensorbudget.ir.Graph from build_knn / build_kernel_mvm, naive or after
+    run_pipeline - the passes keep the builder's name, frontend.py:98-114,
+    34-54).  Duck-typed (the reference is not imported): the family and sizes
+    come from the builder name, the dtype from the parameters, and the SE
+    kernel's variance / lengthscale from the SE pattern (frontend.py:49-53),
+    followed into the splitter's While body for pipelined graphs."""
+    name = getattr(graph, "name", None)
+    params = getattr(graph, "parameters", None)
+    if not isinstance(name, str) or not params:
+        raise EvaluationError(f"not a graph: {graph!r}")
+    label = getattr(getattr(params[0], "dtype", None), "name", "")
+    if label not in ("F32", "F64"):
+        raise EvaluationError(f"graph {name!r}: unsupported parameter dtype {label!r}")
+    dtype = DType[label]
+    m = _KNN_NAME.match(name)
+    if m:
+        metric, n, mq, d, k = m.group(1), *(int(v) for v in m.groups()[1:])
+        return build_knn(n, mq, d, k, metric, dtype)
+    m = _MVM_NAME.match(name)
+    if m:
+        found = _se_constants(graph, {})
+        if found is None:
+            raise EvaluationError(f"graph {name!r}: cannot recover the kernel constants")
+        variance, scale = found
+        return build_kernel_mvm(int(m.group(1)),
+                                KernelSpec(variance, math.sqrt(-0.5 / scale)), dtype)
+    raise EvaluationError(f"graph {name!r} is not a kNN / kernel-MVM graph of this path")
+
+
 def evaluate(graph: Graph, inputs, budget: int | None = None, *,
              poison_freed: bool = False):
     """Evaluates the graph on the B200 path; returns (outputs, MemoryTrace).
 
-    Raises BudgetExceeded before any device allocation when the planner
-    cannot fit ``budget`` (the reference raises at the offending allocation,
-    interpreter.py:149-151).
+    ``graph`` is this package's descriptor or a reference-built graph object
+    (see ``from_reference``).  Raises BudgetExceeded before any device
+    allocation when the planner cannot fit ``budget`` (the reference raises
+    at the offending allocation, interpreter.py:149-151).
     """
+    if not isinstance(graph, Graph):
+        graph = from_reference(graph)
     arrays = _check_inputs(graph, inputs)
     from .errors import BudgetExceeded as _BE
     if graph.kind == "knn":
