@@ -333,3 +333,52 @@ def test_metric_engine_rules_and_zero_rows():
     (vals, idx), _ = tb.evaluate(graph, [x, q])
     rd, ri = oknn.exact(x, q, 3, metric="l1")
     assert np.array_equal(np.asarray(idx.array).astype(np.int64), ri)
+
+
+def test_sharded_knn_with_real_kernels_and_cuda_merge():
+    """The multi-GPU recipe with the real kernels: 3 uneven database shards
+    (index_base = shard start, exact f64 lists) merged by tb_topk_merge equal
+    the single-call answer and the oracle (ties -> lower global index)."""
+    import torch
+    from paper_2206_14148_b200 import distributed
+    x, q = synthetic.quantized_knn(20001, 150, 8, seed=4)      # many exact ties
+    ref_d, ref_i = oknn.exact(x, q, 10)
+    xt, qt = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+    dls, ils = [], []
+    for r in range(3):
+        a, b = distributed.shard_range(20001, r, 3)
+        op = neighbors.KnnOperator(b - a, 150, 8, 10, out_dtype=np.float64)
+        d, i = op.run(xt[a:b].contiguous(), qt, index_base=a)
+        dls.append(d)
+        ils.append(i)
+    od, oi = distributed.merge_topk(torch.stack(dls), torch.stack(ils))
+    check(od.cpu().numpy(), oi.cpu().numpy(), ref_d, ref_i, x, q)
+    d1, i1 = tb.knn(x, q, 10, out_dtype=np.float64)
+    assert np.array_equal(oi.cpu().numpy(), i1)
+
+
+def test_nccl_process_group_world1():
+    """The NCCL code path (SGPR all_reduce of packed Sigma/v/yy, knn_sharded)
+    in a real NCCL process group of size 1 on this B200."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2206_14148_b200 import distributed
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        X, y, Z, _ = synthetic.sgpr_data(6000, 3, 200, seed=3, dtype=np.float32)
+        e_group = tb.SGPR(X, y, Z, "rbf", 1.0, 0.8, 0.05, group=dist.group.WORLD).elbo()
+        e_local = tb.SGPR(X, y, Z, "rbf", 1.0, 0.8, 0.05).elbo()
+        assert e_group == e_local
+        x, q = synthetic.gaussian_knn(9000, 64, 16, seed=2)
+        xt, qt = torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda()
+        d, i = distributed.knn_sharded(xt, qt, 5, index_base=0, group=dist.group.WORLD)
+        ref_d, ref_i = oknn.exact(x, q, 5)
+        check(d.cpu().numpy(), i.cpu().numpy(), ref_d, ref_i, x, q)
+    finally:
+        dist.destroy_process_group()
