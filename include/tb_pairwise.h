@@ -210,6 +210,23 @@ TB_API int tb_sgpr_stats_run(const tb_sgpr_plan* plan, const void* X, const void
 TB_API int tb_sgpr_sigma_unpack(const tb_sgpr_plan* plan, const double* Sigma,
                                 double* full, void* stream);
 
+/* ---------------- SGPR ELBO gradient (N-streaming half) ------------------
+ * GPflow 2.3.1 SGPR training-loss gradient (paper §5.3).  With
+ * G = dELBO/dSigma and g = dELBO/dv from the O(M^3) tail (autodiff), the
+ * data enter only through W = 2 G Kuf + g y^T, and
+ *   grad_hyp[0]      += sum_in W_in dK_in/d variance
+ *   grad_hyp[1 + t]  += sum_in W_in dK_in/d lengthscale_t
+ *   grad_Z[i, t]     += sum_n  W_in dK_in/d Z_it
+ * for one chunk: Xc[nc, dim], Z[M, dim] (dtype), W and K = k(Z, Xc) fp64
+ * [M, nc] row-major.  Fixed-order reductions (deterministic).  No reference
+ * counterpart. */
+TB_API int64_t tb_sgpr_kuf_grad_workspace(int64_t nc, int64_t M, int64_t dim);
+TB_API int tb_sgpr_kuf_grad(const void* Xc, const void* Z, const double* W, const double* K,
+                            int64_t nc, int64_t M, int64_t dim, int32_t kernel, int32_t dtype,
+                            double variance, const double* lengthscales, double* grad_hyp,
+                            double* grad_Z, void* workspace, int64_t workspace_bytes,
+                            void* stream);
+
 /* ---------------- kernel MVM --------------------------------------------
  * out[i] = sum_j k(X_i, Z_j) w_j in fp64 accumulation, X[n,dim], Z[M,dim]
  * (dtype), w[M] fp64 -> out[n] fp64.  Replaces evaluate(build_kernel_mvm)

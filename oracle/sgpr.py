@@ -148,3 +148,41 @@ def exact_log_marginal(X, y, kind="rbf", variance=1.0, lengthscales=1.0,
     a = _tri_solve(L, y)
     return float(-0.5 * a @ a - np.sum(np.log(np.diag(L)))
                  - 0.5 * X.shape[0] * LOG2PI)
+
+
+def elbo_grads_fd(X, y, Z, kind="rbf", variance=1.0, lengthscales=1.0,
+                  noise_variance=0.01, jitter=1e-6, rel_step=1e-5):
+    """Central finite differences of the fp64 ELBO (``elbo`` above) w.r.t.
+    the kernel variance, each lengthscale (ARD), the noise variance and every
+    inducing-point coordinate: the oracle for the GPU gradient (GPflow's
+    training loss is -ELBO).  O(h^2) truncation, h = rel_step * |param|."""
+    Z = np.asarray(Z, np.float64)
+    ls = np.broadcast_to(np.asarray(lengthscales, np.float64), (Z.shape[1],)).copy()
+
+    def f(var, lsv, noise, Zv):
+        return elbo(X, y, Zv, kind, var, lsv, noise, jitter)[0]
+
+    def cd(fn, x0):
+        h = rel_step * max(abs(x0), 1e-3)
+        return (fn(x0 + h) - fn(x0 - h)) / (2 * h)
+
+    g = {"variance": cd(lambda t: f(t, ls, noise_variance, Z), variance),
+         "noise_variance": cd(lambda t: f(variance, ls, t, Z), noise_variance)}
+    gl = np.empty_like(ls)
+    for t in range(ls.size):
+        def fl(val, t=t):
+            l2 = ls.copy()
+            l2[t] = val
+            return f(variance, l2, noise_variance, Z)
+        gl[t] = cd(fl, ls[t])
+    g["lengthscales"] = gl
+    gz = np.empty_like(Z)
+    for i in range(Z.shape[0]):
+        for t in range(Z.shape[1]):
+            def fz(val, i=i, t=t):
+                Z2 = Z.copy()
+                Z2[i, t] = val
+                return f(variance, ls, noise_variance, Z2)
+            gz[i, t] = cd(fz, Z[i, t])
+    g["Z"] = gz
+    return g

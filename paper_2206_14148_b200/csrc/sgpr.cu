@@ -553,6 +553,31 @@ int tb_sgpr_sigma_unpack(const tb_sgpr_plan* p, const double* Sigma, double* ful
   return i8_unpack(Sigma, p->M, p->M_pad, full, st);
 }
 
+int64_t tb_sgpr_kuf_grad_workspace(int64_t nc, int64_t M, int64_t dim) {
+  if (nc < 0 || M < 1 || dim < 1 || dim > kMaxDim) return -1;
+  return kuf_grad_bytes(nc, M, dim);
+}
+
+int tb_sgpr_kuf_grad(const void* Xc, const void* Z, const double* W, const double* K,
+                     int64_t nc, int64_t M, int64_t dim, int32_t kernel, int32_t dtype,
+                     double variance, const double* lengthscales, double* grad_hyp,
+                     double* grad_Z, void* workspace, int64_t workspace_bytes, void* stream) {
+  if (nc < 0 || M < 1) return fail(TB_ERR_ARG, "bad kuf_grad extents");
+  if (!Xc || !Z || !W || !K || !grad_hyp || !grad_Z || !workspace)
+    return fail(TB_ERR_ARG, "null buffer passed to tb_sgpr_kuf_grad");
+  if (dtype != TB_F32 && dtype != TB_F64) return fail(TB_ERR_ARG, "dtype must be f32 or f64");
+  KernParams kp;
+  int rc = make_params(kernel, dim, variance, lengthscales, &kp);
+  if (rc) return rc;
+  if (workspace_bytes < kuf_grad_bytes(nc, M, dim))
+    return fail(TB_ERR_ARG, "workspace smaller than tb_sgpr_kuf_grad_workspace()");
+  if (nc == 0) return TB_OK;
+  std::string why;
+  if (!sm100(&why)) return fail(TB_ERR_NO_DEVICE, why);
+  return launch_kuf_grad(Xc, Z, W, K, nc, M, dtype, kp, grad_hyp, grad_Z, workspace,
+                         (cudaStream_t)stream);
+}
+
 int tb_kernel_matrix(const void* A, const void* B, int64_t na, int64_t nb, int64_t dim,
                      int32_t kernel, int32_t dtype, double variance,
                      const double* lengthscales, double* out, void* stream) {

@@ -214,6 +214,66 @@ class SGPR:
     def elbo(self) -> float:
         return self._tail()
 
+    # -- gradient (GPflow 2.3.1 SGPR training loss; paper §5.3 Table 2) -------
+    def elbo_and_grads(self, chunk_n: int = 4096):
+        """ELBO and its gradient w.r.t. kernel variance, lengthscales (ARD),
+        likelihood noise variance and the inducing points Z (the quantities
+        GPflow trains; values are w.r.t. the constrained parameters).
+
+        The O(M^3) tail is differentiated with torch autograd (fp64, cuSOLVER /
+        cuBLAS, like the tail itself); it yields G = dELBO/dSigma and
+        g = dELBO/dv.  The data then enter only through
+        W = 2 G Kuf + g y^T, streamed over N in chunks: W by one fp64 GEMM
+        (cuBLAS) and the reduction against the kernel derivatives by the
+        fused kernel ``tb_sgpr_kuf_grad``.  Multi-GPU: the chunk sums are
+        all-reduced like the statistics.  Returns (elbo, dict of gradients)."""
+        torch = _torch()
+        s = self._stats or self.statistics()
+        M, dim = int(s.v.numel()), self.dim
+        f64 = torch.float64
+        dev = self.device
+        Zd = self.Z.to(f64).detach().requires_grad_()
+        var = torch.tensor(self.variance, dtype=f64, device=dev, requires_grad=True)
+        ls = torch.tensor(self.lengthscales, dtype=f64, device=dev, requires_grad=True)
+        s2 = torch.tensor(self.noise_variance, dtype=f64, device=dev, requires_grad=True)
+        Sigma = s.full_sigma().detach().requires_grad_()
+        v = s.v.detach().requires_grad_()
+        Kuu = _torch_kernel(Zd, Zd, self.kernel, var, ls)
+        Kuu = Kuu + self.jitter * torch.eye(M, dtype=f64, device=dev)
+        elbo = _elbo_torch(Sigma, v, s.yy, s.N, Kuu, s2, var)
+        elbo.backward()
+        G = 0.5 * (Sigma.grad + Sigma.grad.mT)
+        g = v.grad
+        del Sigma, Kuu
+        grad_hyp = torch.zeros(1 + dim, dtype=f64, device=dev)
+        grad_z = torch.zeros((M, dim), dtype=f64, device=dev)
+        lib = _lib.load()
+        ws = torch.empty(max(int(lib.tb_sgpr_kuf_grad_workspace(chunk_n, M, dim)), 1),
+                         dtype=torch.uint8, device=dev)
+        st = torch.cuda.current_stream(dev)
+        dt = _lib.TB_F32 if self.X.dtype == torch.float32 else _lib.TB_F64
+        G2 = 2.0 * G
+        for n0 in range(0, int(self.X.shape[0]), chunk_n):
+            Xc = self.X[n0:n0 + chunk_n].contiguous()
+            yc = self.y[n0:n0 + chunk_n].to(f64)
+            K = kernel_matrix(self.Z, Xc, self.kernel, self.variance, self.lengthscales)
+            W = torch.addr(G2 @ K, g, yc)                   # 2 G K + g y^T
+            rc = lib.tb_sgpr_kuf_grad(
+                Xc.data_ptr(), self.Z.data_ptr(), W.data_ptr(), K.data_ptr(), int(Xc.shape[0]),
+                M, dim, _lib.KERNELS[self.kernel], dt, self.variance,
+                self.lengthscales.ctypes.data_as(ctypes.c_void_p), grad_hyp.data_ptr(),
+                grad_z.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
+            _lib.check(rc, "sgpr_kuf_grad")
+        if self.group is not None:
+            import torch.distributed as dist
+            dist.all_reduce(grad_hyp, group=self.group)
+            dist.all_reduce(grad_z, group=self.group)
+        grads = {"variance": float(var.grad) + float(grad_hyp[0]),
+                 "lengthscales": (ls.grad + grad_hyp[1:]).cpu().numpy(),
+                 "noise_variance": float(s2.grad),
+                 "Z": (Zd.grad + grad_z).cpu().numpy()}
+        return float(elbo.detach()), grads
+
     def predict_mean(self, Xnew):
         """mu(X*) = K(X*, Z) L^-T LB^-T c (GPflow predict_f mean)."""
         from .mvm import kernel_mvm
@@ -223,6 +283,35 @@ class SGPR:
         Xt = _dev_tensor(Xnew, self.device).to(self.Z.dtype)
         mu = kernel_mvm(Xt, self.Z, self._w, self.kernel, self.variance, self.lengthscales)
         return mu.cpu().numpy() if host else mu
+
+
+def _torch_kernel(A, B, kind, variance, ls):
+    """Differentiable fp64 k(A, B) (same formulas as the CUDA kernels;
+    r^2 by the expansion to stay O(|A| |B|) in memory)."""
+    torch = _torch()
+    a, b = A / ls, B / ls
+    r2 = ((a * a).sum(1)[:, None] + (b * b).sum(1)[None, :] - 2.0 * (a @ b.mT)).clamp_min(0.0)
+    if kind == "rbf":
+        return variance * torch.exp(-0.5 * r2)
+    r = r2.clamp_min(1e-36).sqrt()
+    return variance * (1.0 + math.sqrt(3.0) * r) * torch.exp(-math.sqrt(3.0) * r)
+
+
+def _elbo_torch(Sigma, v, yy, N, Kuu, s2, variance):
+    """Differentiable copy of the tail (SGPR._tail / oracle.sgpr.elbo_from_stats)."""
+    torch = _torch()
+    M = v.numel()
+    L = torch.linalg.cholesky(Kuu)
+    tmp = torch.linalg.solve_triangular(L, Sigma, upper=False)
+    AAT = torch.linalg.solve_triangular(L, tmp.mT, upper=False).mT / s2
+    AAT = 0.5 * (AAT + AAT.mT)
+    B = AAT + torch.eye(M, dtype=AAT.dtype, device=AAT.device)
+    LB = torch.linalg.cholesky(B)
+    Lv = torch.linalg.solve_triangular(L, v.reshape(M, 1), upper=False)
+    c = torch.linalg.solve_triangular(LB, Lv, upper=False) / s2
+    return (-0.5 * N * LOG2PI - torch.log(LB.diagonal()).sum() - 0.5 * N * torch.log(s2)
+            - 0.5 * yy / s2 + 0.5 * (c * c).sum() - 0.5 * N * variance / s2
+            + 0.5 * AAT.diagonal().sum())
 
 
 def sgpr_elbo(X, y, Z, kernel="rbf", variance=1.0, lengthscales=1.0,

@@ -131,3 +131,24 @@ def test_sgpr_i8_cta_pair_kernel_same_statistics(N, M, monkeypatch):
     Sg = st.full_sigma().cpu().numpy()
     assert rel_err(Sg, Sq) < 1e-11
     assert np.allclose(Sg, ref.full_sigma().cpu().numpy(), rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("kind,engine,dtype", [("rbf", "f64", np.float64),
+                                               ("matern32", "f64", np.float64),
+                                               ("rbf", "i8", np.float32),
+                                               ("matern32", "i8", np.float32)])
+def test_elbo_gradient_matches_finite_differences(kind, engine, dtype):
+    """GPflow-style training gradient (variance, ARD lengthscales, noise, Z)
+    vs central finite differences of the fp64 oracle ELBO.  The N-streaming
+    part runs through tb_sgpr_kuf_grad over several chunks."""
+    X, y, Z, _ = synthetic.sgpr_data(3000, 3, 25, seed=17, dtype=dtype)
+    ls = [0.9, 1.3, 0.7]
+    m = tb.SGPR(X, y, Z, kind, 1.4, ls, 0.05, engine=engine)
+    e, g = m.elbo_and_grads(chunk_n=1024)
+    ref_e, _ = osgpr.elbo(X, y, Z, kind, 1.4, ls, 0.05)
+    assert abs(e - ref_e) <= 1e-6 * abs(ref_e)
+    fd = osgpr.elbo_grads_fd(X, y, Z, kind, 1.4, ls, 0.05)
+    tol = 1e-5 if engine == "f64" else 1e-3
+    for key in ("variance", "noise_variance", "lengthscales", "Z"):
+        got, want = np.asarray(g[key], np.float64), np.asarray(fd[key], np.float64)
+        assert np.max(np.abs(got - want)) <= tol * max(np.max(np.abs(want)), 1.0), (key, got, want)
