@@ -200,6 +200,7 @@ def run_sgpr(args, dev, world, rank, dist):
     elbo = m.elbo()
     e2.record()
     torch.cuda.synchronize()
+    peak_eval = torch.cuda.max_memory_allocated(dev) - base
     stats_ms, total_ms = e0.elapsed_time(e1), e0.elapsed_time(e2)
     if dist is not None:
         t = torch.tensor([stats_ms, total_ms], device=dev, dtype=torch.float64)
@@ -226,6 +227,9 @@ def run_sgpr(args, dev, world, rank, dist):
                       "parallelism": f"N-shard{world}", "timed": "1 full evaluation (statistics + "
                       "fp64 tail) after one untimed full-size warm-up evaluation"},
            "peak_stats_mb": peak_stats / 1e6, "planned_peak_mb": st.plan.peak_bytes / 1e6,
+           "peak_eval_mb": peak_eval / 1e6,
+           "peak_note": "max_memory_allocated incl. X, y, Z; peak_eval covers statistics AND the "
+                        "packed in-place O(M^3) tail (tb_sgpr_tail_run)",
            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                         "frac": achieved / peak, "traffic": traffic,
                         "traffic_note": None if traffic is None else

@@ -210,6 +210,21 @@ TB_API int tb_sgpr_stats_run(const tb_sgpr_plan* plan, const void* X, const void
 TB_API int tb_sgpr_sigma_unpack(const tb_sgpr_plan* plan, const double* Sigma,
                                 double* full, void* stream);
 
+/* ---------------- SGPR tail on the packed tiles --------------------------
+ * The O(M^3) part of the ELBO on a TB_SIGMA_TILES Sigma, in place, so the
+ * whole evaluation fits memory_limit (two packed M x M matrices):
+ *   Kuu = L L^T,  Kuu + Sigma/s2 = P P^T (P overwrites Sigma),  X = L^-1 P
+ * out4 = {sum log diag L, sum log diag P, |P^-1 v|^2, ||X||_F^2} (device
+ * doubles) and w_out[M] = P^-T P^-1 v / s2 (the predictive-mean weights).
+ * Then (GPflow SGPR.elbo): sum log diag LB = out4[1] - out4[0],
+ * c^T c = out4[2] / s2^2, tr(AAT) = out4[3] - M_pad.  Synchronises `stream`
+ * (reports a failed Cholesky as TB_ERR_ARG). */
+TB_API int64_t tb_sgpr_tail_workspace(const tb_sgpr_plan* plan);
+TB_API int tb_sgpr_tail_run(const tb_sgpr_plan* plan, const void* Z, double variance,
+                            const double* lengthscales, double jitter, double noise_variance,
+                            double* Sigma, const double* v, double* w_out, double* out4,
+                            void* workspace, int64_t workspace_bytes, void* stream);
+
 /* ---------------- SGPR ELBO gradient (N-streaming half) ------------------
  * GPflow 2.3.1 SGPR training-loss gradient (paper §5.3).  With
  * G = dELBO/dSigma and g = dELBO/dv from the O(M^3) tail (autodiff), the

@@ -49,6 +49,11 @@ int i8_gen_chunk(const void* X, const void* y, const void* Z, int dtype, int64_t
 // Sigma tiles += Gram of the chunk's planes, on `st`
 int i8_gram_chunk(int64_t cur, int64_t M_pad, int64_t nc, double variance, const uint8_t* planes,
                   double* Sigma_tiles, cudaStream_t st);
+// packed-tile O(M^3) tail (sgpr_tail.cu)
+int64_t tail_workspace_bytes(int64_t M, int64_t M_pad, int64_t dim);
+int tail_run(int64_t M, int64_t M_pad, const void* Z, int dtype, const KernParams& kp,
+             double jitter, double noise, double* sigma, const double* v, double* w_out,
+             double* out4, void* workspace, cudaStream_t st);
 // ELBO gradient, N-streaming half (sgpr_grad.cu)
 int64_t kuf_grad_bytes(int64_t nc, int64_t M, int64_t dim);
 int launch_kuf_grad(const void* Xc, const void* Z, const double* W, const double* K,

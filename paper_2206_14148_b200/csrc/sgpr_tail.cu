@@ -1,0 +1,489 @@
+// sgpr_tail.cu — the O(M^3) SGPR tail on the packed lower-tile storage the
+// fixed-point statistics engine produces, so the whole ELBO evaluation stays
+// inside memory_limit (two packed M x M matrices instead of ~4 dense ones).
+//
+// Formulation (algebraically GPflow 2.3.1 SGPR.elbo / predict_f, Titsias):
+//   Kuu = L L^T,   Kuu + Sigma / s2 = P P^T
+//   (then L^-1 P P^T L^-T = I + AAT = B, so with X = L^-1 P)
+//   sum log diag LB = sum log diag P - sum log diag L
+//   c^T c            = |P^-1 v|^2 / s2^2
+//   tr(AAT)          = ||X||_F^2 - M
+//   w (pred. mean)   = P^-T P^-1 v / s2
+// Cost 4/3 M^3 (3 Choleskys-worth) vs 8/3 M^3 for the dense two-sided solve.
+// Storage: 128 x 128 tiles, lower tiles (a >= b) packed at a(a+1)/2 + b,
+// column-major inside; padding rows/cols (>= M) are identity blocks.
+// Kernels: tile Cholesky + triangular inverse of the diagonal tile (one
+// CTA, shared memory); every off-diagonal triangular solve and update is a
+// DMMA tile GEMM (mma.sync m8n8k4 fp64) with that inverse; blocked vector
+// solves (diagonal inverse + parallel matvec updates); fixed-order
+// reductions.
+#include <cmath>
+#include <string>
+
+#include "sgpr_internal.h"
+
+namespace tb {
+
+constexpr int kTT = 128;               // tile edge
+constexpr int kTLd = kTT + 1;          // padded shared-memory row
+constexpr int64_t kTE = kTT * kTT;     // doubles per tile
+
+__host__ __device__ __forceinline__ int64_t tslot(int a, int b) {
+  return (int64_t)a * (a + 1) / 2 + b;
+}
+__device__ __forceinline__ void tri_idx(int u, int& a, int& b) {
+  a = (int)((sqrt(8.0 * u + 1.0) - 1.0) * 0.5);
+  while ((a + 1) * (a + 2) / 2 <= u) ++a;
+  while (a * (a + 1) / 2 > u) --a;
+  b = u - a * (a + 1) / 2;
+}
+
+// ---------------------------------------------------------------- Kuu --
+// dst tile = alpha * dst + k(Z_rows, Z_cols) (+ jitter on the diagonal);
+// padding: identity.  Diagonal tiles: upper part left untouched (ignored).
+__global__ void __launch_bounds__(256)
+tail_kuu_kernel(const double* __restrict__ Zs, int64_t M, KernParams p, double jitter,
+                double alpha, double* __restrict__ dst) {
+  int a, b;
+  tri_idx(blockIdx.x, a, b);
+  double* t = dst + tslot(a, b) * kTE;
+  for (int e = threadIdx.x; e < kTE; e += blockDim.x) {
+    const int c = e / kTT, r = e % kTT;
+    const int64_t i = (int64_t)a * kTT + r, j = (int64_t)b * kTT + c;
+    if (a == b && r < c) continue;
+    double val;
+    if (i < M && j < M) {
+      double r2 = 0.0;
+      for (int d = 0; d < p.dim; ++d) {
+        const double df = Zs[i * p.dim + d] - Zs[j * p.dim + d];
+        r2 = fma(df, df, r2);
+      }
+      val = kern_from_r2(p, r2) + (i == j ? jitter : 0.0);
+    } else {
+      val = i == j ? 1.0 : 0.0;
+    }
+    t[e] = alpha == 0.0 ? val : fma(alpha, t[e], val);
+  }
+}
+
+// Z scaled by 1/l (fp64) once, for the Kuu tiles
+template <typename T>
+__global__ void scale_z_kernel(const T* __restrict__ Z, int64_t M, KernParams p,
+                               double* __restrict__ Zs) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < M * p.dim) Zs[e] = (double)Z[e] * p.inv_ls[e % p.dim];
+}
+
+// ------------------------------------------------- potrf + tri. inverse --
+// Diagonal tile k: in-place Cholesky (lower, upper zeroed), then its
+// inverse L_kk^-1 into inv (column-major).  The off-diagonal triangular
+// solves become DMMA tile GEMMs with this inverse (the usual GPU TRSM
+// blocking; cond(L_kk) <= sqrt(cond(Kuu)) keeps it accurate).
+// One CTA, 512 threads: 4 threads per row (left-looking factorisation, then
+// the in-place inverse), dot products split 4 ways; two barriers per column.
+constexpr int kPThreads = 4 * kTT;     // 4 threads per row: split dot products
+
+__global__ void __launch_bounds__(kPThreads)
+tail_potrf_inv_kernel(double* __restrict__ base, int k, double* __restrict__ inv,
+                      int* __restrict__ info) {
+  extern __shared__ double sA[];          // [kTT][kTLd]
+  __shared__ double dshared;
+  __shared__ double col[kTT];
+  double* t = base + tslot(k, k) * kTE;
+  const int tid = threadIdx.x, i = tid >> 2, sub = tid & 3;
+#pragma unroll 4
+  for (int e = tid; e < kTE; e += kPThreads) {
+    const int c = e / kTT, r = e % kTT;
+    sA[r * kTLd + c] = r >= c ? t[e] : 0.0;
+  }
+  __syncthreads();
+  // left-looking: column j = A[:, j] - L[:, <j] L[j, <j]^T; row i's dot is
+  // split over its 4 threads (q = sub, sub + 4, ...), combined by shuffles
+  for (int j = 0; j < kTT; ++j) {
+    double a = 0.0;
+    if (i >= j) {
+      const double* ri = sA + i * kTLd;
+      const double* rj = sA + j * kTLd;
+      double s0 = 0.0, s1 = 0.0;
+      int q = sub;
+      for (; q + 4 < j; q += 8) {
+        s0 = fma(ri[q], rj[q], s0);
+        s1 = fma(ri[q + 4], rj[q + 4], s1);
+      }
+      if (q < j) s0 = fma(ri[q], rj[q], s0);
+      a = s0 + s1;
+    }
+    a += __shfl_xor_sync(0xffffffffu, a, 1);
+    a += __shfl_xor_sync(0xffffffffu, a, 2);
+    if (i >= j) {
+      a = sA[i * kTLd + j] - a;
+      if (i == j && sub == 0) dshared = a;
+    }
+    __syncthreads();
+    const double djj = dshared;
+    if (!(djj > 0.0)) {                   // uniform: every thread read the same value
+      if (tid == 0) atomicExch(info, k * kTT + j + 1);
+      return;
+    }
+    const double rd = rsqrt(djj);         // one reciprocal root per column
+    if (sub == 0) {
+      if (i > j) sA[i * kTLd + j] = a * rd;
+      if (i == j) sA[j * kTLd + j] = djj * rd;
+    }
+    __syncthreads();
+  }
+#pragma unroll 4
+  for (int e = tid; e < kTE; e += kPThreads) {
+    const int c = e / kTT, r = e % kTT;
+    t[e] = r >= c ? sA[r * kTLd + c] : 0.0;
+  }
+  // L^-1 in place (LAPACK trti2, lower), last column first, trailing block
+  // already inverted:  Inv[j][j] = 1/L[j][j],
+  //   Inv[r][j] = -Inv[j][j] * sum_{j<q<=r} Inv[r][q] L[q][j]
+  __shared__ double rdiag[kTT];
+  if (sub == 0) rdiag[i] = 1.0 / sA[i * kTLd + i];   // all reciprocals at once
+  for (int j = kTT - 1; j >= 0; --j) {
+    if (sub == 0) col[i] = i > j ? sA[i * kTLd + j] : 0.0;      // old L[., j]
+    __syncthreads();
+    const double ijj = rdiag[j];
+    double sum = 0.0;
+    if (i > j) {
+      const double* ri = sA + i * kTLd;
+      for (int q = j + 1 + sub; q <= i; q += 4) sum = fma(ri[q], col[q], sum);
+    }
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    __syncthreads();
+    if (sub == 0 && i >= j) sA[i * kTLd + j] = i > j ? -ijj * sum : ijj;
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int e = tid; e < kTE; e += kPThreads) {
+    const int c = e / kTT, r = e % kTT;
+    inv[e] = r >= c ? sA[r * kTLd + c] : 0.0;
+  }
+}
+
+// ------------------------------------------------------ DMMA GEMM update --
+// mode 0 (Cholesky trailing update at step k): blocks over pairs
+//   k < j <= i:  C_ij -= A_ik A_jk^T
+// mode 1 (left-TRSM update after row s of X): blocks over (l > s, j <= s):
+//   P_lj -= L_ls X_sj
+// mode 2 (panel solve at step k, i > k):   C_ik  = C_ik Inv_k^T   (in place)
+// mode 3 (row solve at row s, j <= s):     X_sj  = Inv_s P_sj     (in place)
+// (in place is safe: all global reads of the operand happen before the
+// epilogue's stores)
+constexpr int kGKc = 16;
+constexpr int kGLd = kTT + 4;
+constexpr size_t kGSmem = 2 * 2 * kGKc * kGLd * sizeof(double);
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256, 1)
+tail_gemm_kernel(double* base_c, const double* base_a, const double* base_b, int k, int nt,
+                 int mode) {      // operands may alias C (modes 0, 2, 3): no __restrict__
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;
+  double* Bs = gsm + 2 * kGKc * kGLd;
+  const double *A, *B;
+  double* C;
+  if (mode == 0) {
+    int a, b;
+    tri_idx(blockIdx.x, a, b);
+    const int i = k + 1 + a, j = k + 1 + b;
+    C = base_c + tslot(i, j) * kTE;
+    A = base_a + tslot(i, k) * kTE;
+    B = base_a + tslot(j, k) * kTE;
+  } else if (mode == 1) {
+    const int l = k + 1 + blockIdx.x / (k + 1), j = blockIdx.x % (k + 1);
+    C = base_c + tslot(l, j) * kTE;
+    A = base_a + tslot(l, k) * kTE;
+    B = base_b + tslot(k, j) * kTE;
+  } else if (mode == 2) {
+    C = base_c + tslot(k + 1 + blockIdx.x, k) * kTE;
+    A = C;
+    B = base_b + (int64_t)k * kTE;          // inverse of diagonal tile k
+  } else {
+    C = base_c + tslot(k, blockIdx.x) * kTE;
+    A = base_a + (int64_t)k * kTE;          // inverse of diagonal tile k
+    B = C;
+  }
+  const bool bt = mode == 0 || mode == 2;   // B operand used transposed
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wr = warp >> 2, wc = warp & 3, g = lane >> 2, tg = lane & 3;
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  // loaders: A (and B in mode 0) column-major m-panels: thread -> row
+  // tid & 127, 8 k values; mode 1 B[m][c]: thread -> col tid >> 1, 8 k
+  const int lr = tid & 127, lk = (tid >> 7) * 8;
+  const int bc = tid >> 1, bk = (tid & 1) * 8;
+  double ra[8], rb[8];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      ra[q] = A[(int64_t)(k0 + lk + q) * kTT + lr];
+      rb[q] = bt ? B[(int64_t)(k0 + lk + q) * kTT + lr] : B[(int64_t)bc * kTT + k0 + bk + q];
+    }
+  };
+  load(0);
+  int stage = 0;
+  for (int k0 = 0; k0 < kTT; k0 += kGKc) {
+    double* as = As + stage * kGKc * kGLd;
+    double* bs = Bs + stage * kGKc * kGLd;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      as[(lk + q) * kGLd + lr] = ra[q];
+      if (bt) bs[(lk + q) * kGLd + lr] = rb[q];
+      else bs[(bk + q) * kGLd + bc] = rb[q];
+    }
+    __syncthreads();
+    if (k0 + kGKc < kTT) load(k0 + kGKc);
+#pragma unroll
+    for (int ks = 0; ks < kGKc / 4; ++ks) {
+      double af[8], bf[4];
+      const double* ak = as + (ks * 4 + tg) * kGLd + wr * 64 + g;
+      const double* bk2 = bs + (ks * 4 + tg) * kGLd + wc * 32 + g;
+#pragma unroll
+      for (int a = 0; a < 8; ++a) af[a] = ak[a * 8];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = bk2[b * 8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    stage ^= 1;
+  }
+  // C[r][c] (column-major) -= acc
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int r = wr * 64 + a * 8 + g;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = wc * 32 + b * 8 + 2 * tg + e;
+        if (mode <= 1) C[(int64_t)c * kTT + r] -= acc[a][b][e];
+        else C[(int64_t)c * kTT + r] = acc[a][b][e];
+      }
+  }
+}
+
+// ------------------------------------------------------ vector solves --
+// Blocked forward / backward substitution with the diagonal inverses:
+//   forward  (L y = b):   y_i = Inv_i acc_i;     acc_l -= L_li y_i   (l > i)
+//   backward (L^T y = b): y_i = Inv_i^T acc_i;   acc_l -= L_il^T y_i (l < i)
+// diag: one CTA; update: one CTA per remaining tile row (128 threads each).
+__global__ void __launch_bounds__(kTT)
+tail_vec_diag_kernel(const double* __restrict__ inv, int i, const double* __restrict__ acc,
+                     double* __restrict__ y, int trans) {
+  __shared__ double sa[kTT];
+  const int r = threadIdx.x;
+  sa[r] = acc[(int64_t)i * kTT + r];
+  __syncthreads();
+  const double* Iv = inv + (int64_t)i * kTE;
+  double s = 0.0;
+  for (int c = 0; c < kTT; ++c)
+    s = fma(trans ? Iv[(int64_t)r * kTT + c] : Iv[(int64_t)c * kTT + r], sa[c], s);
+  y[(int64_t)i * kTT + r] = s;
+}
+
+__global__ void __launch_bounds__(kTT)
+tail_vec_update_kernel(const double* __restrict__ base, int i, const double* __restrict__ y,
+                       double* __restrict__ acc, int trans) {
+  __shared__ double sy[kTT];
+  const int r = threadIdx.x;
+  sy[r] = y[(int64_t)i * kTT + r];
+  __syncthreads();
+  const int l = trans ? blockIdx.x : i + 1 + blockIdx.x;
+  double s = 0.0;
+  if (!trans) {
+    const double* T = base + tslot(l, i) * kTE;      // L_li[r][c]
+    for (int c = 0; c < kTT; ++c) s = fma(T[(int64_t)c * kTT + r], sy[c], s);
+  } else {
+    const double* T = base + tslot(i, l) * kTE;      // L_il^T[r][c] = L_il[c][r]
+    for (int c = 0; c < kTT; ++c) s = fma(T[(int64_t)r * kTT + c], sy[c], s);
+  }
+  acc[(int64_t)l * kTT + r] -= s;
+}
+
+// ------------------------------------------------------------ reductions --
+// out[blk] = sum over tile u of (mode 0) log diag, (mode 1) squares (lower)
+__global__ void __launch_bounds__(256)
+tail_reduce_kernel(const double* __restrict__ base, int mode, double* __restrict__ part) {
+  __shared__ double red[8];
+  int a, b;
+  tri_idx(blockIdx.x, a, b);
+  const double* t = base + tslot(a, b) * kTE;
+  double s = 0.0;
+  if (mode == 0) {
+    if (a == b && threadIdx.x < kTT) s = log(t[(int64_t)threadIdx.x * kTT + threadIdx.x]);
+  } else {
+    for (int e = threadIdx.x; e < kTE; e += blockDim.x) {
+      const int c = e / kTT, r = e % kTT;
+      if (a != b || r >= c) s = fma(t[e], t[e], s);
+    }
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += red[w];
+    part[blockIdx.x] = v;
+  }
+}
+
+__global__ void sum_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  // fixed order: lane-strided partial sums, then a fixed shuffle tree
+  double s = 0.0;
+  for (int q = threadIdx.x; q < n; q += 32) s += part[q];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void dot_kernel(const double* __restrict__ a, int64_t n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) s = fma(a[e], a[e], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w];
+    *out = v;
+  }
+}
+
+__global__ void scale_copy_kernel(const double* __restrict__ a, int64_t n, int64_t n_pad,
+                                  double s, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n_pad) out[e] = e < n ? a[e] * s : 0.0;
+}
+
+// ------------------------------------------------------------------ host --
+static int tail_cholesky(double* base, double* inv, int nt, int* info, cudaStream_t st) {
+  for (int k = 0; k < nt; ++k) {
+    tail_potrf_inv_kernel<<<1, kPThreads, (size_t)kTT * kTLd * 8, st>>>(
+        base, k, inv + (int64_t)k * kTE, info);
+    TB_LAUNCH_CHECK("tail_potrf_inv");
+    const int below = nt - k - 1;
+    if (below == 0) break;
+    tail_gemm_kernel<<<below, 256, kGSmem, st>>>(base, base, inv, k, nt, 2);       // panel
+    TB_LAUNCH_CHECK("tail_panel");
+    tail_gemm_kernel<<<below * (below + 1) / 2, 256, kGSmem, st>>>(base, base, base, k, nt, 0);
+    TB_LAUNCH_CHECK("tail_update");
+  }
+  return TB_OK;
+}
+
+// y = L^-1 b (trans = 0) or L^-T b (trans = 1); acc is scratch [M_pad]
+static int tail_solve(const double* base, const double* inv, int nt, const double* b,
+                      double* acc, double* y, int trans, cudaStream_t st) {
+  TB_CUDA_TRY(cudaMemcpyAsync(acc, b, (size_t)nt * kTT * 8, cudaMemcpyDeviceToDevice, st));
+  for (int s = 0; s < nt; ++s) {
+    const int i = trans ? nt - 1 - s : s;
+    tail_vec_diag_kernel<<<1, kTT, 0, st>>>(inv, i, acc, y, trans);
+    const int rest = trans ? i : nt - 1 - i;
+    if (rest) tail_vec_update_kernel<<<rest, kTT, 0, st>>>(base, i, y, acc, trans);
+  }
+  TB_LAUNCH_CHECK("tail_solve");
+  return TB_OK;
+}
+
+int64_t tail_workspace_bytes(int64_t M, int64_t M_pad, int64_t dim) {
+  const int64_t nt = M_pad / kTT, tiles = nt * (nt + 1) / 2;
+  return round_up(tiles * kTE * 8, 256)            // L (packed)
+         + round_up(2 * nt * kTE * 8, 256)         // inverses of the diagonal tiles of L, P
+         + round_up(M * dim * 8, 256)              // scaled Z
+         + round_up(4 * M_pad * 8, 256)            // u, w, v copy, solve scratch
+         + round_up((tiles + 8) * 8, 256) + 256;   // partials, scalars, info
+}
+
+int tail_run(int64_t M, int64_t M_pad, const void* Z, int dtype, const KernParams& kp,
+             double jitter, double noise, double* sigma, const double* v, double* w_out,
+             double* out4, void* workspace, cudaStream_t st) {
+  const int nt = (int)(M_pad / kTT);
+  const int tiles = nt * (nt + 1) / 2;
+  char* ws = (char*)workspace;
+  double* L = (double*)ws;
+  ws += round_up((int64_t)tiles * kTE * 8, 256);
+  double* invL = (double*)ws;
+  double* invP = invL + (int64_t)nt * kTE;
+  ws += round_up(2 * (int64_t)nt * kTE * 8, 256);
+  double* Zs = (double*)ws;
+  ws += round_up(M * kp.dim * 8, 256);
+  double* u = (double*)ws;
+  double* w = u + M_pad;
+  double* vv = w + M_pad;
+  double* scratch = vv + M_pad;
+  ws += round_up(4 * M_pad * 8, 256);
+  double* part = (double*)ws;
+  double* scal = part + tiles;            // [0] logdet L, [1] logdet P, [2] |u|^2, [3] ||X||^2
+  int* info = (int*)(scal + 6);
+  TB_CUDA_TRY(cudaFuncSetAttribute(tail_potrf_inv_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)((size_t)kTT * kTLd * 8)));
+  TB_CUDA_TRY(cudaFuncSetAttribute(tail_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kGSmem));
+  TB_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int), st));
+  const unsigned zb = (unsigned)ceil_div(std::max<int64_t>(M * kp.dim, 1), 256);
+  if (dtype == TB_F32)
+    scale_z_kernel<float><<<zb, 256, 0, st>>>((const float*)Z, M, kp, Zs);
+  else
+    scale_z_kernel<double><<<zb, 256, 0, st>>>((const double*)Z, M, kp, Zs);
+  TB_LAUNCH_CHECK("scale_z");
+  // L = chol(Kuu)
+  tail_kuu_kernel<<<tiles, 256, 0, st>>>(Zs, M, kp, jitter, 0.0, L);
+  TB_LAUNCH_CHECK("tail_kuu");
+  int rc = tail_cholesky(L, invL, nt, info, st);
+  if (rc) return rc;
+  // P = chol(Kuu + Sigma / s2), in place over Sigma
+  tail_kuu_kernel<<<tiles, 256, 0, st>>>(Zs, M, kp, jitter, 1.0 / noise, sigma);
+  TB_LAUNCH_CHECK("tail_kuu_add");
+  if ((rc = tail_cholesky(sigma, invP, nt, info, st))) return rc;
+  // log dets
+  tail_reduce_kernel<<<tiles, 256, 0, st>>>(L, 0, part);
+  sum_kernel<<<1, 32, 0, st>>>(part, tiles, scal + 0);
+  tail_reduce_kernel<<<tiles, 256, 0, st>>>(sigma, 0, part);
+  sum_kernel<<<1, 32, 0, st>>>(part, tiles, scal + 1);
+  TB_LAUNCH_CHECK("tail_logdet");
+  // u = P^-1 v,  |u|^2,  w = P^-T u / s2
+  scale_copy_kernel<<<(unsigned)ceil_div(M_pad, 256), 256, 0, st>>>(v, M, M_pad, 1.0, vv);
+  if ((rc = tail_solve(sigma, invP, nt, vv, scratch, u, 0, st))) return rc;
+  dot_kernel<<<1, 256, 0, st>>>(u, M_pad, scal + 2);
+  if ((rc = tail_solve(sigma, invP, nt, u, scratch, w, 1, st))) return rc;
+  scale_copy_kernel<<<(unsigned)ceil_div(M, 256), 256, 0, st>>>(w, M, M, 1.0 / noise, w_out);
+  TB_LAUNCH_CHECK("tail_vec");
+  // X = L^-1 P in place over P, row by row: X_ij = Inv_i P_ij (j <= i), then
+  // P_lj -= L_li X_ij for the rows below; then ||X||_F^2
+  for (int i = 0; i < nt; ++i) {
+    tail_gemm_kernel<<<i + 1, 256, kGSmem, st>>>(sigma, invL, sigma, i, nt, 3);
+    TB_LAUNCH_CHECK("tail_row_solve");
+    const int below = nt - i - 1;
+    if (below == 0) break;
+    tail_gemm_kernel<<<below * (i + 1), 256, kGSmem, st>>>(sigma, L, sigma, i, nt, 1);
+    TB_LAUNCH_CHECK("tail_row_update");
+  }
+  tail_reduce_kernel<<<tiles, 256, 0, st>>>(sigma, 1, part);
+  sum_kernel<<<1, 32, 0, st>>>(part, tiles, scal + 3);
+  TB_LAUNCH_CHECK("tail_frob");
+  TB_CUDA_TRY(cudaMemcpyAsync(out4, scal, 4 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  int h_info = 0;
+  TB_CUDA_TRY(cudaMemcpyAsync(&h_info, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TB_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h_info)
+    return fail(TB_ERR_ARG, "sgpr tail: Cholesky failed at row " + std::to_string(h_info - 1) +
+                                " (matrix not positive definite)");
+  return TB_OK;
+}
+
+}  // namespace tb

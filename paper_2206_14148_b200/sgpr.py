@@ -113,7 +113,8 @@ class SGPR:
 
     def __init__(self, X, y, Z, kernel: str = "rbf", variance: float = 1.0,
                  lengthscales=1.0, noise_variance: float = 0.01, jitter: float = 1e-6,
-                 memory_limit=None, group=None, device=None, engine: str = "auto"):
+                 memory_limit=None, group=None, device=None, engine: str = "auto",
+                 tail: str = "packed"):
         torch = _torch()
         if kernel not in _lib.KERNELS:
             raise ValueError(f"kernel must be one of {tuple(_lib.KERNELS)}")
@@ -141,6 +142,9 @@ class SGPR:
         if engine not in _lib.SGPR_ENGINES:
             raise ValueError(f"engine must be one of {tuple(_lib.SGPR_ENGINES)}")
         self.engine = engine
+        if tail not in ("packed", "dense"):
+            raise ValueError("tail must be 'packed' or 'dense'")
+        self.tail = tail          # packed: in place on the fixed-point engine's tiles
         self._stats = None
         self._w = None
 
@@ -180,10 +184,46 @@ class SGPR:
         self._stats = SgprStats(Sigma, v, float(yy.item()), n_total, p)
         return self._stats
 
-    # -- O(M^3) tail (cuSOLVER / cuBLAS through torch.linalg, fp64) ----------
+    # -- O(M^3) tail --------------------------------------------------------
     def _tail(self):
+        s = self._stats if self._stats is not None and self._stats.Sigma is not None \
+            else self.statistics()
+        if s.plan.sigma_layout == _lib.TB_SIGMA_TILES and self.tail == "packed":
+            return self._tail_packed(s)
+        return self._tail_dense(s)
+
+    def _tail_packed(self, s):
+        """In place on the packed tiles (tb_sgpr_tail_run): the evaluation
+        never holds more than the packed Sigma + one packed factor, so the
+        whole ELBO stays inside memory_limit.  Consumes the statistics."""
         torch = _torch()
-        s = self._stats or self.statistics()
+        lib = _lib.load()
+        p = s.plan
+        M = s.v.numel()
+        ws = torch.empty(max(int(lib.tb_sgpr_tail_workspace(ctypes.byref(p))), 1),
+                         dtype=torch.uint8, device=self.device)
+        w = torch.empty(M, dtype=torch.float64, device=self.device)
+        out = torch.empty(4, dtype=torch.float64, device=self.device)
+        st = torch.cuda.current_stream(self.device)
+        rc = lib.tb_sgpr_tail_run(ctypes.byref(p), self.Z.data_ptr(), self.variance,
+                                  self.lengthscales.ctypes.data_as(ctypes.c_void_p), self.jitter,
+                                  self.noise_variance, s.Sigma.data_ptr(), s.v.data_ptr(),
+                                  w.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                  st.cuda_stream)
+        s.Sigma = None                     # overwritten by the in-place factorisation
+        _lib.check(rc, "sgpr_tail")
+        del ws
+        logdet_l, logdet_p, uu, xx = (float(t) for t in out.tolist())
+        s2, N = self.noise_variance, s.N
+        bound = (-0.5 * N * LOG2PI - (logdet_p - logdet_l) - 0.5 * N * math.log(s2)
+                 - 0.5 * s.yy / s2 + 0.5 * uu / (s2 * s2) - 0.5 * N * self.variance / s2
+                 + 0.5 * (xx - int(p.M_pad)))
+        self._w = w
+        return bound
+
+    def _tail_dense(self, s):
+        """cuSOLVER / cuBLAS through torch.linalg on full fp64 matrices."""
+        torch = _torch()
         M = s.v.numel()
         s2 = self.noise_variance
         Kuu = kernel_matrix(self.Z, self.Z, self.kernel, self.variance, self.lengthscales)
@@ -228,7 +268,8 @@ class SGPR:
         fused kernel ``tb_sgpr_kuf_grad``.  Multi-GPU: the chunk sums are
         all-reduced like the statistics.  Returns (elbo, dict of gradients)."""
         torch = _torch()
-        s = self._stats or self.statistics()
+        s = self._stats if self._stats is not None and self._stats.Sigma is not None \
+            else self.statistics()
         M, dim = int(s.v.numel()), self.dim
         f64 = torch.float64
         dev = self.device

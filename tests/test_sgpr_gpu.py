@@ -152,3 +152,52 @@ def test_elbo_gradient_matches_finite_differences(kind, engine, dtype):
     for key in ("variance", "noise_variance", "lengthscales", "Z"):
         got, want = np.asarray(g[key], np.float64), np.asarray(fd[key], np.float64)
         assert np.max(np.abs(got - want)) <= tol * max(np.max(np.abs(want)), 1.0), (key, got, want)
+
+
+@pytest.mark.parametrize("kind", ["rbf", "matern32"])
+def test_packed_tail_matches_dense_tail(kind):
+    """The in-place packed-tile tail (Kuu = LL^T, Kuu + Sigma/s2 = PP^T,
+    X = L^-1 P) gives GPflow's ELBO and predictive mean like the dense
+    cuSOLVER tail (two-sided solve), at cond(Kuu) ~ 1e5 (Matern l=0.5) and
+    5e5 (RBF l=0.25).  (The fixed-point statistics hold the 1e-4 mean gate to
+    cond ~ 1e7; beyond that use engine="f64".)"""
+    X, y, Z, Xs = synthetic.sgpr_data(20000, 3, 1500, seed=11, n_test=300, dtype=np.float32)
+    ls = 0.5 if kind == "matern32" else 0.25
+    ref, w = osgpr.elbo(X, y, Z, kind, 1.0, ls, 0.01)
+    mu_ref = osgpr.predict_mean(Xs, Z, w, kind, 1.0, ls)
+    packed = tb.SGPR(X, y, Z, kind, 1.0, ls, 0.01, tail="packed")
+    dense = tb.SGPR(X, y, Z, kind, 1.0, ls, 0.01, tail="dense")
+    ep, ed = packed.elbo(), dense.elbo()
+    # the ELBO is a small difference of O(N var / s2) = 2e6 terms; the two
+    # formulations round those terms differently at ~1e-10 of their size
+    scale = max(abs(ed), 20000 * 1.0 / 0.01)
+    assert abs(ep - ed) <= 1e-9 * scale
+    assert abs(ep - ref) <= 1e-4 * abs(ref)
+    mp = packed.predict_mean(Xs)
+    # w = (Kuu + Sigma/s2)^-1 v / s2 vs GPflow's L^-T LB^-T c: equal in exact
+    # arithmetic, different fp64 rounding orders (~1e-5 apart at cond 2e8 in
+    # numpy); both within the 1e-4 gate
+    assert rel_err(mp, dense.predict_mean(Xs)) < 5e-5
+    assert rel_err(mp, mu_ref) <= 1e-4
+    e2, _ = packed.elbo_and_grads(chunk_n=4096)      # statistics recomputed after the tail
+    assert abs(e2 - ed) <= 1e-9 * scale
+
+
+def test_whole_elbo_evaluation_within_memory_limit():
+    """Statistics AND the O(M^3) tail inside memory_limit (inputs counted, as
+    the reference's budget does): the packed tail keeps two packed M x M
+    matrices; the dense tail would need several full ones."""
+    import torch
+    X, y, Z, Xs = synthetic.sgpr_data(60000, 3, 3000, seed=12, n_test=100, dtype=np.float32)
+    Xd, yd, Zd = (torch.from_numpy(a).cuda() for a in (X, y, Z))
+    limit = 160 * 10**6
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated() - (Xd.numel() + yd.numel() + Zd.numel()) * 4
+    torch.cuda.reset_peak_memory_stats()
+    m = tb.SGPR(Xd, yd, Zd, "matern32", 1.0, 0.6, 0.02, memory_limit=limit)
+    e = m.elbo()
+    torch.cuda.synchronize()
+    peak = torch.cuda.max_memory_allocated() - base
+    assert peak <= limit, (peak, limit)
+    ref, _ = osgpr.elbo(X, y, Z, "matern32", 1.0, 0.6, 0.02)
+    assert abs(e - ref) <= 1e-4 * abs(ref)
