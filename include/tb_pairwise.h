@@ -191,8 +191,10 @@ typedef struct tb_sgpr_plan {
   int64_t chunk_n;          /* training points per streamed chunk           */
   int64_t workspace_bytes;
   int64_t output_bytes;     /* Sigma + v + yy                               */
-  int64_t peak_bytes;       /* resident + outputs + workspace <= limit      */
-  int64_t off[8];
+  int64_t peak_bytes;       /* resident + outputs + workspace <= limit; for the
+                               fixed-point engine also the packed tail's peak */
+  int64_t off[8];           /* internal; off[5] = tail workspace bytes,
+                               off[6] = tail peak (TB_SIGMA_TILES plans)     */
 } tb_sgpr_plan;
 
 TB_API int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel,

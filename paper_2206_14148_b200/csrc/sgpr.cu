@@ -405,6 +405,16 @@ int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel, int32
         if (fixed + alloc_bytes(nbuf * buf_bytes(nc)) <= limit) return nc;
       return 0;
     };
+    // the packed O(M^3) tail (tb_sgpr_tail_run) runs after the chunk buffers
+    // are released: Sigma + v + packed factor + inverses + w must fit too
+    const int64_t tail_ws = tail_workspace_bytes(M, M_pad, dim);
+    const int64_t tail_peak = fixed + alloc_bytes(tail_ws) + alloc_bytes(M * 8) + alloc_bytes(32);
+    if (tail_peak > limit)
+      return fail(TB_ERR_BUDGET, "sgpr: the O(M^3) tail needs " + std::to_string(tail_peak) +
+                                     " bytes on the device (limit " + std::to_string(memory_limit) +
+                                     ")");
+    plan->off[5] = tail_ws;
+    plan->off[6] = tail_peak;
     const int64_t n1 = largest(1), n2 = N > cap ? largest(2) : 0;
     if (!n1) return budget_fail(buf_bytes(128));
     const int nbuf = (n2 && 2 * n2 >= n1) ? 2 : 1;
@@ -416,7 +426,7 @@ int tb_sgpr_plan_create(int64_t N, int64_t M, int64_t dim, int32_t kernel, int32
     plan->off[3] = plan->off[2] + plan->off[1];
     plan->off[4] = nbuf;
     plan->workspace_bytes = nbuf * buf_bytes(nc);
-    plan->peak_bytes = fixed + alloc_bytes(plan->workspace_bytes);
+    plan->peak_bytes = std::max(fixed + alloc_bytes(plan->workspace_bytes), tail_peak);
     return TB_OK;
   }
   // fp64 engines: one fp64 Kuf chunk [M_pad, nc]; as large as the budget

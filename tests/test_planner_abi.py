@@ -191,8 +191,11 @@ def test_sgpr_planner_engines_and_c4_budget():
     assert p.M_pad == 10_112
     assert p.sigma_bytes == (79 * 80 // 2) * 128 * 128 * 8
     assert p.off[4] == 2 and p.chunk_n == 7808 and p.peak_bytes <= 1_000_000_000
-    one = sgpr.plan(N, M, d, kernel="rbf", memory_limit="700MB", resident_bytes=resident)
-    assert one.off[4] == 1 and one.chunk_n < 7808 and one.peak_bytes <= 700_000_000
+    assert p.off[6] <= p.peak_bytes              # the packed O(M^3) tail fits too
+    with pytest.raises(tb.BudgetExceeded, match="tail"):
+        sgpr.plan(N, M, d, kernel="rbf", memory_limit="900MB", resident_bytes=resident)
+    tight = sgpr.plan(200_000, 2000, d, kernel="rbf", memory_limit="60MB")
+    assert tight.chunk_n < 10_880 and tight.peak_bytes <= 60_000_000
     small = sgpr.plan(5000, 300, 4, kernel="rbf")
     assert small.off[4] == 1 and small.chunk_n == 5120          # one chunk: no overlap
     f = sgpr.plan(N, M, d, kernel="rbf", memory_limit="1GB", resident_bytes=resident,
