@@ -84,6 +84,13 @@ class ClockSampler:
             self.thread.start()
         except OSError:
             self.proc = None
+            return
+        # nvidia-smi takes ~0.1-0.3 s to print its first line: wait for it so
+        # the (short) timed region that follows is actually sampled
+        t_end = time.time() + 3.0
+        while not self.lines and time.time() < t_end and self.proc.poll() is None:
+            time.sleep(0.01)
+        self.lines.clear()
 
     def _read(self):
         for line in self.proc.stdout:
@@ -192,6 +199,8 @@ def run_sgpr(args, dev, world, rank, dist):
         dist.barrier()
     torch.cuda.synchronize()
     m = SGPR(X, y, Z, "rbf", 1.0, 1.0, 0.01, memory_limit=LIMIT, group=group)
+    sampler = ClockSampler(dev.index or 0)
+    sampler.start()
     e0.record()
     st = m.statistics()
     e1.record()
@@ -201,6 +210,7 @@ def run_sgpr(args, dev, world, rank, dist):
     e2.record()
     torch.cuda.synchronize()
     peak_eval = torch.cuda.max_memory_allocated(dev) - base
+    clocks = sampler.stop()
     stats_ms, total_ms = e0.elapsed_time(e1), e0.elapsed_time(e2)
     if dist is not None:
         t = torch.tensor([stats_ms, total_ms], device=dev, dtype=torch.float64)
@@ -217,6 +227,7 @@ def run_sgpr(args, dev, world, rank, dist):
     traffic, alg_bytes, rep = _traffic("sgpr_gram_i8")
     out = {"metric": "sgpr_elbo_evals_per_s", "value": 1e3 / total_ms, "unit": "elbo_evals/s",
            "ms_per_eval": total_ms, "stats_ms": stats_ms, "tail_ms": total_ms - stats_ms,
+           "clocks": clocks,
            "elbo": elbo, "dtype": "f32 inputs; Kuf rounded once to 24-bit fixed point, exact "
                                    "integer Gram (u8 slices, s32 TMEM); fp64 accumulation and tail",
            "config": {"workload": "sgpr_c4_rbf_N2e6_d11_M1e4_1GB", "N": SG_N, "d": SG_D,
@@ -369,15 +380,16 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e and world == 1:
         # the reference-facing call with HOST buffers (tb_knn_run_host): pinned
-        # x, q copied in (database chunk by chunk, overlapped with compute)
-        # and dist, idx copied out, every step.  Its plan caps chunks at n/8
-        # so seven of the eight database copies overlap compute (tools/
-        # e2e_chunks.py: 2/4/8/16 chunks -> 771k/844k/913k/813k q/s).
+        # x, q copied in (queries first, then the database chunk by chunk on
+        # one copy stream, overlapped with compute) and dist, idx copied out,
+        # every step.  Its plan caps chunks at n/16 so fifteen of the sixteen
+        # database copies overlap compute (tools/e2e_chunks.py: 4/8/12/16/24
+        # chunks -> 0.89/0.97/0.99/1.00/0.85 M q/s; the bound is PCIe).
         xh = x.cpu().pin_memory()
         qh = q.cpu().pin_memory()
         op_h = neighbors.KnnOperator(rows, M_Q, DIM, K, dtype=np.float32, out_dtype=out_dtype,
                                      engine=args.engine, memory_limit=LIMIT, device=dev,
-                                     max_chunk_rows=-(-rows // 8))
+                                     max_chunk_rows=-(-rows // 16))
         staging = (x, q, out[0], out[1])      # device buffers refilled every step
         dh = torch.empty(out[0].shape, dtype=out[0].dtype).pin_memory()
         ih = torch.empty(out[1].shape, dtype=out[1].dtype).pin_memory()
@@ -391,12 +403,37 @@ def run_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
+        h0 = time.perf_counter()
         for _ in range(args.steps):
             e2e_step()
+        host_ms = (time.perf_counter() - h0) * 1000 / args.steps
         e1.record()
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
+        if os.environ.get("TB_BENCH_TRACE"):      # diagnosis: CUPTI timeline of 2 steps
+            from torch.profiler import profile, ProfilerActivity
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                for _ in range(2):
+                    e2e_step()
+                torch.cuda.synchronize()
+            tl = sorted((e.time_range.start, e.time_range.end, e.name[:60])
+                        for e in prof.events() if e.device_type.name == "CUDA")
+            with open(os.environ["TB_BENCH_TRACE"], "w") as f:
+                for a, b, nm in tl:
+                    f.write(f"{(a - tl[0][0]) / 1000:9.3f} {(b - a) / 1000:8.3f}  {nm}\n")
+        # the bound of this path: one pinned host->device copy of the same
+        # bytes, alone (PCIe), timed the same way
+        hb = int(x.numel() * 4 + q.numel() * 4)
+        e0.record()
+        for _ in range(3):
+            x.copy_(xh, non_blocking=True)
+            q.copy_(qh, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        h2d_ms = e0.elapsed_time(e1) / 3
         e2e = {"value": M_Q * args.steps / (ems / 1000.0), "unit": UNIT,
+               "h2d_only_ms": h2d_ms, "h2d_gbs": hb / h2d_ms / 1e6, "host_enqueue_ms": host_ms,
+               "frac_of_h2d_bound": h2d_ms / (ems / args.steps),
                "h2d_bytes_per_step": int(x.numel() * 4 + q.numel() * 4),
                "d2h_bytes_per_step": int(dh.numel() * dh.element_size() + ih.numel() * 8),
                "ms_per_step": ems / args.steps,

@@ -161,13 +161,15 @@ int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int32_t me
 
   const int tile_rows = tc ? 256 : 128;
   const int ctas_per_sm = 1;
+  const int passes = engine == TB_ENGINE_TC1 ? 1 : 3;
 
   auto layout = [&](int64_t chunk_rows, int slices) -> int64_t {
     Carve c;
     const int64_t chunk_pad = round_up(chunk_rows, tile_rows);
     const int64_t last = n - (ceil_div(n, chunk_rows) - 1) * chunk_rows;
     const int64_t lists =
-        tc ? std::max(tc_lists(m, chunk_pad, kPlanSms), tc_lists(m, round_up(last, tile_rows), kPlanSms))
+        tc ? std::max(tc_lists(m, chunk_pad, kPlanSms, passes, plan->d_pad),
+                      tc_lists(m, round_up(last, tile_rows), kPlanSms, passes, plan->d_pad))
            : 2 * (int64_t)slices;
     plan->off[kQn64] = c.take(m * 8);
     plan->off[kQnorm] = c.take(m * 4);
@@ -267,7 +269,12 @@ int tb_knn_run_host(const tb_knn_plan* p, const void* x_host, const void* q_host
     // the copy stream starts after the caller's prior work on `stream`
     cudaEventRecord(ready[p->n_chunks], st);
     cudaStreamWaitEvent(cp, ready[p->n_chunks], 0);
-    cudaMemcpyAsync(q_dev, q_host, p->m * p->d * es, cudaMemcpyHostToDevice, st);
+    // the queries go first on the SAME copy stream: host->device copies of
+    // two streams share one copy engine, and a query copy queued on `st`
+    // could be scheduled behind every database chunk (no overlap at all)
+    cudaMemcpyAsync(q_dev, q_host, p->m * p->d * es, cudaMemcpyHostToDevice, cp);
+    cudaEventRecord(ready[p->n_chunks], cp);
+    cudaStreamWaitEvent(st, ready[p->n_chunks], 0);
     for (int64_t c = 0; c < p->n_chunks; ++c) {
       const int64_t c0 = c * p->chunk_rows, rows = std::min(p->chunk_rows, p->n - c0);
       cudaMemcpyAsync((char*)x_dev + c0 * p->d * es, (const char*)x_host + c0 * p->d * es,
@@ -346,7 +353,8 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
                         rows_pad, p->d_pad, xext, st);
     if (rc) return rc;
     const int slices = (int)std::min<int64_t>(p->slices, ceil_div(rows, tile_rows));
-    int lists = tc ? tc_lists(p->m, rows_pad, kPlanSms) : slices * 2;
+    int lists = tc ? tc_lists(p->m, rows_pad, kPlanSms, p->engine == TB_ENGINE_TC1 ? 1 : 3, p->d_pad)
+                   : slices * 2;
     const bool prof = events && 2 * c + 1 < n_events;
     if (prof) TB_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[2 * c], st));
     if (tc) {

@@ -54,7 +54,7 @@ int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi,
                   int64_t rows_pad, int64_t m, int64_t m_pad, int64_t d_pad,
                   int lists, int idx_base, float* cand_s, int* cand_i,
                   unsigned* gthr, cudaStream_t st);
-int tc_lists(int64_t m, int64_t rows_pad, int sms);
+int tc_lists(int64_t m, int64_t rows_pad, int sms, int passes, int64_t d_pad);
 int tc_max_dpad();
 // merge L lists (+ optional previous running list) into out
 int launch_knn_merge(int cand, const float* in_s, const int* in_i, int lists,

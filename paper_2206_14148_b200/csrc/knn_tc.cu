@@ -384,6 +384,286 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ------------------------------------------------ CTA-pair variant (tc3) --
+// Two CTAs of a cluster on one TPC process a pair of query tiles (256
+// queries) against the same 256-row database tile with tcgen05.mma
+// .cta_group::2 M256.N256.K16: each CTA keeps its own query tile resident
+// and stages HALF of every database k-block (128 rows); the leader issues
+// the MMAs for both SMs.  Per SM this halves the TMA bytes and the MMA /
+// barrier instructions of the single issuing thread - the 1-SM kernel's
+// limiters (profiles/r01_knn_tc_ncu_history.md) - while each CTA's epilogue
+// (its 128 queries x 256 columns out of its own TMEM) is unchanged.
+// "full" barriers live in the leader and receive both CTAs' TMA bytes;
+// "empty"/accumulator barriers are arrived in both CTAs by multicast
+// commits; epilogue warps of both CTAs arrive (one lane per warp) on the
+// leader's tempty.  d_pad <= 128, 3 passes.
+constexpr int kPrStages = 8;                        // 16 KB half k-blocks in flight
+constexpr uint32_t kPrHalf = kTcM * 128;            // 128 rows x 64 bf16 = 16 KB
+constexpr uint32_t kPrExt = kTcBExt / 2;            // this CTA's 128 rows of -||x||^2
+static size_t pair_smem_bytes(int nkb) {
+  return 1024 + (size_t)2 * nkb * kPrHalf + kTcAExt + (size_t)kPrStages * kPrHalf +
+         2 * kPrExt + (2 * kPrStages + 10) * 8 + 16;
+}
+
+template <int KC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
+knn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_qhi,
+                   const __grid_constant__ CUtensorMap tm_qlo,
+                   const __grid_constant__ CUtensorMap tm_xhi,
+                   const __grid_constant__ CUtensorMap tm_xlo,
+                   const __grid_constant__ CUtensorMap tm_ext, TcWork work, int m, int nkb,
+                   int idx_base, float* __restrict__ cand_s, int* __restrict__ cand_i,
+                   unsigned* __restrict__ gthr) {
+  constexpr int S = kPrStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* a_base = smem;                                      // q hi | q lo, nkb each
+  uint8_t* b_base = a_base + (size_t)2 * nkb * kPrHalf;
+  uint8_t* bext = b_base + (size_t)S * kPrHalf;                // 2 x 4 KB
+  uint8_t* aext = bext + 2 * kPrExt;                           // 4 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(aext + kTcAExt);
+  uint64_t* empty = full + S;
+  uint64_t* a_full = empty + S;
+  uint64_t* a_empty = a_full + 1;
+  uint64_t* tfull = a_empty + 1;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* efull = tempty + 2;
+  uint64_t* eempty = efull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(eempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int qpairs = (work.qtiles + 1) / 2;
+  const int units = qpairs * work.slices;
+
+  for (int r = threadIdx.x; r < kTcM; r += blockDim.x) {
+    uint4* c0 = reinterpret_cast<uint4*>(aext + (r >> 3) * 256 + (r & 7) * 16);
+    uint4* c1 = reinterpret_cast<uint4*>(aext + (r >> 3) * 256 + 128 + (r & 7) * 16);
+    const uint32_t one = 0x3F80u;                        // bf16(1.0)
+    *c0 = make_uint4(one | (one << 16), one, 0u, 0u);
+    *c1 = make_uint4(0u, 0u, 0u, 0u);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 2 * kTcEpiWarps);   // one lane per epilogue warp, both CTAs
+      mbar_init(&efull[b], 1);
+      mbar_init(&eempty[b], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producers
+    if (lane == 0) {
+      tma_prefetch(&tm_qhi);
+      tma_prefetch(&tm_qlo);
+      tma_prefetch(&tm_xhi);
+      tma_prefetch(&tm_xlo);
+      tma_prefetch(&tm_ext);
+      int s = 0, i = 0;
+      uint32_t ph = 0, seg = 0;
+      for (int u = pair; u < units; u += npairs, ++seg) {
+        const int slice = u / qpairs, qp = u - slice * qpairs;
+        const int qt = 2 * qp + (int)rank;
+        const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
+        mbar_wait(a_empty, (seg & 1) ^ 1);
+        const uint32_t afb = mapa_shared(a_full, 0);
+        if (rank == 0) mbar_expect_tx(a_full, 2 * 2 * nkb * kPrHalf);
+        for (int kb = 0; kb < nkb; ++kb) {
+          tma_load_2d_2sm(a_base + (size_t)kb * kPrHalf, &tm_qhi, afb, kb * kTcKB, qt * kTcM);
+          tma_load_2d_2sm(a_base + (size_t)(nkb + kb) * kPrHalf, &tm_qlo, afb, kb * kTcKB,
+                          qt * kTcM);
+        }
+        for (int t = t0; t < t1; ++t, ++i) {
+          const int e = i & 1;
+          mbar_wait(&eempty[e], ((i >> 1) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&efull[e], 2 * kPrExt);
+          tma_load_2d_2sm(bext + e * kPrExt, &tm_ext, mapa_shared(&efull[e], 0), 0,
+                          t * 32 + (int)rank * 16);
+          for (int kb = 0; kb < nkb; ++kb) {
+#pragma unroll
+            for (int mat = 0; mat < 2; ++mat) {
+              mbar_wait(&empty[s], ph ^ 1);
+              if (work.drain_only & 2) {
+                if (rank == 0) mbar_arrive(&full[s]);
+              } else {
+                if (rank == 0) mbar_expect_tx(&full[s], 2 * kPrHalf);
+                tma_load_2d_2sm(b_base + (size_t)s * kPrHalf, mat ? &tm_xlo : &tm_xhi,
+                                mapa_shared(&full[s], 0), kb * kTcKB,
+                                t * kTcN + (int)rank * kTcM);
+              }
+              if (++s == S) {
+                s = 0;
+                ph ^= 1;
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------- MMA issuer (leader)
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(2 * kTcM, kTcN);    // M256 N256
+      const uint32_t aext_a = smem_u32(aext);
+      int s = 0, i = 0;
+      uint32_t ph = 0, seg = 0;
+      for (int u = pair; u < units; u += npairs, ++seg) {
+        const int slice = u / qpairs;
+        const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
+        mbar_wait(a_full, seg & 1);
+        tc_fence_after();
+        for (int t = t0; t < t1; ++t, ++i) {
+          const int buf = i & 1;
+          mbar_wait(&tempty[buf], ((i >> 1) & 1) ^ 1);
+          mbar_wait(&efull[buf], (i >> 1) & 1);
+          tc_fence_after();
+          const uint32_t d = tmem + buf * kTcN;
+          mma_bf16_2sm(d, desc_k_inter(aext_a, 128, 256),
+                       desc_k_inter(smem_u32(bext + buf * kPrExt), 128, 256), idesc, 0);
+          for (int kb = 0; kb < nkb; ++kb) {
+            const uint32_t ahi = smem_u32(a_base + (size_t)kb * kPrHalf);
+            const uint32_t alo = smem_u32(a_base + (size_t)(nkb + kb) * kPrHalf);
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            uint32_t b0 = smem_u32(b_base + (size_t)s * kPrHalf);
+#pragma unroll
+            for (int kk = 0; kk < kTcKB / 16; ++kk) {
+              const uint32_t ko = kk * 32;
+              if (work.drain_only & 4) continue;
+              mma_bf16_2sm(d, desc_k_sw128(ahi + ko), desc_k_sw128(b0 + ko), idesc, 1);
+              mma_bf16_2sm(d, desc_k_sw128(alo + ko), desc_k_sw128(b0 + ko), idesc, 1);
+            }
+            mma_commit_2sm(&empty[s], 3);
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            b0 = smem_u32(b_base + (size_t)s * kPrHalf);
+#pragma unroll
+            for (int kk = 0; kk < kTcKB / 16; ++kk)
+              if (!(work.drain_only & 4)) mma_bf16_2sm(d, desc_k_sw128(ahi + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, 1);
+            mma_commit_2sm(&empty[s], 3);
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+          mma_commit_2sm(&eempty[buf], 3);
+          mma_commit_2sm(&tfull[buf], 3);
+        }
+        mma_commit_2sm(a_empty, 3);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int ew = warp - 2;
+    const int quad = warp & 3;
+    const int half = ew >> 2;
+    const int row = quad * 32 + lane;
+    const uint32_t tempty_l[2] = {mapa_shared(&tempty[0], 0), mapa_shared(&tempty[1], 0)};
+    auto load_g = [&](int qq) -> unsigned {
+      return qq < m ? *reinterpret_cast<volatile unsigned*>(gthr + qq) : 0u;
+    };
+    TopList<float, KC> L;
+    L.init();
+    int u = pair;
+    if (u < units) {
+      int slice = u / qpairs, qp = u - slice * qpairs;
+      int t1 = min(work.T, work.t0 + slice * work.tps + work.tps);
+      int t = work.t0 + slice * work.tps;
+      int q = (2 * qp + (int)rank) * kTcM + row;
+      unsigned gk = load_g(q);
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        const float thr_g = q < m ? fkey_inv(gk) : -INFINITY;
+        int nu = u, nt = t + 1;
+        if (nt >= t1) {
+          nu = u + npairs;
+          nt = work.t0 + (nu / qpairs) * work.tps;
+        }
+        const bool more = nu < units;
+        if (more) gk = load_g((2 * (nu - (nu / qpairs) * qpairs) + (int)rank) * kTcM + row);
+        mbar_wait(&tfull[buf], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem + ((uint32_t)(quad * 32) << 16) + buf * kTcN + half * (kTcN / 2);
+        const int base = idx_base + t * kTcN + half * (kTcN / 2);
+#pragma unroll 1
+        for (int c = 0; c < kTcN / 64; c += 2) {
+          uint32_t ra[32], rb[32];
+          tmem_ld32(taddr + c * 32, ra);
+          tmem_ld32(taddr + (c + 1) * 32, rb);
+          tmem_ld_wait();
+          if (work.drain_only & 1) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t(&r)[32] = h ? rb : ra;
+            const float thr = fminf(L.worst(), thr_g);
+            float hi = __uint_as_float(r[0]);
+#pragma unroll
+            for (int j = 1; j < 32; ++j) hi = fmaxf(hi, __uint_as_float(r[j]));
+            if (-hi < thr && !(work.drain_only & 8)) {
+              float sc[32];
+              uint32_t mask = 0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                sc[j] = -__uint_as_float(r[j]);
+                mask |= (sc[j] < thr ? 1u : 0u) << j;
+              }
+              insert_masked(L, sc, mask, base + (c + h) * 32, thr_g);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_l[buf]);
+        if (q < m && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst()));
+        if (nu != u) {
+          if (q < m) {
+            const int64_t o = ((int64_t)(work.list0 + slice * 2 + half) * m + q) * KC;
+#pragma unroll
+            for (int p = 0; p < KC; ++p) {
+              cand_s[o + p] = L.s[p];
+              cand_i[o + p] = L.i[p];
+            }
+          }
+          L.init();
+          if (!more) break;
+          u = nu;
+          slice = u / qpairs;
+          qp = u - slice * qpairs;
+          t1 = min(work.T, work.t0 + slice * work.tps + work.tps);
+          q = (2 * qp + (int)rank) * kTcM + row;
+        }
+        t = nt;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_2sm(tmem, 512);
+}
+
 // ---------------------------------------------------------------- host --
 
 // bf16 [rows, cols] row-major, box [box_rows, 64], 128-B swizzle
@@ -412,8 +692,25 @@ int tc_max_dpad() { return kTcMaxDpadSQ; }
 // minimising waves x (tiles per slice + ~2 tiles of per-unit overhead).
 constexpr int kTcSeedTiles = 8;
 
-static void tc_schedule(int64_t m, int64_t rows_pad, int sms, TcWork* seed, TcWork* main_) {
+// CTA pairs (knn_tc_pair_kernel): opt-in with TB_TC_PAIR=1 for the 3-pass
+// engine with a resident query tile.  Measured at C2 (tools/tc_ab.py): the
+// 1-SM kernel's MMA path already runs at the tensor-core rate (4.45 ms vs
+// 4.35 ms paired, debug mode 3), and pairing couples the two CTAs'
+// epilogues through the shared accumulator barrier (5.74 vs 5.31 ms end to
+// end), so the 1-SM kernel is the default.
+static bool tc_pair_on(int passes, int64_t d_pad, int64_t m) {
+  const char* e = std::getenv("TB_TC_PAIR");
+  if (!e || *e != '1') return false;
+  return passes == 3 && d_pad <= kTcMaxDpad && m > kTcM;
+}
+
+// units are (query tile, slice) - or (query-tile pair, slice) on `sms`/2
+// CTA pairs in pair mode
+static void tc_schedule(int64_t m, int64_t rows_pad, int sms, bool pair, TcWork* seed,
+                        TcWork* main_) {
   const int qtiles = (int)ceil_div(std::max<int64_t>(m, 1), kTcM);
+  const int qunits = pair ? (qtiles + 1) / 2 : qtiles;
+  const int workers = pair ? sms / 2 : sms;
   const int T = (int)(rows_pad / kTcN);
   const int S = std::min(T, kTcSeedTiles);
   const char* dbg = std::getenv("TB_TC_DEBUG");
@@ -426,8 +723,8 @@ static void tc_schedule(int64_t m, int64_t rows_pad, int sms, TcWork* seed, TcWo
     for (int k = 1; k <= R && k <= 256; ++k) {
       const int64_t tps = ceil_div(R, k);
       const int64_t keff = ceil_div(R, tps);
-      const int64_t units = (int64_t)qtiles * keff;
-      const int64_t g = std::min<int64_t>(units, sms);
+      const int64_t units = (int64_t)qunits * keff;
+      const int64_t g = std::min<int64_t>(units, workers);
       const int64_t cost = ceil_div(units, g) * (tps + 2);
       if (cost < best) {
         best = cost;
@@ -439,10 +736,54 @@ static void tc_schedule(int64_t m, int64_t rows_pad, int sms, TcWork* seed, TcWo
   *main_ = TcWork{qtiles, S, T, best_k, tps, 2, drain};
 }
 
-int tc_lists(int64_t m, int64_t rows_pad, int sms) {
+int tc_lists(int64_t m, int64_t rows_pad, int sms, int passes, int64_t d_pad) {
   TcWork a, b;
-  tc_schedule(m, rows_pad, sms, &a, &b);
+  tc_schedule(m, rows_pad, sms, tc_pair_on(passes, d_pad, m), &a, &b);
   return 2 + 2 * b.slices;
+}
+
+// -||x||^2 blocks as u8 rows [T*32][256 B] (8-row core-matrix groups):
+// box = one CTA's 16 groups = 128 database rows of a tile
+static int make_ext_map(CUtensorMap* map, const uint8_t* xext, int64_t T) {
+  auto fn = tensor_map_encoder();
+  if (!fn) return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {256, (cuuint64_t)T * 32};
+  cuuint64_t strides[1] = {256};
+  cuuint32_t box[2] = {256, 16};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(xext), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled (ext) failed: " + std::to_string((int)r));
+  return TB_OK;
+}
+
+template <int KC>
+static int tc_pair_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtensorMap& xh,
+                          const CUtensorMap& xl, const CUtensorMap& ext, TcWork work, int grid,
+                          int64_t m, int nkb, int idx_base, float* cs, int* ci, unsigned* gthr,
+                          cudaStream_t st) {
+  const size_t smem = pair_smem_bytes(nkb);
+  TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_pair_kernel<KC>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  knn_tc_pair_kernel<KC><<<grid, kTcThreads, smem, st>>>(qh, ql, xh, xl, ext, work, (int)m, nkb,
+                                                         idx_base, cs, ci, gthr);
+  TB_LAUNCH_CHECK("knn_tc_pair");
+  return TB_OK;
+}
+
+static int tc_pair_dispatch(int cand, const CUtensorMap& qh, const CUtensorMap& ql,
+                            const CUtensorMap& xh, const CUtensorMap& xl, const CUtensorMap& ext,
+                            TcWork work, int grid, int64_t m, int nkb, int idx_base, float* cs,
+                            int* ci, unsigned* gthr, cudaStream_t st) {
+  if (cand == 16)
+    return tc_pair_launch<16>(qh, ql, xh, xl, ext, work, grid, m, nkb, idx_base, cs, ci, gthr, st);
+  if (cand == 32)
+    return tc_pair_launch<32>(qh, ql, xh, xl, ext, work, grid, m, nkb, idx_base, cs, ci, gthr, st);
+  if (cand == 64)
+    return tc_pair_launch<64>(qh, ql, xh, xl, ext, work, grid, m, nkb, idx_base, cs, ci, gthr, st);
+  return fail(TB_ERR_UNSUPPORTED, "tcgen05 engine: unsupported candidate count");
 }
 
 template <int PASSES, int KC, bool SQ>
@@ -480,11 +821,26 @@ int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfl
   if ((rc = make_map(&mql, passes == 3 ? qlo : qhi, m_pad, d_pad, kTcM))) return rc;
   if ((rc = make_map(&mxh, xhi, rows_pad, d_pad, kTcN))) return rc;
   if ((rc = make_map(&mxl, passes == 3 ? xlo : xhi, rows_pad, d_pad, kTcN))) return rc;
+  const bool pair = tc_pair_on(passes, d_pad, m);
   TcWork seed, work;
-  tc_schedule(m, rows_pad, 148, &seed, &work);   // the plan's schedule (planner assumes 148 SMs)
+  tc_schedule(m, rows_pad, 148, pair, &seed, &work);   // the plan's schedule (148 SMs)
   if (2 + 2 * work.slices > lists)
     return fail(TB_ERR_ARG, "tcgen05 engine: candidate buffer smaller than the schedule needs");
   const int nkb = (int)(d_pad / kTcKB);
+  if (pair) {
+    // each CTA of a pair stages 128 of the tile's 256 database rows
+    CUtensorMap mext;
+    if ((rc = make_map(&mxh, xhi, rows_pad, d_pad, kTcM))) return rc;
+    if ((rc = make_map(&mxl, xlo, rows_pad, d_pad, kTcM))) return rc;
+    if ((rc = make_ext_map(&mext, xext, rows_pad / kTcN))) return rc;
+    const int qp = (seed.qtiles + 1) / 2;
+    rc = tc_pair_dispatch(cand, mqh, mql, mxh, mxl, mext, seed, 2 * std::min(qp, sms / 2), m,
+                          nkb, idx_base, cs, ci, gthr, st);
+    if (rc || work.slices == 0) return rc;
+    return tc_pair_dispatch(cand, mqh, mql, mxh, mxl, mext, work,
+                            2 * std::min(qp * work.slices, sms / 2), m, nkb, idx_base, cs, ci,
+                            gthr, st);
+  }
   // every list slot the merge reads must be written: unused ones stay INF
   rc = tc_dispatch(passes, cand, mqh, mql, mxh, mxl, xext, seed, std::min(seed.qtiles, sms),
                    m, nkb, idx_base, cs, ci, gthr, st);

@@ -269,6 +269,18 @@ __device__ __forceinline__ void mma_i8_2sm(uint32_t d_tmem, uint64_t a_desc, uin
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// pair MMA, kind::f16 (bf16 in, fp32 accumulate), leader CTA only
+__device__ __forceinline__ void mma_bf16_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // arrive (once per CTA in cta_mask) on the barrier at this smem offset in
 // each CTA of the pair when the leader's prior tcgen05 ops complete
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t cta_mask) {

@@ -150,6 +150,20 @@ def test_streamed_query_tc_engine_large_d(n, m, d):
     check(dist, idx, rd, ri, xq, qq)
 
 
+@pytest.mark.parametrize("n,m,d", [(70000, 300, 128), (30000, 1000, 64), (9000, 129, 17)])
+def test_cta_pair_tc_kernel(n, m, d, monkeypatch):
+    """The opt-in CTA-pair kernel (TB_TC_PAIR=1: cta_group::2, odd query-tile
+    counts leave the last pair half empty) gives the same exact answers."""
+    monkeypatch.setenv("TB_TC_PAIR", "1")
+    x, q = synthetic.gaussian_knn(n, m, d, seed=n + d)
+    ref_d, ref_i = oknn.exact(x, q, 10)
+    op = neighbors.KnnOperator(n, m, d, 10, engine="tc3")
+    import torch
+    dist, idx = op.run(torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda())
+    check(dist.cpu().numpy(), idx.cpu().numpy(), ref_d, ref_i, x, q)
+    assert op.fallback_count() == 0
+
+
 def test_duplicates_resolve_to_lower_index(engines):
     rng = np.random.default_rng(4)
     base = rng.standard_normal((50, 12)).astype(np.float32)
