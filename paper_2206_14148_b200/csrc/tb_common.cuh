@@ -80,6 +80,25 @@ struct TopList {
       i[0] = j;
     }
   }
+  // Insert (v, j) when j is larger than every index in the list (columns
+  // scanned in ascending order): a score tie then ranks after the entry,
+  // so the lexicographic compare reduces to one strict float compare.
+  __device__ __forceinline__ void insert_after(S v, int j) {
+    bool c[K];
+#pragma unroll
+    for (int p = 0; p < K; ++p) c[p] = v < s[p];
+#pragma unroll
+    for (int p = K - 1; p > 0; --p) {
+      const S ns = c[p - 1] ? s[p - 1] : (c[p] ? v : s[p]);
+      const int ni = c[p - 1] ? i[p - 1] : (c[p] ? j : i[p]);
+      s[p] = ns;
+      i[p] = ni;
+    }
+    if (c[0]) {
+      s[0] = v;
+      i[0] = j;
+    }
+  }
   __device__ __forceinline__ void offer(S v, int j) {
     if (lex_less(v, j, s[K - 1], i[K - 1])) insert(v, j);
   }
@@ -97,7 +116,9 @@ struct TopList {
 
 // Offer the scores sc[j] whose bit is set in `mask` (ascending j, index
 // base + j).  Kept out of line with a dynamic index so that one copy of the
-// insertion network serves all 32 columns (I-cache friendliness).
+// insertion network serves all 32 columns (I-cache friendliness).  Every
+// caller scans columns in ascending index order within a list's lifetime,
+// so base + j exceeds every index already held (TopList::insert_after).
 template <int K>
 __device__ __forceinline__ void insert_masked(TopList<float, K>& L, const float (&sc)[32],
                                            uint32_t mask, int base, float cap = INFINITY) {
@@ -108,7 +129,7 @@ __device__ __forceinline__ void insert_masked(TopList<float, K>& L, const float 
     const int j = __ffs(mask) - 1;
     mask &= mask - 1;
     const float v = tmp[j];
-    if (v < L.worst() && v < cap) L.insert(v, base + j);
+    if (v < L.worst() && v < cap) L.insert_after(v, base + j);
   }
 }
 
