@@ -79,88 +79,177 @@ __global__ void scale_z_kernel(const T* __restrict__ Z, int64_t M, KernParams p,
 // inverse L_kk^-1 into inv (column-major).  The off-diagonal triangular
 // solves become DMMA tile GEMMs with this inverse (the usual GPU TRSM
 // blocking; cond(L_kk) <= sqrt(cond(Kuu)) keeps it accurate).
-// One CTA, 512 threads: 4 threads per row (left-looking factorisation, then
-// the in-place inverse), dot products split 4 ways; two barriers per column.
-constexpr int kPThreads = 4 * kTT;     // 4 threads per row: split dot products
+// One CTA; the lower triangle lives in registers as 4x4 blocks, one block
+// per thread (528 blocks).  Both factorisations are right-looking over
+// 4-wide block columns / rows, three (two) barriers per block:
+//   Cholesky, block column jb:  the owner of (jb, jb) factors it in
+//   registers and publishes it; the owners of (bi, jb) solve their panel
+//   block against it and publish it; every trailing block applies the
+//   rank-4 update (16 shared loads, 64 FMAs from registers).
+//   Inverse (X = L^-1 from L X = I), block row jb:  the owners of (jb, bc)
+//   finalise X_jb,bc = L_jb,jb^-1 R_jb,bc and publish it; every block below
+//   subtracts L_bi,jb X_jb,bc.
+constexpr int kPB = 4;                              // register block edge
+constexpr int kPNB = kTT / kPB;                     // 32 block rows
+constexpr int kPBlocks = kPNB * (kPNB + 1) / 2;     // 528 lower blocks
+constexpr int kPThreads = (kPBlocks + 31) / 32 * 32;
 
 __global__ void __launch_bounds__(kPThreads)
 tail_potrf_inv_kernel(double* __restrict__ base, int k, double* __restrict__ inv,
                       int* __restrict__ info) {
-  extern __shared__ double sA[];          // [kTT][kTLd]
-  __shared__ double dshared;
-  __shared__ double col[kTT];
-  double* t = base + tslot(k, k) * kTE;
-  const int tid = threadIdx.x, i = tid >> 2, sub = tid & 3;
-#pragma unroll 4
-  for (int e = tid; e < kTE; e += kPThreads) {
-    const int c = e / kTT, r = e % kTT;
-    sA[r * kTLd + c] = r >= c ? t[e] : 0.0;
-  }
-  __syncthreads();
-  // left-looking: column j = A[:, j] - L[:, <j] L[j, <j]^T; row i's dot is
-  // split over its 4 threads (q = sub, sub + 4, ...), combined by shuffles
-  for (int j = 0; j < kTT; ++j) {
-    double a = 0.0;
-    if (i >= j) {
-      const double* ri = sA + i * kTLd;
-      const double* rj = sA + j * kTLd;
-      double s0 = 0.0, s1 = 0.0;
-      int q = sub;
-      for (; q + 4 < j; q += 8) {
-        s0 = fma(ri[q], rj[q], s0);
-        s1 = fma(ri[q + 4], rj[q + 4], s1);
-      }
-      if (q < j) s0 = fma(ri[q], rj[q], s0);
-      a = s0 + s1;
-    }
-    a += __shfl_xor_sync(0xffffffffu, a, 1);
-    a += __shfl_xor_sync(0xffffffffu, a, 2);
-    if (i >= j) {
-      a = sA[i * kTLd + j] - a;
-      if (i == j && sub == 0) dshared = a;
-    }
-    __syncthreads();
-    const double djj = dshared;
-    if (!(djj > 0.0)) {                   // uniform: every thread read the same value
-      if (tid == 0) atomicExch(info, k * kTT + j + 1);
-      return;
-    }
-    const double rd = rsqrt(djj);         // one reciprocal root per column
-    if (sub == 0) {
-      if (i > j) sA[i * kTLd + j] = a * rd;
-      if (i == j) sA[j * kTLd + j] = djj * rd;
-    }
-    __syncthreads();
-  }
-#pragma unroll 4
-  for (int e = tid; e < kTE; e += kPThreads) {
-    const int c = e / kTT, r = e % kTT;
-    t[e] = r >= c ? sA[r * kTLd + c] : 0.0;
-  }
-  // L^-1 in place (LAPACK trti2, lower), last column first, trailing block
-  // already inverted:  Inv[j][j] = 1/L[j][j],
-  //   Inv[r][j] = -Inv[j][j] * sum_{j<q<=r} Inv[r][q] L[q][j]
+  extern __shared__ double sL[];                    // [kTT][kTLd] row-major, final L
+  __shared__ __align__(16) double pan[kTT][kPB];    // panel block column / X block row
+  __shared__ double sld[kPB][kPB], srd[kPB];        // factored diagonal block, 1/diag
   __shared__ double rdiag[kTT];
-  if (sub == 0) rdiag[i] = 1.0 / sA[i * kTLd + i];   // all reciprocals at once
-  for (int j = kTT - 1; j >= 0; --j) {
-    if (sub == 0) col[i] = i > j ? sA[i * kTLd + j] : 0.0;      // old L[., j]
-    __syncthreads();
-    const double ijj = rdiag[j];
-    double sum = 0.0;
-    if (i > j) {
-      const double* ri = sA + i * kTLd;
-      for (int q = j + 1 + sub; q <= i; q += 4) sum = fma(ri[q], col[q], sum);
+  __shared__ int sfail;
+  double* t = base + tslot(k, k) * kTE;
+  const int tid = threadIdx.x;
+  const bool own = tid < kPBlocks;
+  int bi = 0, bj = 0;
+  if (own) tri_idx(tid, bi, bj);
+  const int r0 = bi * kPB, c0 = bj * kPB;
+  double a[kPB][kPB];
+#pragma unroll
+  for (int r = 0; r < kPB; ++r)
+#pragma unroll
+    for (int c = 0; c < kPB; ++c)
+      a[r][c] = own && r0 + r >= c0 + c ? t[(int64_t)(c0 + c) * kTT + r0 + r] : 0.0;
+  if (tid == 0) sfail = 0;
+  __syncthreads();
+  for (int jb = 0; jb < kPNB; ++jb) {
+    if (own && bi == jb && bj == jb) {      // diagonal block: factor in registers
+      int bad = 0;
+#pragma unroll
+      for (int q = 0; q < kPB; ++q) {
+        const double d = a[q][q];
+        if (!(d > 0.0) && !bad) bad = q + 1;
+        const double rl = rsqrt(d);
+        a[q][q] = d * rl;
+        srd[q] = rl;
+#pragma unroll
+        for (int r = q + 1; r < kPB; ++r) a[r][q] *= rl;
+#pragma unroll
+        for (int r = q + 1; r < kPB; ++r)
+#pragma unroll
+          for (int c = q + 1; c <= r; ++c) a[r][c] = fma(-a[r][q], a[c][q], a[r][c]);
+      }
+#pragma unroll
+      for (int r = 0; r < kPB; ++r)
+#pragma unroll
+        for (int c = 0; c < kPB; ++c) sld[r][c] = r >= c ? a[r][c] : 0.0;
+      if (bad) {
+        sfail = 1;
+        atomicExch(info, k * kTT + jb * kPB + bad);
+      }
     }
-    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
     __syncthreads();
-    if (sub == 0 && i >= j) sA[i * kTLd + j] = i > j ? -ijj * sum : ijj;
+    if (sfail) return;                      // uniform
+    if (own && bj == jb && bi > jb) {       // panel: A_bi,jb <- A_bi,jb L_jb,jb^-T
+#pragma unroll
+      for (int r = 0; r < kPB; ++r) {
+#pragma unroll
+        for (int q = 0; q < kPB; ++q) {
+          double x = a[r][q];
+#pragma unroll
+          for (int p = 0; p < q; ++p) x = fma(-a[r][p], sld[q][p], x);
+          a[r][q] = x * srd[q];
+        }
+        *reinterpret_cast<double4*>(&pan[r0 + r][0]) = make_double4(a[r][0], a[r][1], a[r][2], a[r][3]);
+      }
+    }
+    __syncthreads();
+    if (own && bj > jb) {                   // trailing rank-4 update
+      double u[kPB][kPB];
+#pragma unroll
+      for (int r = 0; r < kPB; ++r) {
+        const double4 pu = *reinterpret_cast<const double4*>(&pan[r0 + r][0]);
+        u[r][0] = pu.x; u[r][1] = pu.y; u[r][2] = pu.z; u[r][3] = pu.w;
+      }
+#pragma unroll
+      for (int c = 0; c < kPB; ++c) {
+        const double4 pw = *reinterpret_cast<const double4*>(&pan[c0 + c][0]);
+#pragma unroll
+        for (int r = 0; r < kPB; ++r) {
+          if (bi == bj && c > r) continue;
+          double x = a[r][c];
+          x = fma(-u[r][0], pw.x, x);
+          x = fma(-u[r][1], pw.y, x);
+          x = fma(-u[r][2], pw.z, x);
+          a[r][c] = fma(-u[r][3], pw.w, x);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // L out (global, column-major, upper zeroed) and to shared for the inverse
+  if (own) {
+#pragma unroll
+    for (int r = 0; r < kPB; ++r)
+#pragma unroll
+      for (int c = 0; c < kPB; ++c) {
+        const int row = r0 + r, col = c0 + c;
+        const double v = row >= col ? a[r][c] : 0.0;
+        sL[row * kTLd + col] = v;
+        t[(int64_t)col * kTT + row] = v;
+        if (bi != bj) t[(int64_t)row * kTT + col] = 0.0;      // mirrored upper block
+      }
   }
   __syncthreads();
-#pragma unroll 4
-  for (int e = tid; e < kTE; e += kPThreads) {
-    const int c = e / kTT, r = e % kTT;
-    inv[e] = r >= c ? sA[r * kTLd + c] : 0.0;
+  if (tid < kTT) rdiag[tid] = 1.0 / sL[tid * kTLd + tid];
+#pragma unroll
+  for (int r = 0; r < kPB; ++r)
+#pragma unroll
+    for (int c = 0; c < kPB; ++c) a[r][c] = own && r0 + r == c0 + c ? 1.0 : 0.0;
+  __syncthreads();
+  double (*xs)[kTT] = reinterpret_cast<double (*)[kTT]>(&pan[0][0]);   // [4][128]
+  for (int jb = 0; jb < kPNB; ++jb) {
+    if (own && bi == jb) {                  // X_jb,bc = L_jb,jb^-1 R_jb,bc
+#pragma unroll
+      for (int r = 0; r < kPB; ++r) {
+        const double* lr = sL + (r0 + r) * kTLd + r0;
+#pragma unroll
+        for (int c = 0; c < kPB; ++c) {
+          double x = a[r][c];
+#pragma unroll
+          for (int p = 0; p < r; ++p) x = fma(-lr[p], a[p][c], x);
+          a[r][c] = x * rdiag[r0 + r];
+        }
+        *reinterpret_cast<double4*>(&xs[r][c0]) = make_double4(a[r][0], a[r][1], a[r][2], a[r][3]);
+      }
+    }
+    __syncthreads();
+    if (own && bi > jb && bj <= jb) {       // R_bi,bc -= L_bi,jb X_jb,bc
+      double xv[kPB][kPB];
+#pragma unroll
+      for (int p = 0; p < kPB; ++p) {
+        const double4 v = *reinterpret_cast<const double4*>(&xs[p][c0]);
+        xv[p][0] = v.x; xv[p][1] = v.y; xv[p][2] = v.z; xv[p][3] = v.w;
+      }
+#pragma unroll
+      for (int r = 0; r < kPB; ++r) {
+        const double* lr = sL + (r0 + r) * kTLd + jb * kPB;
+        const double l0 = lr[0], l1 = lr[1], l2 = lr[2], l3 = lr[3];
+#pragma unroll
+        for (int c = 0; c < kPB; ++c) {
+          double x = a[r][c];
+          x = fma(-l0, xv[0][c], x);
+          x = fma(-l1, xv[1][c], x);
+          x = fma(-l2, xv[2][c], x);
+          a[r][c] = fma(-l3, xv[3][c], x);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (own) {
+#pragma unroll
+    for (int r = 0; r < kPB; ++r)
+#pragma unroll
+      for (int c = 0; c < kPB; ++c) {
+        const int row = r0 + r, col = c0 + c;
+        inv[(int64_t)col * kTT + row] = row >= col ? a[r][c] : 0.0;
+        if (bi != bj) inv[(int64_t)row * kTT + col] = 0.0;
+      }
   }
 }
 
