@@ -158,13 +158,16 @@ class KnnOperator:
         return dist, idx
 
     def run_host(self, xh, qh, out_host=None, *, index_base: int = 0, stream=None,
-                 staging=None):
+                 staging=None, synchronize: bool = True):
         """Host (CPU) x[n,d], q[m,d] in -> host (dist, idx) out, through
-        tb_knn_run_host: database chunk c+1 is copied to the device while
-        chunk c computes.  ``xh``/``qh`` are torch CPU tensors (pin them for
-        asynchronous copies); ``staging`` = (x_dev, q_dev, dist_dev, idx_dev)
-        device buffers to reuse (allocated on first use otherwise).  Returns
-        host tensors after synchronising the stream."""
+        tb_knn_run_host: the queries, then database chunk c+1, are copied to
+        the device while chunk c computes.  ``xh``/``qh`` are torch CPU
+        tensors (pin them for asynchronous copies); ``staging`` = (x_dev,
+        q_dev, dist_dev, idx_dev) device buffers to reuse (allocated on first
+        use otherwise).  Returns the host tensors; with ``synchronize`` (the
+        default, like the reference's evaluate) the stream is synchronised
+        first so they hold the result, otherwise they are ready once the
+        stream reaches this call's end."""
         torch = _torch()
         p = self.plan
         for name, t, rows in (("x", xh, p.n), ("q", qh, p.m)):
@@ -193,6 +196,8 @@ class KnnOperator:
                                          idd.data_ptr(), self.workspace.data_ptr(),
                                          self.workspace.numel(), st.cuda_stream)
         _lib.check(rc, "knn_host")
+        if synchronize:
+            st.synchronize()
         return dh, ih
 
     def fallback_count(self, stream=None) -> int:
