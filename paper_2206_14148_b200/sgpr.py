@@ -23,7 +23,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .errors import EvaluationError
+from .errors import BudgetExceeded, EvaluationError
 from .mvm import _as_lengthscales
 from .sizes import as_limit
 
@@ -268,9 +268,19 @@ class SGPR:
         fused kernel ``tb_sgpr_kuf_grad``.  Multi-GPU: the chunk sums are
         all-reduced like the statistics.  Returns (elbo, dict of gradients)."""
         torch = _torch()
+        M, dim = int(self.Z.shape[0]), self.dim
+        if self.memory_limit is not None:
+            limit = as_limit(self.memory_limit)
+            resident = (self.X.numel() + self.y.numel() + self.Z.numel()) * self.X.element_size()
+            need = grad_memory_bytes(M, dim, chunk_n) + resident
+            if need > limit:
+                raise BudgetExceeded(
+                    "sgpr_elbo_and_grads", need, resident,
+                    message=f"sgpr_elbo_and_grads: the dense fp64 autograd tail needs "
+                            f"~{need / 1e9:.2f} GB at M={M} (N-independent), over "
+                            f"memory_limit={limit}; the ELBO alone (elbo()) stays in budget")
         s = self._stats if self._stats is not None and self._stats.Sigma is not None \
             else self.statistics()
-        M, dim = int(s.v.numel()), self.dim
         f64 = torch.float64
         dev = self.device
         Zd = self.Z.to(f64).detach().requires_grad_()
@@ -324,6 +334,19 @@ class SGPR:
         Xt = _dev_tensor(Xnew, self.device).to(self.Z.dtype)
         mu = kernel_mvm(Xt, self.Z, self._w, self.kernel, self.variance, self.lengthscales)
         return mu.cpu().numpy() if host else mu
+
+
+def grad_memory_bytes(M: int, dim: int, chunk_n: int = 4096) -> int:
+    """Device bytes SGPR.elbo_and_grads needs beyond its inputs (planner-style
+    estimate, checked against torch's peak by tests/test_sgpr_gpu.py).  The
+    O(M^3) tail is differentiated densely (torch autograd through
+    cholesky / triangular solves): ~16 live M x M fp64 matrices at its peak.
+    The N-streaming pass then holds G (twice) plus three M x chunk_n fp64
+    panels (K, G K, W) and the reduction partials.  Independent of N."""
+    mm = 8 * M * M
+    tail = 16 * mm
+    stream = 2 * mm + 3 * 8 * M * chunk_n + 8 * (-(-chunk_n // 128)) * (M * dim + (1 + dim) * (-(-M // 32)))
+    return int(max(tail, stream)) + (1 << 20)
 
 
 def _torch_kernel(A, B, kind, variance, ls):

@@ -154,6 +154,30 @@ def test_elbo_gradient_matches_finite_differences(kind, engine, dtype):
         assert np.max(np.abs(got - want)) <= tol * max(np.max(np.abs(want)), 1.0), (key, got, want)
 
 
+def test_gradient_memory_estimate_and_budget():
+    """elbo_and_grads is N-independent in memory but its dense autograd tail
+    is O(M^2): grad_memory_bytes must bound torch's measured peak (and not by
+    much), and a memory_limit below it raises BudgetExceeded before work."""
+    import torch
+    from paper_2206_14148_b200.sgpr import grad_memory_bytes
+    N, d, M, chunk = 30000, 4, 1536, 2048
+    X, y, Z, _ = synthetic.sgpr_data(N, d, M, seed=5, dtype=np.float32)
+    m = tb.SGPR(X, y, Z, "rbf", 1.0, 0.7, 0.05)
+    m.statistics()
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    m.elbo_and_grads(chunk_n=chunk)
+    torch.cuda.synchronize()
+    peak = torch.cuda.max_memory_allocated() - base
+    est = grad_memory_bytes(M, d, chunk)
+    assert peak <= est <= 2.0 * peak, (peak, est)
+    resident = (X.size + y.size + Z.size) * 4
+    small = tb.SGPR(X, y, Z, "rbf", 1.0, 0.7, 0.05, memory_limit=resident + est // 2)
+    with pytest.raises(tb.BudgetExceeded):
+        small.elbo_and_grads(chunk_n=chunk)
+
+
 @pytest.mark.parametrize("kind", ["rbf", "matern32"])
 def test_packed_tail_matches_dense_tail(kind):
     """The in-place packed-tile tail (Kuu = LL^T, Kuu + Sigma/s2 = PP^T,
