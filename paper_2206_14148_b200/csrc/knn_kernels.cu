@@ -386,9 +386,54 @@ __global__ void knn_merge_kernel(const float* __restrict__ in_s,
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= m) return;
+  const int total = lists + (prev_s ? 1 : 0);
+  float* os = out_s + r * KC;
+  int* oi = out_i + r * KC;
+  if (KC <= 32 && total <= 32) {
+    // one sorted list per lane, held in registers: KC rounds of a warp-wide
+    // lexicographic argmin over the list heads; the winning lane pops
+    float v[KC];
+    int j[KC];
+    if (lane < total) {
+      const float* s = lane < lists ? in_s + ((int64_t)lane * m + r) * KC : prev_s + r * KC;
+      const int* ix = lane < lists ? in_i + ((int64_t)lane * m + r) * KC : prev_i + r * KC;
+#pragma unroll
+      for (int u = 0; u < KC / 4; ++u) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(s) + u);
+        const int4 b = __ldg(reinterpret_cast<const int4*>(ix) + u);
+        v[4 * u] = a.x; v[4 * u + 1] = a.y; v[4 * u + 2] = a.z; v[4 * u + 3] = a.w;
+        j[4 * u] = b.x; j[4 * u + 1] = b.y; j[4 * u + 2] = b.z; j[4 * u + 3] = b.w;
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < KC; ++p) {
+        v[p] = INFINITY;
+        j[p] = kInvalidIdx;
+      }
+    }
+#pragma unroll 1
+    for (int t = 0; t < KC; ++t) {
+      float bv = v[0];
+      int bj = j[0];
+      warp_lex_min(bv, bj);
+      if (bj != kInvalidIdx && j[0] == bj && v[0] == bv) {   // indices are unique
+#pragma unroll
+        for (int p = 0; p < KC - 1; ++p) {
+          v[p] = v[p + 1];
+          j[p] = j[p + 1];
+        }
+        v[KC - 1] = INFINITY;
+        j[KC - 1] = kInvalidIdx;
+      }
+      if (lane == 0) {
+        os[t] = bv;
+        oi[t] = bj;
+      }
+    }
+    return;
+  }
   TopList<float, KC> L;
   L.init();
-  const int total = lists + (prev_s ? 1 : 0);
   for (int l = lane; l < total; l += 32) {
     const float* s = l < lists ? in_s + ((int64_t)l * m + r) * KC : prev_s + r * KC;
     const int* ix = l < lists ? in_i + ((int64_t)l * m + r) * KC : prev_i + r * KC;
@@ -399,8 +444,6 @@ __global__ void knn_merge_kernel(const float* __restrict__ in_s,
       L.insert(v, j);
     }
   }
-  float* os = out_s + r * KC;
-  int* oi = out_i + r * KC;
   warp_drain(L, KC, [&](int t, float v, int j) {
     os[t] = v;
     oi[t] = j;
