@@ -107,13 +107,25 @@ rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
     }
     __align__(16) __nv_bfloat16 h[8];
     __align__(16) __nv_bfloat16 l[8];
+    if (sizeof(T) == 4 && !NORM && scale == 1.0) {
+      // f32 rows: x - bf16(x) is exact in f32, so the split needs no fp64
+      // (same bits as the fp64 path); only the norm accumulates in fp64
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const double u = NORM ? v[j] * inv : v[j];
-      acc = fma(u, u, acc);
-      const double sv = scale * u;             // scale: exact power of two
-      h[j] = __double2bfloat16(sv);
-      l[j] = __double2bfloat16(sv - (double)__bfloat162float(h[j]));
+      for (int j = 0; j < 8; ++j) {
+        const float f = (float)v[j];
+        acc = fma(v[j], v[j], acc);
+        h[j] = __float2bfloat16_rn(f);
+        l[j] = __float2bfloat16_rn(f - __bfloat162float(h[j]));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double u = NORM ? v[j] * inv : v[j];
+        acc = fma(u, u, acc);
+        const double sv = scale * u;             // scale: exact power of two
+        h[j] = __double2bfloat16(sv);
+        l[j] = __double2bfloat16(sv - (double)__bfloat162float(h[j]));
+      }
     }
     *reinterpret_cast<uint4*>(hi + r * d_pad + c0) = *reinterpret_cast<const uint4*>(h);
     *reinterpret_cast<uint4*>(lo + r * d_pad + c0) = *reinterpret_cast<const uint4*>(l);
