@@ -378,13 +378,16 @@ def run_ours(args):
     # end to end through the public operator: pinned host inputs copied in,
     # results copied out, every step
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
         # the reference-facing call with HOST buffers (tb_knn_run_host): pinned
         # x, q copied in (queries first, then the database chunk by chunk on
         # one copy stream, overlapped with compute) and dist, idx copied out,
         # every step.  Its plan caps chunks at n/16 so fifteen of the sixteen
         # database copies overlap compute (tools/e2e_chunks.py: 4/8/12/16/24
         # chunks -> 0.89/0.97/0.99/1.00/0.85 M q/s; the bound is PCIe).
+        # N > 1: every rank copies its shard in, the per-shard lists meet on
+        # the device (NCCL all_gather + merge) and the global result is copied
+        # out on every rank (distributed.knn_sharded_host).
         xh = x.cpu().pin_memory()
         qh = q.cpu().pin_memory()
         op_h = neighbors.KnnOperator(rows, M_Q, DIM, K, dtype=np.float32, out_dtype=out_dtype,
@@ -394,11 +397,18 @@ def run_ours(args):
         dh = torch.empty(out[0].shape, dtype=out[0].dtype).pin_memory()
         ih = torch.empty(out[1].shape, dtype=out[1].dtype).pin_memory()
 
-        def e2e_step():
-            op_h.run_host(xh, qh, (dh, ih), staging=staging)
+        if use_dist:
+            def e2e_step():
+                distributed.knn_sharded_host(xh, qh, K, index_base=start, operator=op_h,
+                                             staging=staging, out_host=(dh, ih))
+        else:
+            def e2e_step():
+                op_h.run_host(xh, qh, (dh, ih), staging=staging)
 
         for _ in range(max(1, args.warmup)):
             e2e_step()
+        if use_dist:
+            dist.barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -410,7 +420,12 @@ def run_ours(args):
         e1.record()
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
-        if os.environ.get("TB_BENCH_TRACE"):      # diagnosis: CUPTI timeline of 2 steps
+        if use_dist:
+            dist.barrier()
+            tt = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        if os.environ.get("TB_BENCH_TRACE") and not use_dist:   # diagnosis: CUPTI timeline
             from torch.profiler import profile, ProfilerActivity
             with profile(activities=[ProfilerActivity.CUDA]) as prof:
                 for _ in range(2):
@@ -422,7 +437,7 @@ def run_ours(args):
                 for a, b, nm in tl:
                     f.write(f"{(a - tl[0][0]) / 1000:9.3f} {(b - a) / 1000:8.3f}  {nm}\n")
         # the bound of this path: one pinned host->device copy of the same
-        # bytes, alone (PCIe), timed the same way
+        # bytes, alone (PCIe), timed the same way (this rank's bytes)
         hb = int(x.numel() * 4 + q.numel() * 4)
         e0.record()
         for _ in range(3):
@@ -431,15 +446,23 @@ def run_ours(args):
         e1.record()
         torch.cuda.synchronize()
         h2d_ms = e0.elapsed_time(e1) / 3
+        hb_job, ob_job = hb, int(dh.numel() * dh.element_size() + ih.numel() * 8)
+        if use_dist:
+            tb_ = torch.tensor([hb_job, ob_job], device=dev, dtype=torch.float64)
+            dist.all_reduce(tb_)
+            hb_job, ob_job = (int(v) for v in tb_.tolist())
         e2e = {"value": M_Q * args.steps / (ems / 1000.0), "unit": UNIT,
                "h2d_only_ms": h2d_ms, "h2d_gbs": hb / h2d_ms / 1e6, "host_enqueue_ms": host_ms,
                "frac_of_h2d_bound": h2d_ms / (ems / args.steps),
-               "h2d_bytes_per_step": int(x.numel() * 4 + q.numel() * 4),
-               "d2h_bytes_per_step": int(dh.numel() * dh.element_size() + ih.numel() * 8),
+               "h2d_bytes_per_step": hb_job,
+               "d2h_bytes_per_step": ob_job,
                "ms_per_step": ems / args.steps,
                "chunks": int(op_h.plan.n_chunks),
-               "path": "KnnOperator.run_host -> tb_knn_run_host: pinned host x,q in "
-                       "(per-chunk H2D overlapped with compute), dist,idx out"}
+               "path": ("distributed.knn_sharded_host: per rank KnnOperator.run_host -> "
+                        "tb_knn_run_host (pinned shard + queries in), NCCL all_gather + "
+                        "tb_topk_merge, global dist,idx out" if use_dist else
+                        "KnnOperator.run_host -> tb_knn_run_host: pinned host x,q in "
+                        "(per-chunk H2D overlapped with compute), dist,idx out")}
         del op_h
 
     peaks, peak_src = _peaks()

@@ -92,6 +92,40 @@ def knn_sharded(x_shard, q, k: int, *, index_base: int, group=None, operator=Non
     return od, oi
 
 
+def knn_sharded_host(xh_shard, qh, k: int, *, index_base: int, operator, group=None,
+                     staging=None, out_host=None):
+    """knn_sharded from HOST buffers: this rank's database shard and the
+    queries are copied in through ``operator.run_host`` (tb_knn_run_host,
+    chunk copies overlapped with compute), the per-shard lists are exchanged
+    on the device (all_gather + tb_topk_merge) and the global (dist, idx)
+    is copied back into pinned host tensors.  ``operator`` must be planned
+    for this shard with fp64 output (exact ties across shards)."""
+    torch = _torch()
+    if staging is None:
+        p = operator.plan
+        td = torch.float32 if operator.dtype == np.float32 else torch.float64
+        staging = (torch.empty((int(p.n), int(p.d)), dtype=td, device=operator.device),
+                   torch.empty((int(p.m), int(p.d)), dtype=td, device=operator.device),
+                   *operator.alloc_outputs())
+    dd, idd = staging[2], staging[3]
+    dh_local = torch.empty(tuple(dd.shape), dtype=dd.dtype).pin_memory()
+    ih_local = torch.empty(tuple(idd.shape), dtype=torch.int64).pin_memory()
+
+    def local(_x, _q, _k, base):
+        operator.run_host(xh_shard, qh, (dh_local, ih_local), index_base=base,
+                          staging=staging, synchronize=False)
+        return dd, idd
+
+    od, oi = knn_sharded(None, None, k, index_base=index_base, group=group, local_fn=local)
+    if out_host is None:
+        out_host = (torch.empty(tuple(od.shape), dtype=od.dtype).pin_memory(),
+                    torch.empty(tuple(oi.shape), dtype=torch.int64).pin_memory())
+    out_host[0].copy_(od, non_blocking=True)
+    out_host[1].copy_(oi, non_blocking=True)
+    torch.cuda.current_stream(od.device).synchronize()
+    return out_host
+
+
 def _np_dtype(t):
     torch = _torch()
     return np.float32 if t.dtype == torch.float32 else np.float64

@@ -394,5 +394,13 @@ def test_nccl_process_group_world1():
         d, i = distributed.knn_sharded(xt, qt, 5, index_base=0, group=dist.group.WORLD)
         ref_d, ref_i = oknn.exact(x, q, 5)
         check(d.cpu().numpy(), i.cpu().numpy(), ref_d, ref_i, x, q)
+        # host buffers in and out (bench e2e at N > 1): shard 1 of 2, offset
+        xs = torch.from_numpy(x[4000:]).pin_memory()
+        op = neighbors.KnnOperator(5000, 64, 16, 5, out_dtype=np.float64, max_chunk_rows=1200)
+        dh, ih = distributed.knn_sharded_host(xs, torch.from_numpy(q).pin_memory(), 5,
+                                              index_base=4000, operator=op,
+                                              group=dist.group.WORLD)
+        sd, si = oknn.exact(x[4000:], q, 5)
+        check(dh.numpy(), ih.numpy() - 4000, sd, si, x[4000:], q)
     finally:
         dist.destroy_process_group()
