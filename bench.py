@@ -475,7 +475,7 @@ def run_ours(args):
         # burst figure: one step is a few ms and the SM clock stays at its
         # maximum (no power-cap reason in `clocks`), i.e. a kernel timed alone
         peak = peaks["bf16_tflops"] / passes
-        traffic, alg_bytes, rep = _traffic("knn_tc") if engine == "tc3" else (None, None, None)
+        traffic, alg_bytes, rep = _traffic({"tc3": "knn_tc", "tc1": "knn_tc1"}.get(engine, ""))
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "traffic_note": None if traffic is None else

@@ -60,7 +60,7 @@ extern "C" {
 #define TB_ENGINE_AUTO 0
 #define TB_ENGINE_TC3 1   /* tcgen05 bf16x3 split cross term (fp32-class)   */
 #define TB_ENGINE_SIMT 2  /* CUDA-core fp32 cross term                      */
-#define TB_ENGINE_TC1 3   /* tcgen05 single-pass bf16 + certified re-rank   */
+#define TB_ENGINE_TC1 3   /* tcgen05 single-pass fp16 (power-of-two scaled), bound from the measured rounding residuals, certified re-rank (AUTO) */
 
 /* SGPR kernels */
 #define TB_KERNEL_RBF 0

@@ -26,8 +26,9 @@ int fail(int code, const std::string& msg) {
 // a CPU-only host for tests and dry planning); the run checks the device.
 constexpr int kPlanSms = 148;
 constexpr int64_t kAlign = 256;
-// engine chosen for TB_ENGINE_AUTO
-constexpr int kAutoEngine = TB_ENGINE_TC3;
+// engine chosen for TB_ENGINE_AUTO: the fp16 single pass with the measured-
+// residual bound (tc1) certifies C2/C3 with no fallback at 1/3 of tc3's MMAs
+constexpr int kAutoEngine = TB_ENGINE_TC1;
 
 static int64_t elem_size(int dtype) { return dtype == TB_F32 ? 4 : 8; }
 
@@ -139,8 +140,7 @@ int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int32_t me
 
   // candidates kept beyond k: the single-pass engine and long (d > 128)
   // contractions have wider certified error bounds, so they keep more
-  const int64_t margin =
-      engine == TB_ENGINE_TC1 ? std::max<int64_t>(22, k) : (round_up(d, 64) > 128 ? 22 : 6);
+  const int64_t margin = round_up(d, 64) > 128 && engine != TB_ENGINE_SIMT ? 22 : 6;
   const int64_t want = k + margin;
   int cand = want <= 16 ? 16 : want <= 32 ? 32 : want <= 64 ? 64 : 0;
   if (!cand) {
@@ -182,11 +182,14 @@ int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int32_t me
     plan->off[kRunI] = c.take(2 * m * cand * 4);
     plan->off[kGThr] = c.take(m * 4);
     if (tc) {
+      // tc1 (fp16 single pass) stages one plane per operand
+      const int64_t lo = engine == TB_ENGINE_TC1 ? 0 : 1;
       plan->off[kQHi] = c.take(plan->m_pad * plan->d_pad * 2);
-      plan->off[kQLo] = c.take(plan->m_pad * plan->d_pad * 2);
+      plan->off[kQLo] = c.take(lo * plan->m_pad * plan->d_pad * 2);
       plan->off[kXHi] = c.take(chunk_pad * plan->d_pad * 2);
-      plan->off[kXLo] = c.take(chunk_pad * plan->d_pad * 2);
+      plan->off[kXLo] = c.take(lo * chunk_pad * plan->d_pad * 2);
       plan->off[kXExt] = c.take(chunk_pad * 32);
+      plan->off[kQln] = c.take(m * 4);
     }
     return c.used;
   };
@@ -336,8 +339,13 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
 
   TB_CUDA_TRY(cudaMemsetAsync(stats, 0, 256, st));
   if (tc) TB_CUDA_TRY(cudaMemsetAsync(gthr, 0xFF, p->m * 4, st));
-  int rc = launch_query_prep(p->dtype, p->metric, q, p->m, p->d, qn64, qnorm, qhi, qlo,
-                             p->m_pad, p->d_pad, st);
+  const bool f16 = p->engine == TB_ENGINE_TC1;
+  float* qln = f16 ? (float*)at(kQln) : nullptr;
+  const float* f16p = f16 ? reinterpret_cast<const float*>(stats + kF16Slot) : nullptr;
+  int rc = f16 ? launch_query_prep_f16(p->dtype, p->metric, q, p->m, p->d, qn64, qnorm, qln,
+                                       stats, (__half*)qhi, p->m_pad, p->d_pad, st)
+               : launch_query_prep(p->dtype, p->metric, q, p->m, p->d, qn64, qnorm, qhi, qlo,
+                                   p->m_pad, p->d_pad, st);
   if (rc) return rc;
 
   const float* prev_s = nullptr;
@@ -349,8 +357,10 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
     const int64_t rows_pad = round_up(rows, tile_rows);
     const char* xc = (const char*)x + c0 * p->d * es;
     if (ready && c < n_ready) TB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)ready[c], 0));
-    rc = launch_db_prep(p->dtype, p->metric, xc, rows, p->d, xn, stats, xhi, xlo,
-                        rows_pad, p->d_pad, xext, st);
+    rc = f16 ? launch_db_prep_f16(p->dtype, p->metric, xc, rows, p->d, xn, stats,
+                                  (__half*)xhi, rows_pad, p->d_pad, xext, st)
+             : launch_db_prep(p->dtype, p->metric, xc, rows, p->d, xn, stats, xhi, xlo,
+                              rows_pad, p->d_pad, xext, st);
     if (rc) return rc;
     const int slices = (int)std::min<int64_t>(p->slices, ceil_div(rows, tile_rows));
     int lists = tc ? tc_lists(p->m, rows_pad, kPlanSms, p->engine == TB_ENGINE_TC1 ? 1 : 3, p->d_pad)
@@ -360,7 +370,7 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
     if (tc) {
       rc = launch_knn_tc(p->engine == TB_ENGINE_TC1 ? 1 : 3, p->cand, xhi, xlo,
                          qhi, qlo, xext, rows, rows_pad, p->m, p->m_pad, p->d_pad,
-                         lists, (int)c0, cs, ci, gthr, st);
+                         lists, (int)c0, cs, ci, gthr, f16p, st);
     } else {
       rc = launch_knn_simt(p->dtype, p->metric, p->cand, xc, q, xn, rows, p->m, p->d,
                            slices, (int)c0, cs, ci, st);
@@ -382,10 +392,14 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
     dot_rel = (double)(p->d + 4) * u24 * (p->dtype == TB_F64 ? 2.0 : 1.0) + 2 * u24;
   else if (p->engine == TB_ENGINE_TC3)
     dot_rel = 4.0 * std::ldexp(1.0, -16) + (double)(3 * p->d_pad + 16) * 2 * u24;
-  else
-    dot_rel = 2.0 * std::ldexp(1.0, -8) + std::ldexp(1.0, -15) + (double)(p->d_pad + 16) * 2 * u24;
+  else  // tc1: fp32 accumulation only; the fp16 rounding enters through the
+        // measured residual norms (refine kernel, qln + stats[2])
+    dot_rel = (double)(p->d_pad + 32) * u24;
   double c1 = 2.0 * 2.0 * dot_rel;   // 2x safety, 2 for the -2 q.x
   double c2 = 2.0 * 4.0 * u24;        // ||x||^2 rounding + final FMA
+  // tc1: ||x||^2 enters the fp32 sum too, and its fp16 split comes from the
+  // fp32 norms (relative error <= (d + 2) 2^-24)
+  if (f16) c2 += 2.0 * dot_rel + std::ldexp(1.0, -26) + 2.0 * (double)(p->d + 2) * u24;
   if (p->metric == TB_METRIC_L1) {
     // fp32 sum of d non-negative |q-x| terms: relative (d+2)u, plus the
     // rounding of f64 inputs to fp32, u (|q|_1 + |x|_1); 2x safety
@@ -396,7 +410,7 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
   if (const char* f = std::getenv("TB_FORCE_FALLBACK"))
     if (f[0] == '1') c1 = c2 = 1e300;
   rc = launch_knn_refine(p->dtype, p->out_dtype, p->metric, p->cand, prev_s, prev_i, x, q,
-                         qn64, qnorm, stats, p->n, p->m, p->d, p->k, c1, c2,
+                         qn64, qnorm, qln, stats, p->n, p->m, p->d, p->k, c1, c2,
                          out_dist, out_idx, index_base, fb, st);
   if (rc) return rc;
   // the per-chunk candidate lists (kCandS, kCandI) are dead after the last

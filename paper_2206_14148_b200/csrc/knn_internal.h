@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 namespace tb {
@@ -23,8 +24,14 @@ enum KnnSlot {
   kXLo = 12,
   kGThr = 13,   // u32[m]           per-query shared K'-th score bound (ordered key)
   kXExt = 14,   // bf16[chunk_pad][16] augmented-K rows -(h,m,l) of ||x||^2 (core matrices)
-  kNumSlots = 15
+  kQln = 15,    // float[m]         ||q - fp16 q|| (engine tc1's certified bound)
+  kNumSlots = 16
 };
+// stats (u32[64]): [0] max ||x|| bits, [1] fallback count, [2] max ||x - fp16 x||
+// bits, [3] max |q| bits, [4] max |x| bits of the current chunk, [5] the
+// chunk's max ||x - fp16 x||, [kF16Slot..+3] fp16 engine scales (floats:
+// s, t, alpha, 1/(s t)), [12] redo flag of the chunk conversion
+constexpr int kF16Slot = 8;
 
 struct KnnDims {
   int64_t n, m, d, k;
@@ -41,6 +48,12 @@ int launch_db_prep(int dtype, int metric, const void* x, int64_t rows, int64_t d
                    float* xn, unsigned* xmax_bits, __nv_bfloat16* xhi,
                    __nv_bfloat16* xlo, int64_t rows_pad, int64_t d_pad,
                    uint8_t* xext, cudaStream_t st);
+int launch_query_prep_f16(int dtype, int metric, const void* q, int64_t m, int64_t d,
+                          double* qn64, float* qnorm, float* qln, unsigned* stats,
+                          __half* qhi, int64_t m_pad, int64_t d_pad, cudaStream_t st);
+int launch_db_prep_f16(int dtype, int metric, const void* x, int64_t rows, int64_t d,
+                       float* xn, unsigned* stats, __half* xhi, int64_t rows_pad,
+                       int64_t d_pad, uint8_t* xext, cudaStream_t st);
 // SIMT candidate engine: writes lists [2*slices][m][cand]
 int launch_knn_simt(int dtype, int metric, int cand, const void* x_chunk, const void* q,
                     const float* xn, int64_t rows, int64_t m, int64_t d,
@@ -53,7 +66,7 @@ int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi,
                   const __nv_bfloat16* qlo, const uint8_t* xext, int64_t rows,
                   int64_t rows_pad, int64_t m, int64_t m_pad, int64_t d_pad,
                   int lists, int idx_base, float* cand_s, int* cand_i,
-                  unsigned* gthr, cudaStream_t st);
+                  unsigned* gthr, const float* f16p, cudaStream_t st);
 int tc_lists(int64_t m, int64_t rows_pad, int sms, int passes, int64_t d_pad);
 int tc_max_dpad();
 // merge L lists (+ optional previous running list) into out
@@ -63,7 +76,7 @@ int launch_knn_merge(int cand, const float* in_s, const int* in_i, int lists,
 // exact fp64 re-rank + certification
 int launch_knn_refine(int dtype, int out_dtype, int metric, int cand, const float* cs,
                       const int* ci, const void* x, const void* q,
-                      const double* qn64, const float* qnorm,
+                      const double* qn64, const float* qnorm, const float* qln,
                       const unsigned* stats, int64_t n, int64_t m, int64_t d,
                       int64_t k, double c1, double c2, void* out_dist,
                       int64_t* out_idx, int64_t index_base, int* fb_list,

@@ -211,6 +211,321 @@ static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
   return TB_OK;
 }
 
+// ------------------------------------------ fp16 single-pass operand prep --
+// Engine tc1: one fp16 x fp16 -> fp32 MMA pass with a TIGHT certified bound.
+// Operands are scaled by powers of two (exact) into fp16 range: A = fp16(2 s q),
+// B = fp16(t x), A_ext = alpha, B_ext = -(h, m, l) with h + m + l =
+// s t ||x||^2 / alpha, so the accumulator is s t (2 q.x - ||x||^2) and the
+// engine unscales by 1 / (s t).  The rounding residuals are measured exactly
+// (fp64): ||ql|| per query, max ||xl|| per database (stats), and the refine
+// step's bound uses them (Cauchy-Schwarz) instead of a worst-case relative
+// error: |q.x - q'.x'| <= ||q|| XL + ||ql|| (X + 3 XL).
+// Scale slots (floats, stats + kF16Slot): [0] s, [1] t, [2] alpha, [3] 1/(s t).
+
+__global__ void absmax_f32_kernel(const float* __restrict__ src, int64_t n,
+                                  unsigned* __restrict__ bits) {
+  float mx = 0.f;
+  const int64_t n4 = n / 4;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(src) + e);
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  for (int64_t e = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    mx = fmaxf(mx, fabsf(src[e]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(bits, __float_as_uint(mx));
+}
+
+__global__ void absmax_f64_kernel(const double* __restrict__ src, int64_t n,
+                                  unsigned* __restrict__ bits) {
+  float mx = 0.f;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    mx = fmaxf(mx, __double2float_ru(fabs(src[e])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(bits, __float_as_uint(mx));
+}
+
+__device__ __forceinline__ float pow2_floor(float v) {      // largest 2^e <= v
+  return exp2f(floorf(log2f(v)));
+}
+
+// which = 0: queries (s from max|q| in stats[3]).  which = 1: database chunk,
+// after the provisional pass (t = 1) recorded max|x| in stats[4]: t = 1 is
+// kept when max|x| is in [2^-3, 2^14] (no overflow, normal fp16 values for all
+// but tiny elements) and s d max|x|^2 <= 2^29 (the ||x||^2 block fits fp16
+// with alpha <= 2^15); otherwise t is recomputed and stats[12] asks the second
+// pass to redo the conversion.
+__global__ void f16_scales_kernel(unsigned* __restrict__ stats, int64_t d, int which,
+                                  int metric) {
+  float* sc = reinterpret_cast<float*>(stats + kF16Slot);
+  if (which == 0) {
+    const float qm = metric == TB_METRIC_COSINE ? 1.f : __uint_as_float(stats[3]);
+    // |2 s q| <= 256; s, t in [2^-60, 2^60] keep 1/(s t) a normal float
+    sc[0] = qm > 0.f ? fminf(fmaxf(pow2_floor(128.f / qm), 0x1p-60f), 0x1p60f) : 1.f;
+    return;
+  }
+  const float xm = metric == TB_METRIC_COSINE ? 1.f : __uint_as_float(stats[4]);
+  const double s = sc[0];
+  const double cap = 536870912.0;                            // 2^29
+  float t = 1.f;
+  unsigned redo = 0;
+  if (!(xm >= 0.125f && xm <= 16384.f && s * (double)d * (double)xm * (double)xm <= cap)) {
+    t = xm > 0.f ? fminf(fmaxf(pow2_floor(256.f / xm), 0x1p-60f), 0x1p60f) : 1.f;
+    const double V = s * (double)t * (double)d * (double)xm * (double)xm;
+    if (V > cap) t = (float)((double)t / exp2(ceil(log2(V / cap))));
+    redo = t != 1.f;
+  }
+  const double V = s * (double)t * (double)d * (double)xm * (double)xm;
+  double a = exp2(ceil(log2(fmax(V, 1e-30) / 16384.0)));
+  a = fmin(fmax(a, 1.0 / 16384.0), 32768.0);
+  sc[1] = t;
+  sc[2] = (float)a;
+  sc[3] = (float)(1.0 / (s * (double)t));
+  stats[12] = redo;
+  if (redo) stats[5] = 0u;                 // the chunk's residual max is redone
+}
+
+// MODE 0: queries, A = fp16(2 s q), ||ql|| per row (rounded up).
+// MODE 1: database, provisional t = 1; records max |x| (stats[4]).
+// MODE 2: database, t = sc[1]; only when stats[12] asks for it.
+// Database modes: fp32 ||x||^2 (xn), max ||x|| (stats[0]), chunk max ||xl||
+// (stats[5]).  f32 rows without normalisation take an exact fp32 path: t is
+// a power of two, so x t and fp16(x t) / t are exact and x - fp16(x t) / t
+// is exact (Sterbenz); the residual norm is summed in fp32 and rounded up by
+// (1 + (d + 2) 2^-23) so it stays an upper bound.
+template <typename T, int G, bool NORM, int MODE>
+__global__ void __launch_bounds__(256)
+rows_f16_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
+                double* __restrict__ n64, float* __restrict__ n32, float* __restrict__ norm32,
+                float* __restrict__ resid, unsigned* __restrict__ stats,
+                __half* __restrict__ hi, int64_t rows_pad, int64_t d_pad) {
+  __shared__ float wmax[8], wres[8], wabs[8];
+  const float* sc = reinterpret_cast<const float*>(stats + kF16Slot);
+  if (MODE == 2 && *reinterpret_cast<volatile unsigned*>(stats + 12) == 0u) return;
+  const float mulf = MODE == 0 ? 2.f * sc[0] : MODE == 1 ? 1.f : sc[1];
+  const double mul = mulf, imul = 1.0 / (double)mulf;       // powers of two: exact
+  const float imulf = 1.f / mulf;
+  constexpr bool FAST = sizeof(T) == 4 && !NORM;
+  // grid-stride over rows (the stride keeps a row's G lanes in one warp)
+  float nrm = 0.f, res = 0.f, amax = 0.f;
+  const int64_t total = rows_pad * G;
+  for (int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+       gt - threadIdx.x < total; gt += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t r = gt < total ? gt / G : rows_pad;
+  const int seg = (int)(gt % G);
+  double inv = 1.0;
+  if (NORM) {
+    double nn = 0.0;
+    for (int64_t c = (int64_t)seg; r < rows && c < d; c += G) {
+      const double v = (double)src[r * d + c];
+      nn = fma(v, v, nn);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+    inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+  }
+  double acc = 0.0, rn = 0.0;
+  float rnf = 0.f, accf = 0.f;
+  for (int64_t c0 = (int64_t)seg * 8; r < rows_pad && c0 < d_pad; c0 += 8 * G) {
+    double v[8];
+    float f[8];
+    if (r < rows && c0 + 8 <= d && sizeof(T) == 4 && (d & 3) == 0) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(src + r * d + c0));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(src + r * d + c0 + 4));
+      f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+      f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = f[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[j] = (r < rows && c0 + j < d) ? (double)src[r * d + c0 + j] : 0.0;
+        f[j] = (float)v[j];
+      }
+    }
+    __align__(16) __half h[8];
+    if (FAST) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (MODE == 0) acc = fma(v[j], v[j], acc);       // ||q||^2 exact for the re-rank
+        else accf = fmaf(f[j], f[j], accf);               // ||x||^2: fp32, bounded below
+        amax = fmaxf(amax, fabsf(f[j]));
+        h[j] = __float2half_rn(f[j] * mulf);
+        const float e = f[j] - __half2float(h[j]) * imulf;
+        rnf = fmaf(e, e, rnf);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double u = NORM ? v[j] * inv : v[j];
+        acc = fma(u, u, acc);
+        amax = fmaxf(amax, __double2float_ru(fabs(u)));
+        h[j] = __double2half(mul * u);
+        const double e = u - (double)__half2float(h[j]) * imul;
+        rn = fma(e, e, rn);
+      }
+    }
+    *reinterpret_cast<uint4*>(hi + r * d_pad + c0) = *reinterpret_cast<const uint4*>(h);
+  }
+  // fp32 sums of d non-negative terms: relative error <= (d + 2) 2^-24
+  const double up = 1.0 + (double)(d + 2) * 0x1p-23;
+  if (FAST) rn = (double)rnf * up;
+  if (FAST && MODE != 0) acc = (double)accf;
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    rn += __shfl_xor_sync(0xffffffffu, rn, o);
+  }
+  if (seg == 0 && r < rows) {
+    if (n64) n64[r] = acc;
+    if (n32) n32[r] = (float)acc;
+    const float nr = (float)(sqrt(acc) * (FAST && MODE != 0 ? up : 1.0)) * (1.0f + 1e-6f);
+    nrm = fmaxf(nrm, nr);
+    if (norm32) norm32[r] = nr;
+    const float rs = __double2float_ru(sqrt(rn) * (1.0 + 1e-12));
+    res = fmaxf(res, rs);
+    if (MODE == 0 && resid) resid[r] = rs;
+  }
+  }
+  if (MODE != 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      nrm = fmaxf(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
+      res = fmaxf(res, __shfl_xor_sync(0xffffffffu, res, o));
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      wmax[threadIdx.x >> 5] = nrm;
+      wres[threadIdx.x >> 5] = res;
+      wabs[threadIdx.x >> 5] = amax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float m = 0.f, mr = 0.f, ma = 0.f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        m = fmaxf(m, wmax[w]);
+        mr = fmaxf(mr, wres[w]);
+        ma = fmaxf(ma, wabs[w]);
+      }
+      if (MODE == 1) {
+        atomicMax(stats, __float_as_uint(m));
+        atomicMax(stats + 4, __float_as_uint(ma));
+      }
+      atomicMax(stats + 5, __float_as_uint(mr));
+    }
+  }
+}
+
+// -(h, m, l) of s t ||x||^2 / alpha in fp16 (core-matrix layout) from the
+// fp32 norms; padding rows -inf.  Also folds the chunk's residual max into
+// the global one (stats[2]).
+__global__ void ext_f16_kernel(const float* __restrict__ xn, int64_t rows, int64_t rows_pad,
+                               unsigned* __restrict__ stats, uint8_t* __restrict__ ext) {
+  const float* sc = reinterpret_cast<const float*>(stats + kF16Slot);
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) atomicMax(stats + 2, stats[5]);
+  if (r >= rows_pad) return;
+  __half e[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) e[j] = __float2half(0.f);
+  if (r < rows) {
+    const double V = (double)sc[0] * (double)sc[1] * (double)xn[r] / (double)sc[2];
+    const __half h0 = __double2half(V);
+    const double r1 = V - (double)__half2float(h0);
+    const __half h1 = __double2half(r1);
+    const __half h2 = __double2half(r1 - (double)__half2float(h1));
+    e[0] = __hneg(h0);
+    e[1] = __hneg(h1);
+    e[2] = __hneg(h2);
+  } else {
+    e[0] = __float2half(-INFINITY);
+  }
+  uint8_t* base = ext + (r >> 8) * 8192 + ((r & 255) >> 3) * 256 + (r & 7) * 16;
+  *reinterpret_cast<uint4*>(base) = *reinterpret_cast<const uint4*>(e);
+  *reinterpret_cast<uint4*>(base + 128) = make_uint4(0u, 0u, 0u, 0u);
+}
+
+template <typename T, int MODE>
+static void f16_rows_launch(const void* src, int64_t rows, int64_t d, double* n64, float* n32,
+                            float* norm32, float* resid, unsigned* stats, __half* hi,
+                            int64_t rows_pad, int64_t d_pad, bool norm, cudaStream_t st) {
+  const int G = d_pad == 64 ? 8 : d_pad == 128 ? 16 : 32;
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(rows_pad * G, 256), 148 * 8);
+#define TB_F16(GG, NN)                                                                   \
+  rows_f16_kernel<T, GG, NN, MODE><<<blocks, 256, 0, st>>>(                              \
+      (const T*)src, rows, d, n64, n32, norm32, resid, stats, hi, rows_pad, d_pad)
+  if (G == 8) {
+    if (norm) TB_F16(8, true); else TB_F16(8, false);
+  } else if (G == 16) {
+    if (norm) TB_F16(16, true); else TB_F16(16, false);
+  } else {
+    if (norm) TB_F16(32, true); else TB_F16(32, false);
+  }
+#undef TB_F16
+}
+
+template <typename T>
+static int f16_query_prep(const void* q, int64_t m, int64_t d, double* qn64, float* qnorm,
+                          float* qln, unsigned* stats, __half* qhi, int64_t m_pad,
+                          int64_t d_pad, int metric, cudaStream_t st) {
+  if (d_pad % 64) return fail(TB_ERR_UNSUPPORTED, "tensor-core prep needs d_pad % 64 == 0");
+  TB_CUDA_TRY(cudaMemsetAsync(stats + 3, 0, 4, st));
+  if (metric != TB_METRIC_COSINE && m > 0) {
+    const int64_t n = m * d;
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, 256 * 4), 148 * 8);
+    if (sizeof(T) == 4)
+      absmax_f32_kernel<<<blocks, 256, 0, st>>>((const float*)q, n, stats + 3);
+    else
+      absmax_f64_kernel<<<blocks, 256, 0, st>>>((const double*)q, n, stats + 3);
+    TB_LAUNCH_CHECK("absmax");
+  }
+  f16_scales_kernel<<<1, 1, 0, st>>>(stats, d, 0, metric);
+  TB_LAUNCH_CHECK("f16_scales");
+  f16_rows_launch<T, 0>(q, m, d, qn64, nullptr, qnorm, qln, stats, qhi, m_pad, d_pad,
+                        metric == TB_METRIC_COSINE, st);
+  TB_LAUNCH_CHECK("rows_f16");
+  return TB_OK;
+}
+
+template <typename T>
+static int f16_db_prep(const void* x, int64_t rows, int64_t d, float* xn, unsigned* stats,
+                       __half* xhi, int64_t rows_pad, int64_t d_pad, uint8_t* ext, int metric,
+                       cudaStream_t st) {
+  if (d_pad % 64) return fail(TB_ERR_UNSUPPORTED, "tensor-core prep needs d_pad % 64 == 0");
+  TB_CUDA_TRY(cudaMemsetAsync(stats + 4, 0, 8, st));          // chunk max |x|, max ||xl||
+  const bool norm = metric == TB_METRIC_COSINE;
+  f16_rows_launch<T, 1>(x, rows, d, nullptr, xn, nullptr, nullptr, stats, xhi, rows_pad,
+                        d_pad, norm, st);
+  f16_scales_kernel<<<1, 1, 0, st>>>(stats, d, 1, metric);
+  f16_rows_launch<T, 2>(x, rows, d, nullptr, xn, nullptr, nullptr, stats, xhi, rows_pad,
+                        d_pad, norm, st);
+  ext_f16_kernel<<<(unsigned)ceil_div(rows_pad, 256), 256, 0, st>>>(xn, rows, rows_pad, stats,
+                                                                    ext);
+  TB_LAUNCH_CHECK("rows_f16");
+  return TB_OK;
+}
+
+int launch_query_prep_f16(int dtype, int metric, const void* q, int64_t m, int64_t d,
+                          double* qn64, float* qnorm, float* qln, unsigned* stats,
+                          __half* qhi, int64_t m_pad, int64_t d_pad, cudaStream_t st) {
+  if (dtype == TB_F32)
+    return f16_query_prep<float>(q, m, d, qn64, qnorm, qln, stats, qhi, m_pad, d_pad, metric, st);
+  return f16_query_prep<double>(q, m, d, qn64, qnorm, qln, stats, qhi, m_pad, d_pad, metric, st);
+}
+
+int launch_db_prep_f16(int dtype, int metric, const void* x, int64_t rows, int64_t d,
+                       float* xn, unsigned* stats, __half* xhi, int64_t rows_pad,
+                       int64_t d_pad, uint8_t* xext, cudaStream_t st) {
+  if (dtype == TB_F32)
+    return f16_db_prep<float>(x, rows, d, xn, stats, xhi, rows_pad, d_pad, xext, metric, st);
+  return f16_db_prep<double>(x, rows, d, xn, stats, xhi, rows_pad, d_pad, xext, metric, st);
+}
+
 int launch_query_prep(int dtype, int metric, const void* q, int64_t m, int64_t d,
                       double* qn64, float* qnorm, __nv_bfloat16* qhi,
                       __nv_bfloat16* qlo, int64_t m_pad, int64_t d_pad,
@@ -524,6 +839,7 @@ __global__ void knn_refine_kernel(const float* __restrict__ cs,
                                   const T* __restrict__ x, const T* __restrict__ q,
                                   const double* __restrict__ qn64,
                                   const float* __restrict__ qnorm,
+                                  const float* __restrict__ qln,
                                   unsigned* __restrict__ stats, int64_t m,
                                   int64_t d, int k, double c1, double c2,
                                   OT* __restrict__ out_dist,
@@ -585,7 +901,14 @@ __global__ void knn_refine_kernel(const float* __restrict__ cs,
       if (MET == TB_METRIC_L1) {
         ok = (double)tstar / (1.0 + c1) - c2 * ((double)qnorm[r] + X) > kth;
       } else {
-        const double E = c1 * (double)qnorm[r] * X + c2 * X * X;
+        double E = c1 * (double)qnorm[r] * X + c2 * X * X;
+        if (qln) {
+          // fp16 single pass: measured rounding residuals (Cauchy-Schwarz),
+          // |q.x - q'.x'| <= ||q|| XL + ||ql|| (X + 3 XL), times 2 for -2 q.x
+          const double XL = (double)__uint_as_float(stats[2]);
+          E += 2.0 * (1.0 + 1e-6) *
+               ((double)qnorm[r] * XL + (double)qln[r] * (X + 3.0 * XL));
+        }
         const double exact_score_k = MET == TB_METRIC_COSINE ? 2.0 * kth - 1.0 : kth - qn64[r];
         ok = (double)tstar - E > exact_score_k;
       }
@@ -600,7 +923,7 @@ __global__ void knn_refine_kernel(const float* __restrict__ cs,
 template <typename T, typename OT, int MET>
 static int refine_dispatch(int cand, const float* cs, const int* ci,
                            const void* x, const void* q, const double* qn64,
-                           const float* qnorm, unsigned* stats, int64_t m,
+                           const float* qnorm, const float* qln, unsigned* stats, int64_t m,
                            int64_t d, int64_t k, double c1, double c2,
                            void* od, int64_t* oi, int64_t base, int* fb,
                            cudaStream_t st) {
@@ -609,7 +932,7 @@ static int refine_dispatch(int cand, const float* cs, const int* ci,
 #define TB_REFINE_CASE(KC)                                                   \
   case KC:                                                                   \
     knn_refine_kernel<T, OT, KC, MET><<<blocks, warps * 32, 0, st>>>(        \
-        cs, ci, (const T*)x, (const T*)q, qn64, qnorm, stats, m, d, (int)k,  \
+        cs, ci, (const T*)x, (const T*)q, qn64, qnorm, qln, stats, m, d, (int)k,  \
         c1, c2, (OT*)od, oi, base, fb);                                      \
     break;
   switch (cand) {
@@ -625,7 +948,7 @@ static int refine_dispatch(int cand, const float* cs, const int* ci,
 
 int launch_knn_refine(int dtype, int out_dtype, int metric, int cand, const float* cs,
                       const int* ci, const void* x, const void* q,
-                      const double* qn64, const float* qnorm,
+                      const double* qn64, const float* qnorm, const float* qln,
                       const unsigned* stats, int64_t n, int64_t m, int64_t d,
                       int64_t k, double c1, double c2, void* out_dist,
                       int64_t* out_idx, int64_t index_base, int* fb_list,
@@ -634,7 +957,7 @@ int launch_knn_refine(int dtype, int out_dtype, int metric, int cand, const floa
   if (m <= 0) return TB_OK;
   unsigned* s = const_cast<unsigned*>(stats);
 #define TB_REF(T, OT, MET)                                                                  \
-  return refine_dispatch<T, OT, MET>(cand, cs, ci, x, q, qn64, qnorm, s, m, d, k, c1, c2,   \
+  return refine_dispatch<T, OT, MET>(cand, cs, ci, x, q, qn64, qnorm, qln, s, m, d, k, c1, c2,   \
                                      out_dist, out_idx, index_base, fb_list, st)
 #define TB_REF_MET(T, OT)                                        \
   if (metric == TB_METRIC_L1) TB_REF(T, OT, TB_METRIC_L1);       \

@@ -86,7 +86,11 @@ struct TcWork {
 // extra K=16 MMA per tile (A_ext rows = [1,1,1,0...], B_ext rows =
 // -(h,m,l), the bf16 triple split of ||x||^2; SWIZZLE_NONE K-major core
 // matrices).  The selection score is s = -acc' = ||x||^2 - 2 q.x.
-template <int PASSES, int KC, bool SQ>
+// F16 (engine tc1): one fp16 pass; operands were scaled by powers of two
+// (f16p = [s, t, alpha, 1/(s t)], knn_kernels.cu rows_f16_kernel), so the
+// accumulator holds s t (2 q.x - ||x||^2): A_ext rows are [alpha x3] and the
+// scores published (thresholds, candidate lists) are unscaled by 1/(s t).
+template <int PASSES, int KC, bool SQ, bool F16>
 __global__ void __launch_bounds__(kTcThreads, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               const __grid_constant__ CUtensorMap tm_qlo,
@@ -94,7 +98,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               const __grid_constant__ CUtensorMap tm_xlo,
               const uint8_t* __restrict__ xext, TcWork work, int m, int nkb,
               int idx_base, float* __restrict__ cand_s, int* __restrict__ cand_i,
-              unsigned* __restrict__ gthr) {
+              unsigned* __restrict__ gthr, const float* __restrict__ f16p) {
   using Cfg = TcCfg<PASSES, SQ>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -118,10 +122,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
 
   // constant A_ext: row r = [1, 1, 1, 0 ... 0] in the interleaved layout
   // (8-row groups of 256 B: k-chunk 0 at +0, k-chunk 1 at +128)
+  uint32_t one = 0x3F80u;                                // bf16(1.0)
+  float sc_mul = 1.f, sc_inv = 1.f;                      // engine units <-> score units
+  if (F16) {
+    one = __half_as_ushort(__float2half(f16p[2]));       // alpha (power of two)
+    sc_inv = f16p[3];
+    sc_mul = 1.f / sc_inv;
+  }
   for (int r = threadIdx.x; r < kTcM; r += blockDim.x) {
     uint4* c0 = reinterpret_cast<uint4*>(aext + (r >> 3) * 256 + (r & 7) * 16);
     uint4* c1 = reinterpret_cast<uint4*>(aext + (r >> 3) * 256 + 128 + (r & 7) * 16);
-    const uint32_t one = 0x3F80u;                        // bf16(1.0)
     *c0 = make_uint4(one | (one << 16), one, 0u, 0u);
     *c1 = make_uint4(0u, 0u, 0u, 0u);
   }
@@ -213,7 +223,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(kTcM, kTcN);
+      constexpr uint32_t idesc = F16 ? idesc_f16_f32(kTcM, kTcN) : idesc_bf16_f32(kTcM, kTcN);
       const uint32_t aext_a = smem_u32(aext);
       int s = 0, i = 0;
       uint32_t ph = 0, seg = 0;
@@ -309,7 +319,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         const int buf = i & 1;
         // candidates must also beat the best K'-th score any list has
         // published for this query (a valid bound for the union)
-        const float thr_g = q < m ? fkey_inv(gk) : -INFINITY;
+        const float thr_g = q < m ? fkey_inv(gk) * sc_mul : -INFINITY;
         int nu = u, nt = t + 1;
         if (nt >= t1) {
           nu = u + gridDim.x;
@@ -355,14 +365,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         mbar_arrive(&tempty[buf]);
         // publish the running K'-th score every tile: the other column half
         // and every other CTA on this query tighten their thresholds with it
-        if (q < m && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst()));
+        if (q < m && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst() * sc_inv));
         if (nu != u) {
           // unit done: publish this (slice, column half)'s candidates
           if (q < m) {
             const int64_t o = ((int64_t)(work.list0 + slice * 2 + half) * m + q) * KC;
 #pragma unroll
             for (int p = 0; p < KC; ++p) {
-              cand_s[o + p] = L.s[p];
+              cand_s[o + p] = L.s[p] * sc_inv;
               cand_i[o + p] = L.i[p];
             }
           }
@@ -668,14 +678,15 @@ knn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_qhi,
 
 // bf16 [rows, cols] row-major, box [box_rows, 64], 128-B swizzle
 static int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
-                    uint32_t box_rows) {
+                    uint32_t box_rows, bool f16 = false) {
   auto fn = tensor_map_encoder();
   if (!fn) return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
   cuuint32_t box[2] = {(cuuint32_t)kTcKB, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+  CUresult r = fn(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                  2, const_cast<void*>(base), dims,
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -790,12 +801,13 @@ template <int PASSES, int KC, bool SQ>
 static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtensorMap& xh,
                      const CUtensorMap& xl, const uint8_t* xext, TcWork work,
                      int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
-                     unsigned* gthr, cudaStream_t st) {
+                     unsigned* gthr, const float* f16p, cudaStream_t st) {
+  constexpr bool F16 = PASSES == 1;            // engine tc1 is the fp16 single pass
   const size_t smem = TcCfg<PASSES, SQ>::smem_bytes(nkb);
-  TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<PASSES, KC, SQ>,
+  TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<PASSES, KC, SQ, F16>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  knn_tc_kernel<PASSES, KC, SQ><<<grid, kTcThreads, smem, st>>>(qh, ql, xh, xl, xext, work,
-                                                            (int)m, nkb, idx_base, cs, ci, gthr);
+  knn_tc_kernel<PASSES, KC, SQ, F16><<<grid, kTcThreads, smem, st>>>(
+      qh, ql, xh, xl, xext, work, (int)m, nkb, idx_base, cs, ci, gthr, f16p);
   TB_LAUNCH_CHECK("knn_tc");
   return TB_OK;
 }
@@ -803,13 +815,13 @@ static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtenso
 int tc_dispatch(int passes, int cand, const CUtensorMap& mqh, const CUtensorMap& mql,
                 const CUtensorMap& mxh, const CUtensorMap& mxl, const uint8_t* xext,
                 TcWork work, int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
-                unsigned* gthr, cudaStream_t st);
+                unsigned* gthr, const float* f16p, cudaStream_t st);
 
 int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfloat16* xlo,
                   const __nv_bfloat16* qhi, const __nv_bfloat16* qlo, const uint8_t* xext,
                   int64_t rows, int64_t rows_pad, int64_t m, int64_t m_pad, int64_t d_pad,
                   int lists, int idx_base, float* cs, int* ci, unsigned* gthr,
-                  cudaStream_t st) {
+                  const float* f16p, cudaStream_t st) {
   if (d_pad > kTcMaxDpadSQ || d_pad % kTcKB)
     return fail(TB_ERR_UNSUPPORTED, "tcgen05 engine: d_pad must be a multiple of 64, <= 1024");
   int dev = 0, sms = 148;
@@ -817,10 +829,11 @@ int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfl
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   CUtensorMap mqh, mql, mxh, mxl;
   int rc;
-  if ((rc = make_map(&mqh, qhi, m_pad, d_pad, kTcM))) return rc;
-  if ((rc = make_map(&mql, passes == 3 ? qlo : qhi, m_pad, d_pad, kTcM))) return rc;
-  if ((rc = make_map(&mxh, xhi, rows_pad, d_pad, kTcN))) return rc;
-  if ((rc = make_map(&mxl, passes == 3 ? xlo : xhi, rows_pad, d_pad, kTcN))) return rc;
+  const bool f16 = passes == 1;
+  if ((rc = make_map(&mqh, qhi, m_pad, d_pad, kTcM, f16))) return rc;
+  if ((rc = make_map(&mql, passes == 3 ? qlo : qhi, m_pad, d_pad, kTcM, f16))) return rc;
+  if ((rc = make_map(&mxh, xhi, rows_pad, d_pad, kTcN, f16))) return rc;
+  if ((rc = make_map(&mxl, passes == 3 ? xlo : xhi, rows_pad, d_pad, kTcN, f16))) return rc;
   const bool pair = tc_pair_on(passes, d_pad, m);
   TcWork seed, work;
   tc_schedule(m, rows_pad, 148, pair, &seed, &work);   // the plan's schedule (148 SMs)
@@ -843,22 +856,23 @@ int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfl
   }
   // every list slot the merge reads must be written: unused ones stay INF
   rc = tc_dispatch(passes, cand, mqh, mql, mxh, mxl, xext, seed, std::min(seed.qtiles, sms),
-                   m, nkb, idx_base, cs, ci, gthr, st);
+                   m, nkb, idx_base, cs, ci, gthr, f16p, st);
   if (rc || work.slices == 0) return rc;
   return tc_dispatch(passes, cand, mqh, mql, mxh, mxl, xext, work,
-                     std::min(work.qtiles * work.slices, sms), m, nkb, idx_base, cs, ci, gthr, st);
+                     std::min(work.qtiles * work.slices, sms), m, nkb, idx_base, cs, ci, gthr,
+                     f16p, st);
 }
 
 int tc_dispatch(int passes, int cand, const CUtensorMap& mqh, const CUtensorMap& mql,
                 const CUtensorMap& mxh, const CUtensorMap& mxl, const uint8_t* xext,
                 TcWork work, int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
-                unsigned* gthr, cudaStream_t st) {
+                unsigned* gthr, const float* f16p, cudaStream_t st) {
 #define TB_TC(P, KC)                                                                       \
   return nkb * kTcKB > kTcMaxDpad                                                          \
              ? tc_launch<P, KC, true>(mqh, mql, mxh, mxl, xext, work, grid, m, nkb, idx_base, \
-                                      cs, ci, gthr, st)                                      \
+                                      cs, ci, gthr, f16p, st)                                \
              : tc_launch<P, KC, false>(mqh, mql, mxh, mxl, xext, work, grid, m, nkb, idx_base, \
-                                       cs, ci, gthr, st)
+                                       cs, ci, gthr, f16p, st)
   if (passes == 3) {
     if (cand == 16) TB_TC(3, 16);
     if (cand == 32) TB_TC(3, 32);

@@ -200,6 +200,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
          | (1u << 10)         // B bf16
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// instruction descriptor, kind::f16: fp16 x fp16 -> f32, both K-major
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N) {
+  return (1u << 4)            // D format f32
+         | (0u << 7)          // A f16
+         | (0u << 10)         // B f16
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 // instruction descriptor, kind::i8: u8 x u8 -> s32, both K-major
 __host__ __device__ constexpr uint32_t idesc_u8_s32(int M, int N) {
   return (2u << 4)            // D format s32

@@ -164,6 +164,21 @@ def test_cta_pair_tc_kernel(n, m, d, monkeypatch):
     assert op.fallback_count() == 0
 
 
+@pytest.mark.parametrize("scale", [1e5, 1e3, 1e-4, 3e-9])
+def test_fp16_engine_scaling_is_exact(scale):
+    """Engine tc1 (fp16 single pass) scales operands by powers of two into
+    fp16 range: large data (redo pass with t < 1), tiny data (t > 1) and data
+    that fits as is must all give the exact answer without fallbacks."""
+    import torch
+    x, q = synthetic.gaussian_knn(40000, 300, 96, seed=int(-np.log10(scale) * 10) % 97)
+    x, q = x * np.float32(scale), q * np.float32(scale)
+    ref_d, ref_i = oknn.exact(x, q, 10)
+    op = neighbors.KnnOperator(40000, 300, 96, 10, engine="tc1")
+    dist, idx = op.run(torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda())
+    check(dist.cpu().numpy(), idx.cpu().numpy(), ref_d, ref_i, x, q)
+    assert op.fallback_count() == 0
+
+
 def test_duplicates_resolve_to_lower_index(engines):
     rng = np.random.default_rng(4)
     base = rng.standard_normal((50, 12)).astype(np.float32)

@@ -14,7 +14,7 @@ timeout 600 python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $O/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline \
   --no-sgpr --no-e2e > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:knn_tc -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:knn_tc -s 3 -c 1 \
   -o $O/knn_tc python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-sgpr \
   > $O/ncu_knn.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tail_potrf -s 3 -c 1 \
