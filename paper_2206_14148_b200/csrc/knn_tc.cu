@@ -59,6 +59,25 @@ struct TcCfg {
   }
 };
 
+// max of 32 fp32 accumulator words with the 3-input FMNMX3 of sm_100
+// (max.f32 d, a, b, c): 16 instructions instead of 31
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float max_of_32(const uint32_t (&r)[32]) {
+  float m[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i)
+    m[i] = max3f(__uint_as_float(r[3 * i]), __uint_as_float(r[3 * i + 1]),
+                 __uint_as_float(r[3 * i + 2]));
+  m[10] = fmaxf(__uint_as_float(r[30]), __uint_as_float(r[31]));
+  const float a = max3f(m[0], m[1], m[2]), b = max3f(m[3], m[4], m[5]);
+  const float c = max3f(m[6], m[7], m[8]), e = fmaxf(m[9], m[10]);
+  return fmaxf(max3f(a, b, c), e);
+}
+
 // order-preserving float <-> u32 keys for the shared per-query threshold
 __device__ __forceinline__ uint32_t fkey(float f) {
   const uint32_t b = __float_as_uint(f);
@@ -346,9 +365,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             // over acc' (score = -acc'); the rare insertions run from one
             // compact loop so the hot path fits the I-cache
             const float thr = fminf(L.worst(), thr_g);
-            float hi = __uint_as_float(r[0]);
-#pragma unroll
-            for (int j = 1; j < 32; ++j) hi = fmaxf(hi, __uint_as_float(r[j]));
+            const float hi = max_of_32(r);
             if (-hi < thr && !(work.drain_only & 8)) {
               float sc[32];
               uint32_t mask = 0;
@@ -627,9 +644,7 @@ knn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           for (int h = 0; h < 2; ++h) {
             const uint32_t(&r)[32] = h ? rb : ra;
             const float thr = fminf(L.worst(), thr_g);
-            float hi = __uint_as_float(r[0]);
-#pragma unroll
-            for (int j = 1; j < 32; ++j) hi = fmaxf(hi, __uint_as_float(r[j]));
+            const float hi = max_of_32(r);
             if (-hi < thr && !(work.drain_only & 8)) {
               float sc[32];
               uint32_t mask = 0;
