@@ -78,6 +78,30 @@ __device__ __forceinline__ float max_of_32(const uint32_t (&r)[32]) {
   return fmaxf(max3f(a, b, c), e);
 }
 
+// Offer the columns whose bit is set in `mask` (ascending), score = -acc.
+// The j-th accumulator word is picked by a 5-level select tree on the bits
+// of j (31 selects, registers only): no local-memory staging of the 32
+// scores as a dynamically indexed array would need.
+template <int K>
+__device__ __forceinline__ void insert_masked_acc(TopList<float, K>& L, const uint32_t (&r)[32],
+                                                  uint32_t mask, int base, float cap) {
+  while (mask) {
+    const int j = __ffs(mask) - 1;
+    mask &= mask - 1;
+    float t16[16], t8[8], t4[4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      t16[i] = __uint_as_float((j & 1) ? r[2 * i + 1] : r[2 * i]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t8[i] = (j & 2) ? t16[2 * i + 1] : t16[2 * i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t4[i] = (j & 4) ? t8[2 * i + 1] : t8[2 * i];
+    const float t2a = (j & 8) ? t4[1] : t4[0], t2b = (j & 8) ? t4[3] : t4[2];
+    const float v = -((j & 16) ? t2b : t2a);
+    if (v < L.worst() && v < cap) L.insert_after(v, base + j);
+  }
+}
+
 // order-preserving float <-> u32 keys for the shared per-query threshold
 __device__ __forceinline__ uint32_t fkey(float f) {
   const uint32_t b = __float_as_uint(f);
@@ -367,14 +391,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             const float thr = fminf(L.worst(), thr_g);
             const float hi = max_of_32(r);
             if (-hi < thr && !(work.drain_only & 8)) {
-              float sc[32];
+              const float nthr = -thr;                   // score < thr <=> acc > -thr
               uint32_t mask = 0;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                sc[j] = -__uint_as_float(r[j]);
-                mask |= (sc[j] < thr ? 1u : 0u) << j;
-              }
-              insert_masked(L, sc, mask, base + (c + h) * 32, thr_g);
+              for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(r[j]) > nthr ? 1u : 0u) << j;
+              insert_masked_acc(L, r, mask, base + (c + h) * 32, thr_g);
             }
           }
         }
@@ -646,14 +667,11 @@ knn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             const float thr = fminf(L.worst(), thr_g);
             const float hi = max_of_32(r);
             if (-hi < thr && !(work.drain_only & 8)) {
-              float sc[32];
+              const float nthr = -thr;                   // score < thr <=> acc > -thr
               uint32_t mask = 0;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                sc[j] = -__uint_as_float(r[j]);
-                mask |= (sc[j] < thr ? 1u : 0u) << j;
-              }
-              insert_masked(L, sc, mask, base + (c + h) * 32, thr_g);
+              for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(r[j]) > nthr ? 1u : 0u) << j;
+              insert_masked_acc(L, r, mask, base + (c + h) * 32, thr_g);
             }
           }
         }
