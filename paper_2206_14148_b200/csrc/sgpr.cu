@@ -474,13 +474,22 @@ int tb_sgpr_stats_run(const tb_sgpr_plan* p, const void* X, const void* y, const
     uint8_t* planes[2] = {(uint8_t*)workspace + p->off[0], (uint8_t*)workspace + p->off[2]};
     double* vpart[2] = {(double*)((uint8_t*)workspace + p->off[1]),
                         (double*)((uint8_t*)workspace + p->off[3])};
-    cudaStream_t gen = st;
+    cudaStream_t gen = st, user = st;
     cudaEvent_t ev[5] = {};   // start, gen done (buf 0/1), gram done (buf 0/1)
     if (nbuf == 2) {
+      // the Grams run on a HIGH-priority internal stream: when a Gram and the
+      // next chunk's generation become ready together, the block scheduler
+      // places the Gram's persistent CTAs first and the generator's blocks
+      // fill the room left beside them, instead of the generator flooding
+      // every SM and the two phases serialising
+      int lo = 0, hi = 0;
+      TB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       TB_CUDA_TRY(cudaStreamCreateWithFlags(&gen, cudaStreamNonBlocking));
+      TB_CUDA_TRY(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
       for (auto& e : ev) TB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      TB_CUDA_TRY(cudaEventRecord(ev[0], st));
+      TB_CUDA_TRY(cudaEventRecord(ev[0], user));
       TB_CUDA_TRY(cudaStreamWaitEvent(gen, ev[0], 0));
+      TB_CUDA_TRY(cudaStreamWaitEvent(st, ev[0], 0));
     }
     int64_t c = 0;
     for (int64_t n0 = 0; n0 < N && rc == TB_OK; n0 += nc, ++c) {
@@ -499,11 +508,15 @@ int tb_sgpr_stats_run(const tb_sgpr_plan* p, const void* X, const void* y, const
       if (nbuf == 2 && rc == TB_OK) TB_CUDA_TRY(cudaEventRecord(ev[3 + b], st));
     }
     if (nbuf == 2) {
-      // v / yy (side stream) complete before anything later on `st`
+      // v / yy (side stream) and the Grams complete before anything later on
+      // the caller's stream
       cudaEventRecord(ev[0], gen);
-      cudaStreamWaitEvent(st, ev[0], 0);
+      cudaStreamWaitEvent(user, ev[0], 0);
+      cudaEventRecord(ev[1], st);
+      cudaStreamWaitEvent(user, ev[1], 0);
       for (auto& e : ev) cudaEventDestroy(e);
       cudaStreamDestroy(gen);
+      cudaStreamDestroy(st);
     }
     return rc;
   }

@@ -56,59 +56,96 @@ constexpr int kI8Threads = 64 + 32 * kI8EpiWarps;
 constexpr size_t kI8Smem = 1024 + (size_t)kI8Stages * kI8StageBytes + 512;   // + barriers
 
 // ------------------------------------------------------------ kuf_quant --
-// Block: 32 inducing rows x 128 points, 128 threads (one point each, all 32
-// rows); small enough to co-reside with the persistent Gram CTA of the
-// previous chunk (which leaves ~11k registers and ~30 KB of shared memory
-// per SM), so the fp64 generation overlaps the tensor-core Gram.
+// Block: 32 inducing rows x 128 points, 128 threads.  Lane l owns inducing
+// row i0 + l (its scaled z in registers) and warp w the points w*32..+31, so
+// that
+//   * the scaled points x_c / l are staged once per block in shared memory
+//     and read as broadcast 16-byte loads (one per two dimensions),
+//   * v_i = sum_c q_ic y_c accumulates in the owning thread's register (no
+//     per-element warp reductions), the 4 warps' partials combined in a fixed
+//     order,
+//   * q = rint(k 2^24 / variance) comes from the low word of
+//     min(k qscale, 2^24 - 1) + 1.5 * 2^52 (round-to-nearest-even in the add,
+//     no float->int conversion), and (double) q is that sum minus the magic,
+//   * the three digit bytes are staged in shared memory (rows padded to 132
+//     bytes against bank conflicts) and written out as coalesced 128-byte
+//     rows.
+// r^2 and k are the same fp64 expressions, in the same order, as before and
+// as oracle.sgpr.sufficient_stats_fixed24.  EXACT: DMAX is the dimension
+// (no predicated-off dimensions issue).
 constexpr int kI8QuantThreads = 128;
-template <typename T, int DMAX>
+constexpr int kQRows = 32, kQPts = 128, kQLd = kQPts + 4;
+template <typename T, int DMAX, bool EXACT>
 __global__ void __launch_bounds__(kI8QuantThreads)
 kuf_quant_kernel(const T* __restrict__ X, const T* __restrict__ y, const T* __restrict__ Z,
                  int64_t n0, int64_t cur, int64_t M, int64_t M_pad, int64_t nc, KernParams p,
                  double qscale, uint8_t* __restrict__ planes, double* __restrict__ vpart) {
-  __shared__ double zs[32][DMAX + 1];
-  __shared__ double red[32][4];
-  const int i0 = blockIdx.y * 32;
-  const int64_t c = (int64_t)blockIdx.x * 128 + (threadIdx.x & 127);
-  for (int e = threadIdx.x; e < 32 * p.dim; e += blockDim.x) {
-    const int r = e / p.dim, t = e % p.dim;
-    zs[r][t] = (i0 + r < M) ? (double)Z[(int64_t)(i0 + r) * p.dim + t] * p.inv_ls[t] : 0.0;
+  constexpr int DP = (DMAX + 1) & ~1;
+  extern __shared__ __align__(16) double xs_dyn[];     // [kQPts][DP]
+  double (*xs)[DP] = reinterpret_cast<double (*)[DP]>(xs_dyn);
+  __shared__ double ys[kQPts];
+  __shared__ __align__(16) uint8_t qb[3][kQRows][kQLd];
+  __shared__ double vred[4][kQRows];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * kQPts;
+  const int i0 = blockIdx.y * kQRows;
+  const int dim = EXACT ? DMAX : p.dim;
+  for (int e = tid; e < kQPts * DP; e += kI8QuantThreads) {
+    const int pc = e / DP, t = e % DP;
+    const int64_t c = c0 + pc;
+    xs[pc][t] = (c < cur && t < dim) ? (double)X[(n0 + c) * p.dim + t] * p.inv_ls[t] : 0.0;
   }
+  for (int pc = tid; pc < kQPts; pc += kI8QuantThreads) {
+    const int64_t c = c0 + pc;
+    ys[pc] = c < cur ? (double)y[n0 + c] : 0.0;
+  }
+  const int64_t i = i0 + lane;
+  const bool row_ok = i < M;
+  double zr[DP];
+#pragma unroll
+  for (int t = 0; t < DP; ++t)
+    zr[t] = (row_ok && t < dim) ? (double)Z[i * p.dim + t] * p.inv_ls[t] : 0.0;
   __syncthreads();
-  const bool valid = c < cur;
-  double xs[DMAX];
+  const double magic = 6755399441055744.0;            // 1.5 * 2^52
+  double vacc = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < 32; ++k) {
+    const int pc = warp * 32 + k;
+    double r2 = 0.0;
 #pragma unroll
-  for (int t = 0; t < DMAX; ++t)
-    if (t < p.dim) xs[t] = valid ? (double)X[(n0 + c) * p.dim + t] * p.inv_ls[t] : 0.0;
-  const double yc = valid ? (double)y[n0 + c] : 0.0;
-  const int64_t plane = M_pad * nc;
-  const int lane = threadIdx.x & 31, wq = (threadIdx.x & 127) >> 5;
-  for (int r = 0; r < 32; ++r) {
-    const int64_t i = i0 + r;
-    uint32_t q = 0;
-    if (valid && i < M) {
-      double r2 = 0.0;
-#pragma unroll
-      for (int t = 0; t < DMAX; ++t)
-        if (t < p.dim) {
-          const double df = zs[r][t] - xs[t];
-          r2 = fma(df, df, r2);
-        }
-      const double k = kern_from_r2(p, r2);
-      q = (uint32_t)fmin(rint(k * qscale), 16777215.0);
+    for (int t = 0; t < DP; t += 2) {
+      const double2 xv = *reinterpret_cast<const double2*>(&xs[pc][t]);
+      if (EXACT || t < dim) {
+        const double d0 = zr[t] - xv.x;
+        r2 = fma(d0, d0, r2);
+      }
+      if (t + 1 < DMAX && (EXACT || t + 1 < dim)) {
+        const double d1 = zr[t + 1] - xv.y;
+        r2 = fma(d1, d1, r2);
+      }
     }
-    uint8_t* dst = planes + i * nc + c;
-    dst[0] = (uint8_t)(q & 255u);
-    dst[plane] = (uint8_t)((q >> 8) & 255u);
-    dst[2 * plane] = (uint8_t)(q >> 16);
-    // v partial: exact products q * y (24 + 24 bits), warp-ordered sums
-    const double s = warp_sum((double)q * yc);
-    if (lane == 0) red[r][wq] = s;
+    uint32_t q = 0;
+    if (row_ok && c0 + pc < cur) {
+      const double qm = fmin(kern_from_r2(p, r2) * qscale, 16777215.0) + magic;
+      q = (uint32_t)__double2loint(qm);
+      vacc = fma(qm - magic, ys[pc], vacc);             // exact q * y products
+    }
+    qb[0][lane][pc] = (uint8_t)(q & 255u);
+    qb[1][lane][pc] = (uint8_t)((q >> 8) & 255u);
+    qb[2][lane][pc] = (uint8_t)(q >> 16);
   }
+  vred[warp][lane] = vacc;
   __syncthreads();
-  if (threadIdx.x < 32)
-    vpart[(int64_t)blockIdx.x * M_pad + i0 + threadIdx.x] =
-        ((red[threadIdx.x][0] + red[threadIdx.x][1]) + red[threadIdx.x][2]) + red[threadIdx.x][3];
+  if (tid < kQRows)
+    vpart[(int64_t)blockIdx.x * M_pad + i0 + tid] =
+        ((vred[0][tid] + vred[1][tid]) + vred[2][tid]) + vred[3][tid];
+  const int64_t plane = M_pad * nc;
+  for (int e = tid; e < 3 * kQRows * (kQPts / 4); e += kI8QuantThreads) {
+    const int pl = e / (kQRows * (kQPts / 4));
+    const int rr = (e / (kQPts / 4)) % kQRows, seg = e % (kQPts / 4);
+    *reinterpret_cast<uint32_t*>(planes + pl * plane + (int64_t)(i0 + rr) * nc + c0 + seg * 4) =
+        *reinterpret_cast<const uint32_t*>(&qb[pl][rr][seg * 4]);
+  }
 }
 
 __global__ void v_reduce_kernel(const double* __restrict__ vpart, int nseg, int64_t M,
@@ -658,16 +695,29 @@ int i8_gen_chunk(const void* X, const void* y, const void* Z, int dtype, int64_t
   const int64_t ncur = round_up(cur, 128);           // columns written this chunk
   const double qscale = std::ldexp(1.0, kI8FracBits) / kp.variance;
   dim3 g((unsigned)(ncur / 128), (unsigned)(M_pad / 32));
-#define TB_KQ(T, D)                                                                        \
-  kuf_quant_kernel<T, D><<<g, kI8QuantThreads, 0, st>>>((const T*)X, (const T*)y, (const T*)Z, \
-                                                        n0, cur, M, M_pad, nc, kp, qscale,    \
-                                                        planes, vpart)
-#define TB_KQ_DIM(T)                   \
-  if (kp.dim <= 4) TB_KQ(T, 4);        \
-  else if (kp.dim <= 8) TB_KQ(T, 8);   \
-  else if (kp.dim <= 16) TB_KQ(T, 16); \
-  else if (kp.dim <= 32) TB_KQ(T, 32); \
-  else TB_KQ(T, 64)
+#define TB_KQ(T, D, EX)                                                                    \
+  do {                                                                                     \
+    const int xs_bytes = kQPts * ((D + 1) & ~1) * 8;                                       \
+    if (xs_bytes > 32768)                                                                  \
+      TB_CUDA_TRY(cudaFuncSetAttribute(kuf_quant_kernel<T, D, EX>,                         \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                       xs_bytes));                                         \
+    kuf_quant_kernel<T, D, EX><<<g, kI8QuantThreads, xs_bytes, st>>>(                      \
+        (const T*)X, (const T*)y, (const T*)Z, n0, cur, M, M_pad, nc, kp, qscale, planes,  \
+        vpart);                                                                            \
+  } while (0)
+#define TB_KQ_DIM(T)                                                      \
+  switch (kp.dim) {                                                       \
+    case 1: TB_KQ(T, 1, true); break;   case 2: TB_KQ(T, 2, true); break; \
+    case 3: TB_KQ(T, 3, true); break;   case 4: TB_KQ(T, 4, true); break; \
+    case 5: TB_KQ(T, 5, true); break;   case 6: TB_KQ(T, 6, true); break; \
+    case 7: TB_KQ(T, 7, true); break;   case 8: TB_KQ(T, 8, true); break; \
+    case 11: TB_KQ(T, 11, true); break; case 16: TB_KQ(T, 16, true); break; \
+    default:                                                              \
+      if (kp.dim <= 16) TB_KQ(T, 16, false);                              \
+      else if (kp.dim <= 32) TB_KQ(T, 32, false);                         \
+      else TB_KQ(T, 64, false);                                           \
+  }
   if (dtype == TB_F32) {
     TB_KQ_DIM(float);
   } else {
@@ -716,6 +766,12 @@ int i8_gram_chunk(int64_t cur, int64_t M_pad, int64_t nc, double variance, const
   const int units = (int)i8_tiles(M_pad);
   TB_CUDA_TRY(cudaFuncSetAttribute(sgpr_gram_i8_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem));
+  // the whole 228 KB as shared memory: with the Gram CTA's ~199 KB there is
+  // room beside it for a digit-plane producer block (kuf_quant, ~6 KB, 56
+  // registers x 128 threads fit the Gram's unused register file), so the
+  // next chunk's generation can run on the CUDA cores next to the Gram
+  TB_CUDA_TRY(cudaFuncSetAttribute(sgpr_gram_i8_kernel,
+                                   cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   sgpr_gram_i8_kernel<<<std::min(units, sms), kI8Threads, kI8Smem, st>>>(tm, units, nkb,
                                                                          (int)M_pad, scale,
                                                                          Sigma_tiles, dbg);
