@@ -78,13 +78,24 @@ __device__ __forceinline__ float max_of_32(const uint32_t (&r)[32]) {
   return fmaxf(max3f(a, b, c), e);
 }
 
+// order-preserving float <-> u32 keys for the shared per-query threshold
+__device__ __forceinline__ uint32_t fkey(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+  if (k >= 0xFF800000u) return INFINITY;   // unset (0xFFFFFFFF) or +inf
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
 // Offer the columns whose bit is set in `mask` (ascending), score = -acc.
 // The j-th accumulator word is picked by a 5-level select tree on the bits
 // of j (31 selects, registers only): no local-memory staging of the 32
 // scores as a dynamically indexed array would need.
 template <int K>
 __device__ __forceinline__ void insert_masked_acc(TopList<float, K>& L, const uint32_t (&r)[32],
-                                                  uint32_t mask, int base, float cap) {
+                                                  uint32_t mask, int base, float cap,
+                                                  unsigned* pool = nullptr, float sc_inv = 1.f) {
   while (mask) {
     const int j = __ffs(mask) - 1;
     mask &= mask - 1;
@@ -98,18 +109,13 @@ __device__ __forceinline__ void insert_masked_acc(TopList<float, K>& L, const ui
     for (int i = 0; i < 4; ++i) t4[i] = (j & 4) ? t8[2 * i + 1] : t8[2 * i];
     const float t2a = (j & 8) ? t4[1] : t4[0], t2b = (j & 8) ? t4[3] : t4[2];
     const float v = -((j & 16) ? t2b : t2a);
-    if (v < L.worst() && v < cap) L.insert_after(v, base + j);
+    if (v < L.worst() && v < cap) {
+      L.insert_after(v, base + j);
+      // union bound: slot (index mod K') keeps the best score hashed to it;
+      // K' finite slots = K' distinct elements at or below their maximum
+      if (pool) atomicMin(pool + ((base + j) & (K - 1)), fkey(v * sc_inv));
+    }
   }
-}
-
-// order-preserving float <-> u32 keys for the shared per-query threshold
-__device__ __forceinline__ uint32_t fkey(float f) {
-  const uint32_t b = __float_as_uint(f);
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float fkey_inv(uint32_t k) {
-  if (k >= 0xFF800000u) return INFINITY;   // unset (0xFFFFFFFF) or +inf
-  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
 }
 
 // Work of one database chunk: units (query tile qt, database slice) ordered
@@ -141,7 +147,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               const __grid_constant__ CUtensorMap tm_xlo,
               const uint8_t* __restrict__ xext, TcWork work, int m, int nkb,
               int idx_base, float* __restrict__ cand_s, int* __restrict__ cand_i,
-              unsigned* __restrict__ gthr, const float* __restrict__ f16p) {
+              unsigned* __restrict__ gthr, const float* __restrict__ f16p,
+              unsigned* __restrict__ pool) {
   using Cfg = TcCfg<PASSES, SQ>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -351,6 +358,17 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     };
     TopList<float, KC> L;
     L.init();
+    // per-query pool of K' hashed slots (see insert_masked_acc): its maximum
+    // bounds the K'-th best of everything inserted anywhere.  Read one slot
+    // per tile round-robin; after a full round the running max of the values
+    // read is valid (slots only decrease) and becomes pool_thr.
+    unsigned pk = 0xFFFFFFFFu;
+    float p_max = -INFINITY, pool_thr = INFINITY;
+    int p_slot = 0;
+    auto load_p = [&](int qq, int sl) -> unsigned {
+      return qq < m ? *reinterpret_cast<volatile unsigned*>(pool + (int64_t)qq * KC + sl)
+                    : 0xFFFFFFFFu;
+    };
     int u = blockIdx.x;
     if (u < units) {
       int slice = u / work.qtiles, qt = u - slice * work.qtiles;
@@ -358,11 +376,19 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       int t = work.t0 + slice * work.tps;
       int q = qt * kTcM + row;
       unsigned gk = load_g(q);
+      pk = load_p(q, 0);
       for (int i = 0;; ++i) {
         const int buf = i & 1;
         // candidates must also beat the best K'-th score any list has
-        // published for this query (a valid bound for the union)
-        const float thr_g = q < m ? fkey_inv(gk) * sc_mul : -INFINITY;
+        // published for this query and the pool bound (both valid for the union)
+        p_max = fmaxf(p_max, fkey_inv(pk) * sc_mul);
+        if (++p_slot == KC) {
+          pool_thr = p_max;
+          p_max = -INFINITY;
+          p_slot = 0;
+        }
+        pk = load_p(q, p_slot);
+        const float thr_g = q < m ? fminf(fkey_inv(gk) * sc_mul, pool_thr) : -INFINITY;
         int nu = u, nt = t + 1;
         if (nt >= t1) {
           nu = u + gridDim.x;
@@ -395,7 +421,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               uint32_t mask = 0;
 #pragma unroll
               for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(r[j]) > nthr ? 1u : 0u) << j;
-              insert_masked_acc(L, r, mask, base + (c + h) * 32, thr_g);
+              insert_masked_acc(L, r, mask, base + (c + h) * 32, thr_g,
+                                pool + (int64_t)q * KC, sc_inv);
             }
           }
         }
@@ -421,6 +448,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           qt = u - slice * work.qtiles;
           t1 = min(work.T, work.t0 + slice * work.tps + work.tps);
           q = qt * kTcM + row;
+          p_max = -INFINITY;
+          pool_thr = INFINITY;
+          p_slot = 0;
+          pk = load_p(q, 0);
         }
         t = nt;
       }
@@ -840,7 +871,7 @@ static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtenso
   TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<PASSES, KC, SQ, F16>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   knn_tc_kernel<PASSES, KC, SQ, F16><<<grid, kTcThreads, smem, st>>>(
-      qh, ql, xh, xl, xext, work, (int)m, nkb, idx_base, cs, ci, gthr, f16p);
+      qh, ql, xh, xl, xext, work, (int)m, nkb, idx_base, cs, ci, gthr, f16p, gthr + m);
   TB_LAUNCH_CHECK("knn_tc");
   return TB_OK;
 }
