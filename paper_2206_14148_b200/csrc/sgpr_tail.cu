@@ -280,9 +280,21 @@ tail_gemm_kernel(double* base_c, const double* base_a, const double* base_b, int
   double* Bs = gsm + 2 * kGKc * kGLd;
   const double *A, *B;
   double* C;
-  if (mode == 0) {
+  if (mode == 0 || mode >= 4) {
+    // 0: whole trailing triangle; 4: its first column (j = k + 1) only;
+    // 5: the rest (j >= k + 2), so that the next diagonal tile can be
+    // factored while mode 5 runs (look-ahead)
     int a, b;
-    tri_idx(blockIdx.x, a, b);
+    if (mode == 4) {
+      a = blockIdx.x;
+      b = 0;
+    } else {
+      tri_idx(blockIdx.x, a, b);
+      if (mode == 5) {
+        ++a;
+        ++b;
+      }
+    }
     const int i = k + 1 + a, j = k + 1 + b;
     C = base_c + tslot(i, j) * kTE;
     A = base_a + tslot(i, k) * kTE;
@@ -301,7 +313,7 @@ tail_gemm_kernel(double* base_c, const double* base_a, const double* base_b, int
     A = base_a + (int64_t)k * kTE;          // inverse of diagonal tile k
     B = C;
   }
-  const bool bt = mode == 0 || mode == 2;   // B operand used transposed
+  const bool bt = mode == 0 || mode == 2 || mode >= 4;   // B operand used transposed
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wr = warp >> 2, wc = warp & 3, g = lane >> 2, tg = lane & 3;
   double acc[8][4][2];
@@ -359,7 +371,7 @@ tail_gemm_kernel(double* base_c, const double* base_a, const double* base_b, int
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = wc * 32 + b * 8 + 2 * tg + e;
-        if (mode <= 1) C[(int64_t)c * kTT + r] -= acc[a][b][e];
+        if (mode <= 1 || mode >= 4) C[(int64_t)c * kTT + r] -= acc[a][b][e];
         else C[(int64_t)c * kTT + r] = acc[a][b][e];
       }
   }
@@ -459,18 +471,33 @@ __global__ void scale_copy_kernel(const double* __restrict__ a, int64_t n, int64
 }
 
 // ------------------------------------------------------------------ host --
-static int tail_cholesky(double* base, double* inv, int nt, int* info, cudaStream_t st) {
-  for (int k = 0; k < nt; ++k) {
-    tail_potrf_inv_kernel<<<1, kPThreads, (size_t)kTT * kTLd * 8, st>>>(
-        base, k, inv + (int64_t)k * kTE, info);
-    TB_LAUNCH_CHECK("tail_potrf_inv");
+// Blocked right-looking Cholesky with one step of look-ahead: after the
+// panel of step k, the first trailing column is updated alone, then the
+// diagonal tile k+1 is factored on a high-priority side stream while the rest
+// of the trailing update runs on `st`.
+static int tail_cholesky(double* base, double* inv, int nt, int* info, cudaStream_t st,
+                         cudaStream_t side, cudaEvent_t e_col, cudaEvent_t e_diag) {
+  tail_potrf_inv_kernel<<<1, kPThreads, (size_t)kTT * kTLd * 8, st>>>(base, 0, inv, info);
+  TB_LAUNCH_CHECK("tail_potrf_inv");
+  for (int k = 0; k + 1 < nt; ++k) {
     const int below = nt - k - 1;
-    if (below == 0) break;
+    if (k > 0) TB_CUDA_TRY(cudaStreamWaitEvent(st, e_diag, 0));     // potrf(k) done
     tail_gemm_kernel<<<below, 256, kGSmem, st>>>(base, base, inv, k, nt, 2);       // panel
     TB_LAUNCH_CHECK("tail_panel");
-    tail_gemm_kernel<<<below * (below + 1) / 2, 256, kGSmem, st>>>(base, base, base, k, nt, 0);
-    TB_LAUNCH_CHECK("tail_update");
+    tail_gemm_kernel<<<below, 256, kGSmem, st>>>(base, base, base, k, nt, 4);      // column k+1
+    TB_LAUNCH_CHECK("tail_update_col");
+    TB_CUDA_TRY(cudaEventRecord(e_col, st));
+    TB_CUDA_TRY(cudaStreamWaitEvent(side, e_col, 0));
+    tail_potrf_inv_kernel<<<1, kPThreads, (size_t)kTT * kTLd * 8, side>>>(
+        base, k + 1, inv + (int64_t)(k + 1) * kTE, info);
+    TB_LAUNCH_CHECK("tail_potrf_inv");
+    TB_CUDA_TRY(cudaEventRecord(e_diag, side));
+    if (below > 1) {
+      tail_gemm_kernel<<<below * (below - 1) / 2, 256, kGSmem, st>>>(base, base, base, k, nt, 5);
+      TB_LAUNCH_CHECK("tail_update_rest");
+    }
   }
+  if (nt > 1) TB_CUDA_TRY(cudaStreamWaitEvent(st, e_diag, 0));
   return TB_OK;
 }
 
@@ -533,12 +560,28 @@ int tail_run(int64_t M, int64_t M_pad, const void* Z, int dtype, const KernParam
   // L = chol(Kuu)
   tail_kuu_kernel<<<tiles, 256, 0, st>>>(Zs, M, kp, jitter, 0.0, L);
   TB_LAUNCH_CHECK("tail_kuu");
-  int rc = tail_cholesky(L, invL, nt, info, st);
+  cudaStream_t side = nullptr;
+  cudaEvent_t e_col = nullptr, e_diag = nullptr;
+  int lo_p = 0, hi_p = 0;
+  TB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
+  TB_CUDA_TRY(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi_p));
+  TB_CUDA_TRY(cudaEventCreateWithFlags(&e_col, cudaEventDisableTiming));
+  TB_CUDA_TRY(cudaEventCreateWithFlags(&e_diag, cudaEventDisableTiming));
+  struct Cleanup {
+    cudaStream_t s;
+    cudaEvent_t a, b;
+    ~Cleanup() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      cudaStreamDestroy(s);
+    }
+  } cleanup{side, e_col, e_diag};
+  int rc = tail_cholesky(L, invL, nt, info, st, side, e_col, e_diag);
   if (rc) return rc;
   // P = chol(Kuu + Sigma / s2), in place over Sigma
   tail_kuu_kernel<<<tiles, 256, 0, st>>>(Zs, M, kp, jitter, 1.0 / noise, sigma);
   TB_LAUNCH_CHECK("tail_kuu_add");
-  if ((rc = tail_cholesky(sigma, invP, nt, info, st))) return rc;
+  if ((rc = tail_cholesky(sigma, invP, nt, info, st, side, e_col, e_diag))) return rc;
   // log dets
   tail_reduce_kernel<<<tiles, 256, 0, st>>>(L, 0, part);
   sum_kernel<<<1, 32, 0, st>>>(part, tiles, scal + 0);
