@@ -133,20 +133,22 @@ def test_edge_shapes(n, m, d, k, engines):
         check(dist, idx, ref_d, ref_i, x, q)
 
 
+@pytest.mark.parametrize("engine", ["tc3", "tc1"])
 @pytest.mark.parametrize("n,m,d", [(60000, 300, 784), (20000, 130, 300), (5000, 64, 1000)])
-def test_streamed_query_tc_engine_large_d(n, m, d):
+def test_streamed_query_tc_engine_large_d(n, m, d, engine):
     """d > 128: the tcgen05 engine streams query k-blocks through the ring
-    (C3 is MNIST-shaped, d = 784).  Exact vs the fp64 oracle; no fallback."""
+    (C3 is MNIST-shaped, d = 784), bf16x3 and fp16 single pass.  Exact vs
+    the fp64 oracle; no fallback."""
     x, q = synthetic.gaussian_knn(n, m, d, seed=d)
     ref_d, ref_i = oknn.exact(x, q, 10)
-    op = neighbors.KnnOperator(n, m, d, 10, engine="tc3")
+    op = neighbors.KnnOperator(n, m, d, 10, engine=engine)
     import torch
     dist, idx = op.run(torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda())
     check(dist.cpu().numpy(), idx.cpu().numpy(), ref_d, ref_i, x, q)
     assert op.fallback_count() == 0
     xq, qq = synthetic.quantized_knn(n // 4, m, d, seed=1)      # tie stress
     rd, ri = oknn.exact(xq, qq, 10)
-    dist, idx = tb.knn(xq, qq, 10, engine="tc3")
+    dist, idx = tb.knn(xq, qq, 10, engine=engine)
     check(dist, idx, rd, ri, xq, qq)
 
 
