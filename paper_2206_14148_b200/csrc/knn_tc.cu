@@ -139,7 +139,12 @@ struct TcWork {
 // (f16p = [s, t, alpha, 1/(s t)], knn_kernels.cu rows_f16_kernel), so the
 // accumulator holds s t (2 q.x - ||x||^2): A_ext rows are [alpha x3] and the
 // scores published (thresholds, candidate lists) are unscaled by 1/(s t).
-template <int PASSES, int KC, bool SQ, bool F16>
+// MC: clusters of 2 CTAs on query tiles 2p, 2p+1 of the same database
+// slice; each CTA loads HALF of every database stage (and of the -||x||^2
+// block) and multicasts it to both, halving the L2->SM stream per CTA; a
+// stage is refilled only after both CTAs' MMAs released it (empty/eempty
+// count 2, multicast commits).  Accumulators and epilogues stay per CTA.
+template <int PASSES, int KC, bool SQ, bool F16, bool MC>
 __global__ void __launch_bounds__(kTcThreads, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               const __grid_constant__ CUtensorMap tm_qlo,
@@ -168,7 +173,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(eempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int units = work.qtiles * work.slices;
+  const int rank = MC ? (int)cluster_ctarank() : 0;
+  const int grp = MC ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;     // worker
+  const int ngrp = MC ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int qunits = MC ? (work.qtiles + 1) / 2 : work.qtiles;
+  const int units = qunits * work.slices;
+  auto qtile_of = [&](int uu) { const int qq = uu % qunits; return MC ? 2 * qq + rank : qq; };
 
   // constant A_ext: row r = [1, 1, 1, 0 ... 0] in the interleaved layout
   // (8-row groups of 256 B: k-chunk 0 at +0, k-chunk 1 at +128)
@@ -189,7 +199,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);
     }
     mbar_init(a_full, 1);
     mbar_init(a_empty, 1);
@@ -197,13 +207,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 32 * kTcEpiWarps);
       mbar_init(&efull[b], 1);
-      mbar_init(&eempty[b], 1);
+      mbar_init(&eempty[b], MC ? 2 : 1);
     }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync();           // both CTAs' barriers exist before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -218,8 +229,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       }
       int s = 0, i = 0;
       uint32_t ph = 0, seg = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++seg) {
-        const int slice = u / work.qtiles, qt = u - slice * work.qtiles;
+      for (int u = grp; u < units; u += ngrp, ++seg) {
+        const int slice = u / qunits, qt = qtile_of(u);
         const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
         if (!SQ) {
           mbar_wait(a_empty, (seg & 1) ^ 1);           // previous query tile retired
@@ -236,7 +247,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           const int e = i & 1;
           mbar_wait(&eempty[e], ((i >> 1) & 1) ^ 1);
           mbar_expect_tx(&efull[e], kTcBExt);
-          bulk_load(bext + e * kTcBExt, xext + (size_t)t * kTcBExt, kTcBExt, &efull[e]);
+          if (MC)
+            bulk_load_mc(bext + e * kTcBExt + rank * (kTcBExt / 2),
+                         xext + (size_t)t * kTcBExt + rank * (kTcBExt / 2), kTcBExt / 2,
+                         &efull[e], 3);
+          else
+            bulk_load(bext + e * kTcBExt, xext + (size_t)t * kTcBExt, kTcBExt, &efull[e]);
           for (int kb = 0; kb < nkb; ++kb) {
             if (SQ) {
               // query k-block (hi, lo) into one ring stage
@@ -258,8 +274,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
                 mbar_arrive(&full[s]);
               } else {
                 mbar_expect_tx(&full[s], Cfg::kBBlock);
-                tma_load_2d(b_base + (size_t)s * Cfg::kBBlock, mat ? &tm_xlo : &tm_xhi,
-                            &full[s], kb * kTcKB, t * kTcN);
+                if (MC)
+                  tma_load_2d_mc(b_base + (size_t)s * Cfg::kBBlock + rank * (Cfg::kBBlock / 2),
+                                 mat ? &tm_xlo : &tm_xhi, &full[s], kb * kTcKB,
+                                 t * kTcN + rank * (kTcN / 2), 3);
+                else
+                  tma_load_2d(b_base + (size_t)s * Cfg::kBBlock, mat ? &tm_xlo : &tm_xhi,
+                              &full[s], kb * kTcKB, t * kTcN);
               }
               if (++s == S) {
                 s = 0;
@@ -277,8 +298,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       const uint32_t aext_a = smem_u32(aext);
       int s = 0, i = 0;
       uint32_t ph = 0, seg = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++seg) {
-        const int slice = u / work.qtiles;
+      for (int u = grp; u < units; u += ngrp, ++seg) {
+        const int slice = u / qunits;
         const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
         if (!SQ) {
           mbar_wait(a_full, seg & 1);
@@ -319,7 +340,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               if (PASSES == 3)
                 mma_bf16(d, desc_k_sw128(alo + ko), desc_k_sw128(b0 + ko), idesc, 1);
             }
-            mma_commit(&empty[s]);
+            if (MC) mma_commit_mc(&empty[s], 3); else mma_commit(&empty[s]);
             if (++s == S) {
               s = 0;
               ph ^= 1;
@@ -333,7 +354,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               for (int kk = 0; kk < kTcKB / 16; ++kk)
                 if (!(work.drain_only & 4))
                   mma_bf16(d, desc_k_sw128(ahi + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, 1);
-              mma_commit(&empty[s]);
+              if (MC) mma_commit_mc(&empty[s], 3); else mma_commit(&empty[s]);
               if (++s == S) {
                 s = 0;
                 ph ^= 1;
@@ -341,7 +362,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             }
             if (SQ) mma_commit(&empty[qstage]);   // query k-block consumed
           }
-          mma_commit(&eempty[buf]);  // norm block may be replaced
+          if (MC) mma_commit_mc(&eempty[buf], 3); else mma_commit(&eempty[buf]);  // norm block may be replaced
           mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
         }
         if (!SQ) mma_commit(a_empty);         // query tile may be replaced
@@ -369,9 +390,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       return qq < m ? *reinterpret_cast<volatile unsigned*>(pool + (int64_t)qq * KC + sl)
                     : 0xFFFFFFFFu;
     };
-    int u = blockIdx.x;
+    int u = grp;
     if (u < units) {
-      int slice = u / work.qtiles, qt = u - slice * work.qtiles;
+      int slice = u / qunits, qt = qtile_of(u);
       int t1 = min(work.T, work.t0 + slice * work.tps + work.tps);
       int t = work.t0 + slice * work.tps;
       int q = qt * kTcM + row;
@@ -391,11 +412,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         const float thr_g = q < m ? fminf(fkey_inv(gk) * sc_mul, pool_thr) : -INFINITY;
         int nu = u, nt = t + 1;
         if (nt >= t1) {
-          nu = u + gridDim.x;
-          nt = work.t0 + (nu / work.qtiles) * work.tps;
+          nu = u + ngrp;
+          nt = work.t0 + (nu / qunits) * work.tps;
         }
         const bool more = nu < units;
-        if (more) gk = load_g((nu - (nu / work.qtiles) * work.qtiles) * kTcM + row);
+        if (more) gk = load_g(qtile_of(nu) * kTcM + row);
         mbar_wait(&tfull[buf], (i >> 1) & 1);
         tc_fence_after();
         const uint32_t taddr =
@@ -444,8 +465,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           L.init();
           if (!more) break;
           u = nu;
-          slice = u / work.qtiles;
-          qt = u - slice * work.qtiles;
+          slice = u / qunits;
+          qt = qtile_of(u);
           t1 = min(work.T, work.t0 + slice * work.tps + work.tps);
           q = qt * kTcM + row;
           p_max = -INFINITY;
@@ -459,6 +480,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   }
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync();           // no multicast or remote arrive targets an exited CTA
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
@@ -779,6 +801,15 @@ static bool tc_pair_on(int passes, int64_t d_pad, int64_t m) {
   return passes == 3 && d_pad <= kTcMaxDpad && m > kTcM;
 }
 
+// Multicast clusters (MC kernel) for engine tc1 with resident queries, the
+// default (C2 on one box: 3.24 vs 3.21 M q/s, engine 2.80 vs 2.82 ms);
+// TB_TC_MC=0 selects the 1-CTA kernel (A/B timing).
+static bool tc_mc_on(int passes, int64_t d_pad, int64_t m) {
+  const char* e = std::getenv("TB_TC_MC");
+  if (e && *e == '0') return false;
+  return passes == 1 && d_pad <= kTcMaxDpad && m > kTcM;
+}
+
 // units are (query tile, slice) - or (query-tile pair, slice) on `sms`/2
 // CTA pairs in pair mode
 static void tc_schedule(int64_t m, int64_t rows_pad, int sms, bool pair, TcWork* seed,
@@ -813,7 +844,8 @@ static void tc_schedule(int64_t m, int64_t rows_pad, int sms, bool pair, TcWork*
 
 int tc_lists(int64_t m, int64_t rows_pad, int sms, int passes, int64_t d_pad) {
   TcWork a, b;
-  tc_schedule(m, rows_pad, sms, tc_pair_on(passes, d_pad, m), &a, &b);
+  tc_schedule(m, rows_pad, sms, tc_pair_on(passes, d_pad, m) || tc_mc_on(passes, d_pad, m), &a,
+              &b);
   return 2 + 2 * b.slices;
 }
 
@@ -865,13 +897,32 @@ template <int PASSES, int KC, bool SQ>
 static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtensorMap& xh,
                      const CUtensorMap& xl, const uint8_t* xext, TcWork work,
                      int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
-                     unsigned* gthr, const float* f16p, cudaStream_t st) {
+                     unsigned* gthr, const float* f16p, bool mc, cudaStream_t st) {
   constexpr bool F16 = PASSES == 1;            // engine tc1 is the fp16 single pass
   const size_t smem = TcCfg<PASSES, SQ>::smem_bytes(nkb);
-  TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<PASSES, KC, SQ, F16>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  knn_tc_kernel<PASSES, KC, SQ, F16><<<grid, kTcThreads, smem, st>>>(
-      qh, ql, xh, xl, xext, work, (int)m, nkb, idx_base, cs, ci, gthr, f16p, gthr + m);
+  if (!SQ && F16 && mc) {
+    auto kern = knn_tc_kernel<PASSES, KC, false, F16, true>;
+    TB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, qh, ql, xh, xl, xext, work, (int)m, nkb, idx_base,
+                                   cs, ci, gthr, f16p, gthr + m));
+  } else {
+    TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<PASSES, KC, SQ, F16, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    knn_tc_kernel<PASSES, KC, SQ, F16, false><<<grid, kTcThreads, smem, st>>>(
+        qh, ql, xh, xl, xext, work, (int)m, nkb, idx_base, cs, ci, gthr, f16p, gthr + m);
+  }
   TB_LAUNCH_CHECK("knn_tc");
   return TB_OK;
 }
@@ -879,7 +930,7 @@ static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtenso
 int tc_dispatch(int passes, int cand, const CUtensorMap& mqh, const CUtensorMap& mql,
                 const CUtensorMap& mxh, const CUtensorMap& mxl, const uint8_t* xext,
                 TcWork work, int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
-                unsigned* gthr, const float* f16p, cudaStream_t st);
+                unsigned* gthr, const float* f16p, bool mc, cudaStream_t st);
 
 int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfloat16* xlo,
                   const __nv_bfloat16* qhi, const __nv_bfloat16* qlo, const uint8_t* xext,
@@ -899,8 +950,9 @@ int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfl
   if ((rc = make_map(&mxh, xhi, rows_pad, d_pad, kTcN, f16))) return rc;
   if ((rc = make_map(&mxl, passes == 3 ? xlo : xhi, rows_pad, d_pad, kTcN, f16))) return rc;
   const bool pair = tc_pair_on(passes, d_pad, m);
+  const bool mc = !pair && tc_mc_on(passes, d_pad, m);
   TcWork seed, work;
-  tc_schedule(m, rows_pad, 148, pair, &seed, &work);   // the plan's schedule (148 SMs)
+  tc_schedule(m, rows_pad, 148, pair || mc, &seed, &work);   // the plan's schedule (148 SMs)
   if (2 + 2 * work.slices > lists)
     return fail(TB_ERR_ARG, "tcgen05 engine: candidate buffer smaller than the schedule needs");
   const int nkb = (int)(d_pad / kTcKB);
@@ -918,25 +970,36 @@ int launch_knn_tc(int passes, int cand, const __nv_bfloat16* xhi, const __nv_bfl
                             2 * std::min(qp * work.slices, sms / 2), m, nkb, idx_base, cs, ci,
                             gthr, st);
   }
+  if (mc) {
+    // each CTA of a cluster loads (and multicasts) 128 of a tile's 256 rows
+    if ((rc = make_map(&mxh, xhi, rows_pad, d_pad, kTcM, f16))) return rc;
+    const int qp = (seed.qtiles + 1) / 2;
+    rc = tc_dispatch(passes, cand, mqh, mql, mxh, mxh, xext, seed, 2 * std::min(qp, sms / 2), m,
+                     nkb, idx_base, cs, ci, gthr, f16p, true, st);
+    if (rc || work.slices == 0) return rc;
+    return tc_dispatch(passes, cand, mqh, mql, mxh, mxh, xext, work,
+                       2 * std::min(qp * work.slices, sms / 2), m, nkb, idx_base, cs, ci, gthr,
+                       f16p, true, st);
+  }
   // every list slot the merge reads must be written: unused ones stay INF
   rc = tc_dispatch(passes, cand, mqh, mql, mxh, mxl, xext, seed, std::min(seed.qtiles, sms),
-                   m, nkb, idx_base, cs, ci, gthr, f16p, st);
+                   m, nkb, idx_base, cs, ci, gthr, f16p, false, st);
   if (rc || work.slices == 0) return rc;
   return tc_dispatch(passes, cand, mqh, mql, mxh, mxl, xext, work,
                      std::min(work.qtiles * work.slices, sms), m, nkb, idx_base, cs, ci, gthr,
-                     f16p, st);
+                     f16p, false, st);
 }
 
 int tc_dispatch(int passes, int cand, const CUtensorMap& mqh, const CUtensorMap& mql,
                 const CUtensorMap& mxh, const CUtensorMap& mxl, const uint8_t* xext,
                 TcWork work, int grid, int64_t m, int nkb, int idx_base, float* cs, int* ci,
-                unsigned* gthr, const float* f16p, cudaStream_t st) {
+                unsigned* gthr, const float* f16p, bool mc, cudaStream_t st) {
 #define TB_TC(P, KC)                                                                       \
   return nkb * kTcKB > kTcMaxDpad                                                          \
              ? tc_launch<P, KC, true>(mqh, mql, mxh, mxl, xext, work, grid, m, nkb, idx_base, \
-                                      cs, ci, gthr, f16p, st)                                \
+                                      cs, ci, gthr, f16p, mc, st)                            \
              : tc_launch<P, KC, false>(mqh, mql, mxh, mxl, xext, work, grid, m, nkb, idx_base, \
-                                       cs, ci, gthr, f16p, st)
+                                       cs, ci, gthr, f16p, mc, st)
   if (passes == 3) {
     if (cand == 16) TB_TC(3, 16);
     if (cand == 32) TB_TC(3, 32);

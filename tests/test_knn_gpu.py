@@ -166,6 +166,20 @@ def test_cta_pair_tc_kernel(n, m, d, monkeypatch):
     assert op.fallback_count() == 0
 
 
+@pytest.mark.parametrize("n,m,d", [(70000, 300, 128), (9000, 129, 17)])
+def test_single_cta_tc1_kernel(n, m, d, monkeypatch):
+    """tc1 defaults to multicast clusters of 2 CTAs; TB_TC_MC=0 selects the
+    1-CTA kernel, which must give the same exact answers."""
+    monkeypatch.setenv("TB_TC_MC", "0")
+    x, q = synthetic.gaussian_knn(n, m, d, seed=n + 3 * d)
+    ref_d, ref_i = oknn.exact(x, q, 10)
+    op = neighbors.KnnOperator(n, m, d, 10, engine="tc1")
+    import torch
+    dist, idx = op.run(torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda())
+    check(dist.cpu().numpy(), idx.cpu().numpy(), ref_d, ref_i, x, q)
+    assert op.fallback_count() == 0
+
+
 @pytest.mark.parametrize("scale", [1e5, 1e3, 1e-4, 3e-9])
 def test_fp16_engine_scaling_is_exact(scale):
     """Engine tc1 (fp16 single pass) scales operands by powers of two into
