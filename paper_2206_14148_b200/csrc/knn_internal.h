@@ -30,7 +30,7 @@ enum KnnSlot {
 // stats (u32[64]): [0] max ||x|| bits, [1] fallback count, [2] max ||x - fp16 x||
 // bits, [3] max |q| bits, [4] max |x| bits of the current chunk, [5] the
 // chunk's max ||x - fp16 x||, [kF16Slot..+3] fp16 engine scales (floats:
-// s, t, alpha, 1/(s t)), [12] redo flag of the chunk conversion
+// s, t, alpha, 1/(s t)), [12] redo flag of the chunk conversion, [13] max 1/t
 constexpr int kF16Slot = 8;
 
 struct KnnDims {

@@ -287,6 +287,7 @@ __global__ void f16_scales_kernel(unsigned* __restrict__ stats, int64_t d, int w
   sc[2] = (float)a;
   sc[3] = (float)(1.0 / (s * (double)t));
   stats[12] = redo;
+  atomicMax(stats + 13, __float_as_uint(1.f / t));   // max 1/t over chunks (refine)
   if (redo) stats[5] = 0u;                 // the chunk's residual max is redone
 }
 
@@ -901,13 +902,27 @@ __global__ void knn_refine_kernel(const float* __restrict__ cs,
       if (MET == TB_METRIC_L1) {
         ok = (double)tstar / (1.0 + c1) - c2 * ((double)qnorm[r] + X) > kth;
       } else {
-        double E = c1 * (double)qnorm[r] * X + c2 * X * X;
+        // Norm split (l2): every row with ||x|| > R >= ||q|| has exact score
+        // ||x||^2 - 2 q.x >= R^2 - 2 ||q|| R, which exceeds the k-th exact
+        // score kth - ||q||^2 once R > ||q|| + sqrt(kth); only rows with
+        // ||x|| <= R need the rounding bound, evaluated at R instead of the
+        // largest norm in the database (outliers no longer widen E).
+        const double qn = (double)qnorm[r];
+        double R = X;
+        if (MET == TB_METRIC_L2) {
+          const double Rq = (qn + sqrt(fmax(kth, 0.0))) * (1.0 + 1e-9);
+          if (Rq < X) R = Rq;
+        }
+        double E = c1 * qn * R + c2 * R * R;
         if (qln) {
           // fp16 single pass: measured rounding residuals (Cauchy-Schwarz),
-          // |q.x - q'.x'| <= ||q|| XL + ||ql|| (X + 3 XL), times 2 for -2 q.x
-          const double XL = (double)__uint_as_float(stats[2]);
-          E += 2.0 * (1.0 + 1e-6) *
-               ((double)qnorm[r] * XL + (double)qln[r] * (X + 3.0 * XL));
+          // |q.x - q'.x'| <= ||q|| XL + ||ql|| (R + 3 XL), times 2 for -2 q.x;
+          // rows with ||x|| <= R have ||xl|| <= 2^-11 ||x|| + sqrt(d) 2^-25 / t
+          double XL = (double)__uint_as_float(stats[2]);
+          if (R < X)
+            XL = fmin(XL, (0x1p-11 * R + sqrt((double)d) * 0x1p-25 *
+                                             (double)__uint_as_float(stats[13])) * (1.0 + 1e-6));
+          E += 2.0 * (1.0 + 1e-6) * (qn * XL + (double)qln[r] * (R + 3.0 * XL));
         }
         const double exact_score_k = MET == TB_METRIC_COSINE ? 2.0 * kth - 1.0 : kth - qn64[r];
         ok = (double)tstar - E > exact_score_k;
