@@ -173,7 +173,8 @@ int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int32_t me
            : 2 * (int64_t)slices;
     plan->off[kQn64] = c.take(m * 8);
     plan->off[kQnorm] = c.take(m * 4);
-    plan->off[kStats] = c.take(256);
+    // counters | tc1 centring mean [d] + per-block partials [64][d + 1]
+    plan->off[kStats] = c.take(256 + 8 * (plan->d_pad + 64 * (plan->d_pad + 1)));
     plan->off[kFbList] = c.take(m * 4);
     plan->off[kXn] = c.take(chunk_pad * 4);
     plan->off[kCandS] = c.take(lists * m * cand * 4);
@@ -342,11 +343,20 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
   const bool f16 = p->engine == TB_ENGINE_TC1;
   float* qln = f16 ? (float*)at(kQln) : nullptr;
   const float* f16p = f16 ? reinterpret_cast<const float*>(stats + kF16Slot) : nullptr;
-  int rc = f16 ? launch_query_prep_f16(p->dtype, p->metric, q, p->m, p->d, qn64, qnorm, qln,
+  int rc = TB_OK;
+  // the query prep of tc1 follows the centring decision, which reads the
+  // first database rows: it runs once chunk 0 is on the device
+  auto query_prep = [&]() -> int {
+    if (f16 && p->metric == TB_METRIC_L2) {
+      const int64_t rows0 = std::min(p->chunk_rows, p->n);
+      int r0 = launch_f16_center(p->dtype, x, rows0, p->d, stats, st);
+      if (r0) return r0;
+    }
+    return f16 ? launch_query_prep_f16(p->dtype, p->metric, q, p->m, p->d, qn64, qnorm, qln,
                                        stats, (__half*)qhi, p->m_pad, p->d_pad, st)
                : launch_query_prep(p->dtype, p->metric, q, p->m, p->d, qn64, qnorm, qhi, qlo,
                                    p->m_pad, p->d_pad, st);
-  if (rc) return rc;
+  };
 
   const float* prev_s = nullptr;
   const int* prev_i = nullptr;
@@ -357,6 +367,7 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
     const int64_t rows_pad = round_up(rows, tile_rows);
     const char* xc = (const char*)x + c0 * p->d * es;
     if (ready && c < n_ready) TB_CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)ready[c], 0));
+    if (c == 0 && (rc = query_prep())) return rc;
     rc = f16 ? launch_db_prep_f16(p->dtype, p->metric, xc, rows, p->d, xn, stats,
                                   (__half*)xhi, rows_pad, p->d_pad, xext, st)
              : launch_db_prep(p->dtype, p->metric, xc, rows, p->d, xn, stats, xhi, xlo,

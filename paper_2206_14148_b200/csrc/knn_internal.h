@@ -30,7 +30,8 @@ enum KnnSlot {
 // stats (u32[64]): [0] max ||x|| bits, [1] fallback count, [2] max ||x - fp16 x||
 // bits, [3] max |q| bits, [4] max |x| bits of the current chunk, [5] the
 // chunk's max ||x - fp16 x||, [kF16Slot..+3] fp16 engine scales (floats:
-// s, t, alpha, 1/(s t)), [12] redo flag of the chunk conversion, [13] max 1/t
+// s, t, alpha, 1/(s t)), [12] redo flag of the chunk conversion, [13] max 1/t,
+// [14] centring flag, [15] max |mu|; words 64.. hold mu (fp64 [d]) for tc1
 constexpr int kF16Slot = 8;
 
 struct KnnDims {
@@ -51,6 +52,10 @@ int launch_db_prep(int dtype, int metric, const void* x, int64_t rows, int64_t d
 int launch_query_prep_f16(int dtype, int metric, const void* q, int64_t m, int64_t d,
                           double* qn64, float* qnorm, float* qln, unsigned* stats,
                           __half* qhi, int64_t m_pad, int64_t d_pad, cudaStream_t st);
+// l2 + tc1: sample mean of the first rows of x and the centring decision
+// (stats[14], mu as fp64 at stats + 64 words, max |mu| in stats[15])
+int launch_f16_center(int dtype, const void* x, int64_t rows, int64_t d, unsigned* stats,
+                      cudaStream_t st);
 int launch_db_prep_f16(int dtype, int metric, const void* x, int64_t rows, int64_t d,
                        float* xn, unsigned* stats, __half* xhi, int64_t rows_pad,
                        int64_t d_pad, uint8_t* xext, cudaStream_t st);

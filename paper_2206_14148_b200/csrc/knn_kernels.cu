@@ -264,7 +264,8 @@ __global__ void f16_scales_kernel(unsigned* __restrict__ stats, int64_t d, int w
                                   int metric) {
   float* sc = reinterpret_cast<float*>(stats + kF16Slot);
   if (which == 0) {
-    const float qm = metric == TB_METRIC_COSINE ? 1.f : __uint_as_float(stats[3]);
+    float qm = metric == TB_METRIC_COSINE ? 1.f : __uint_as_float(stats[3]);
+    if (metric != TB_METRIC_COSINE && stats[14]) qm += __uint_as_float(stats[15]);   // |q - mu|
     // |2 s q| <= 256; s, t in [2^-60, 2^60] keep 1/(s t) a normal float
     sc[0] = qm > 0.f ? fminf(fmaxf(pow2_floor(128.f / qm), 0x1p-60f), 0x1p60f) : 1.f;
     return;
@@ -299,7 +300,7 @@ __global__ void f16_scales_kernel(unsigned* __restrict__ stats, int64_t d, int w
 // a power of two, so x t and fp16(x t) / t are exact and x - fp16(x t) / t
 // is exact (Sterbenz); the residual norm is summed in fp32 and rounded up by
 // (1 + (d + 2) 2^-23) so it stays an upper bound.
-template <typename T, int G, bool NORM, int MODE>
+template <typename T, int G, bool NORM, int MODE, bool CENTRED>
 __global__ void __launch_bounds__(256)
 rows_f16_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
                 double* __restrict__ n64, float* __restrict__ n32, float* __restrict__ norm32,
@@ -311,7 +312,14 @@ rows_f16_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
   const float mulf = MODE == 0 ? 2.f * sc[0] : MODE == 1 ? 1.f : sc[1];
   const double mul = mulf, imul = 1.0 / (double)mulf;       // powers of two: exact
   const float imulf = 1.f / mulf;
-  constexpr bool FAST = sizeof(T) == 4 && !NORM;
+  // centred rows (l2 only, translation invariant): x - mu, q - mu with the
+  // sample mean mu chosen by f16_center_kernel; fp64 path then
+  // both variants are launched; the one that does not match the device-side
+  // centring decision exits at once
+  if (!NORM && (*reinterpret_cast<volatile unsigned*>(stats + 14) != 0u) != CENTRED) return;
+  constexpr bool centred = CENTRED && !NORM;
+  const double* mu = reinterpret_cast<const double*>(stats + 64);
+  constexpr bool FAST = sizeof(T) == 4 && !NORM && !centred;
   // grid-stride over rows (the stride keeps a row's G lanes in one warp)
   float nrm = 0.f, res = 0.f, amax = 0.f;
   const int64_t total = rows_pad * G;
@@ -349,6 +357,10 @@ rows_f16_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
         f[j] = (float)v[j];
       }
     }
+    if (centred && r >= rows) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = c0 + j < d ? mu[c0 + j] : 0.0;   // u = 0 on padding
+    }
     __align__(16) __half h[8];
     if (FAST) {
 #pragma unroll
@@ -363,7 +375,7 @@ rows_f16_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const double u = NORM ? v[j] * inv : v[j];
+        const double u = NORM ? v[j] * inv : (centred && c0 + j < d ? v[j] - mu[c0 + j] : v[j]);
         acc = fma(u, u, acc);
         amax = fmaxf(amax, __double2float_ru(fabs(u)));
         h[j] = __double2half(mul * u);
@@ -458,8 +470,13 @@ static void f16_rows_launch(const void* src, int64_t rows, int64_t d, double* n6
   const int G = d_pad == 64 ? 8 : d_pad == 128 ? 16 : 32;
   const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(rows_pad * G, 256), 148 * 8);
 #define TB_F16(GG, NN)                                                                   \
-  rows_f16_kernel<T, GG, NN, MODE><<<blocks, 256, 0, st>>>(                              \
-      (const T*)src, rows, d, n64, n32, norm32, resid, stats, hi, rows_pad, d_pad)
+  do {                                                                                     \
+    rows_f16_kernel<T, GG, NN, MODE, false><<<blocks, 256, 0, st>>>(                       \
+        (const T*)src, rows, d, n64, n32, norm32, resid, stats, hi, rows_pad, d_pad);      \
+    if (!NN)                                                                               \
+      rows_f16_kernel<T, GG, false, MODE, true><<<blocks, 256, 0, st>>>(                   \
+          (const T*)src, rows, d, n64, n32, norm32, resid, stats, hi, rows_pad, d_pad);    \
+  } while (0)
   if (G == 8) {
     if (norm) TB_F16(8, true); else TB_F16(8, false);
   } else if (G == 16) {
@@ -468,6 +485,103 @@ static void f16_rows_launch(const void* src, int64_t rows, int64_t d, double* n6
     if (norm) TB_F16(32, true); else TB_F16(32, false);
   }
 #undef TB_F16
+}
+
+// Sample mean of the first S database rows and the decision to centre
+// (one block): centre when ||mu||^2 exceeds half the mean ||x - mu||^2 of the
+// sample, i.e. when a common offset would dominate the norms that scale the
+// certified rounding bound.  mu is stored as fp64 at stats + 64 words.
+constexpr int kCenterBlocks = 64, kCenterRows = 32;       // sample = 2048 rows
+// stage 1: block b sums rows [b*128, b*128+128) of the sample per column
+// (coalesced) and the squared norms; partials at stats + 64 + 2 d words
+template <typename T>
+__global__ void __launch_bounds__(1024)
+f16_center_partial_kernel(const T* __restrict__ x, int64_t S, int64_t d,
+                          unsigned* __restrict__ stats) {
+  double* part = reinterpret_cast<double*>(stats + 64) + d;      // [kCenterBlocks][d + 1]
+  __shared__ double colsum[1024];
+  __shared__ double sq;
+  const int tid = threadIdx.x;
+  const int P = (int)blockDim.x / (int)d;
+  const int c = tid % (int)d, lp = tid / (int)d;
+  if (tid == 0) sq = 0.0;
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * kCenterRows;
+  const int64_t r1 = std::min<int64_t>(S, r0 + kCenterRows);
+  double sx = 0.0, sxx = 0.0;
+  if (lp < P)
+    for (int64_t r = r0 + lp; r < r1; r += P) {
+      const double v = (double)x[r * d + c];
+      sx += v;
+      sxx = fma(v, v, sxx);
+    }
+  colsum[tid] = lp < P ? sx : 0.0;
+  const double wsq = warp_sum(lp < P ? sxx : 0.0);        // one shared atomic per warp
+  if ((tid & 31) == 0) atomicAdd(&sq, wsq);
+  __syncthreads();
+  if (tid < d) {
+    double a = 0.0;
+    for (int pp = 0; pp < P; ++pp) a += colsum[pp * d + tid];
+    part[blockIdx.x * (d + 1) + tid] = a;
+  }
+  if (tid == 0) part[blockIdx.x * (d + 1) + d] = sq;
+}
+
+// stage 2 (one block): fixed-order combination -> mu, ||mu||^2, mean
+// ||x - mu||^2 over the sample, the centring decision and max |mu|
+__global__ void __launch_bounds__(1024)
+f16_center_final_kernel(int64_t S, int64_t d, int nb, unsigned* __restrict__ stats) {
+  double* mu = reinterpret_cast<double*>(stats + 64);
+  const double* part = mu + d;
+  __shared__ double red[2];
+  __shared__ double acc[1024];
+  const int tid = threadIdx.x;
+  const int P = (int)blockDim.x / (int)d;
+  const int c = tid % (int)d, lp = tid / (int)d;
+  if (tid == 0) red[0] = red[1] = 0.0;
+  double a = 0.0;
+  if (lp < P)
+    for (int bb = lp; bb < nb; bb += P) a += part[bb * (d + 1) + c];   // fixed order
+  acc[tid] = a;
+  __syncthreads();
+  double mm = 0.0;
+  float am = 0.f;
+  if (tid < d) {
+    double t = 0.0;
+    for (int pp = 0; pp < P; ++pp) t += acc[pp * d + tid];
+    t /= (double)S;
+    mu[tid] = t;
+    mm = t * t;
+    am = __double2float_ru(fabs(t));
+  }
+  mm = warp_sum(mm);
+  for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+  if ((tid & 31) == 0) {
+    atomicAdd(&red[0], mm);
+    atomicMax(stats + 15, __float_as_uint(am));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double sq = 0.0;
+    for (int bb = 0; bb < nb; ++bb) sq += part[bb * (d + 1) + d];
+    const double spread = sq / (double)S - red[0];        // mean ||x_r - mu||^2
+    stats[14] = red[0] > 0.5 * spread ? 1u : 0u;
+  }
+}
+
+int launch_f16_center(int dtype, const void* x, int64_t rows, int64_t d, unsigned* stats,
+                      cudaStream_t st) {
+  const int64_t S = std::min<int64_t>(rows, (int64_t)kCenterBlocks * kCenterRows);
+  if (S <= 0 || d > 1024) return TB_OK;
+  const unsigned threads = (unsigned)(1024 / d * d);
+  const int nb = (int)ceil_div(S, kCenterRows);
+  if (dtype == TB_F32)
+    f16_center_partial_kernel<float><<<nb, threads, 0, st>>>((const float*)x, S, d, stats);
+  else
+    f16_center_partial_kernel<double><<<nb, threads, 0, st>>>((const double*)x, S, d, stats);
+  f16_center_final_kernel<<<1, threads, 0, st>>>(S, d, nb, stats);
+  TB_LAUNCH_CHECK("f16_center");
+  return TB_OK;
 }
 
 template <typename T>

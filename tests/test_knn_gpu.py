@@ -180,6 +180,24 @@ def test_single_cta_tc1_kernel(n, m, d, monkeypatch):
     assert op.fallback_count() == 0
 
 
+@pytest.mark.parametrize("offset,tail", [(100.0, False), (0.5, False), (0.0, True)])
+def test_fp16_engine_offset_and_heavy_tail_data(offset, tail):
+    """tc1 centres l2 data with a large common offset on the sample mean
+    (distances are translation invariant), and the norm-split certification
+    keeps heavy-tailed outliers from widening every query's bound: exact,
+    and (almost) no query needs the brute-force fallback."""
+    import torch
+    rng = np.random.default_rng(7)
+    a = rng.standard_cauchy((30300, 48)).clip(-1e4, 1e4) if tail else \
+        rng.standard_normal((30300, 48)) + offset
+    x, q = a[:30000].astype(np.float32), a[30000:].astype(np.float32)
+    ref_d, ref_i = oknn.exact(x, q, 10)
+    op = neighbors.KnnOperator(30000, 300, 48, 10, engine="tc1")
+    dist, idx = op.run(torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda())
+    check(dist.cpu().numpy(), idx.cpu().numpy(), ref_d, ref_i, x, q)
+    assert op.fallback_count() <= 3
+
+
 @pytest.mark.parametrize("scale", [1e5, 1e3, 1e-4, 3e-9])
 def test_fp16_engine_scaling_is_exact(scale):
     """Engine tc1 (fp16 single pass) scales operands by powers of two into
