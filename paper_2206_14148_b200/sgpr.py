@@ -260,9 +260,13 @@ class SGPR:
         likelihood noise variance and the inducing points Z (the quantities
         GPflow trains; values are w.r.t. the constrained parameters).
 
-        The O(M^3) tail is differentiated with torch autograd (fp64, cuSOLVER /
-        cuBLAS, like the tail itself); it yields G = dELBO/dSigma and
-        g = dELBO/dv.  The data then enter only through
+        The O(M^3) tail is differentiated analytically on dense fp64
+        matrices (cuSOLVER Cholesky / inverse, cuBLAS; at most ~4 M x M live):
+        with A = Kuu + Sigma / s2 and w = A^-1 v / s2, G = dELBO/dSigma =
+        (Kuu^-1 - A^-1 - w w^T) / (2 s2), g = dELBO/dv = w / s2,
+        dELBO/dKuu = s2 G - Kuu^-1 Sigma Kuu^-1 / (2 s2), plus the explicit
+        noise and variance terms; dELBO/dKuu is contracted with the kernel
+        derivatives by ``tb_sgpr_kuf_grad`` over Z x Z.  The data then enter only through
         W = 2 G Kuf + g y^T, streamed over N in chunks: W by one fp64 GEMM
         (cuBLAS) and the reduction against the kernel derivatives by the
         fused kernel ``tb_sgpr_kuf_grad``.  Multi-GPU: the chunk sums are
@@ -276,54 +280,93 @@ class SGPR:
             if need > limit:
                 raise BudgetExceeded(
                     "sgpr_elbo_and_grads", need, resident,
-                    message=f"sgpr_elbo_and_grads: the dense fp64 autograd tail needs "
+                    message=f"sgpr_elbo_and_grads: the dense fp64 gradient tail needs "
                             f"~{need / 1e9:.2f} GB at M={M} (N-independent), over "
                             f"memory_limit={limit}; the ELBO alone (elbo()) stays in budget")
         s = self._stats if self._stats is not None and self._stats.Sigma is not None \
             else self.statistics()
         f64 = torch.float64
         dev = self.device
-        Zd = self.Z.to(f64).detach().requires_grad_()
-        var = torch.tensor(self.variance, dtype=f64, device=dev, requires_grad=True)
-        ls = torch.tensor(self.lengthscales, dtype=f64, device=dev, requires_grad=True)
-        s2 = torch.tensor(self.noise_variance, dtype=f64, device=dev, requires_grad=True)
-        Sigma = s.full_sigma().detach().requires_grad_()
-        v = s.v.detach().requires_grad_()
-        Kuu = _torch_kernel(Zd, Zd, self.kernel, var, ls)
-        Kuu = Kuu + self.jitter * torch.eye(M, dtype=f64, device=dev)
-        elbo = _elbo_torch(Sigma, v, s.yy, s.N, Kuu, s2, var)
-        elbo.backward()
-        G = 0.5 * (Sigma.grad + Sigma.grad.mT)
-        g = v.grad
-        del Sigma, Kuu
-        grad_hyp = torch.zeros(1 + dim, dtype=f64, device=dev)
-        grad_z = torch.zeros((M, dim), dtype=f64, device=dev)
+        N, s2, var = float(s.N), self.noise_variance, self.variance
         lib = _lib.load()
-        ws = torch.empty(max(int(lib.tb_sgpr_kuf_grad_workspace(chunk_n, M, dim)), 1),
-                         dtype=torch.uint8, device=dev)
         st = torch.cuda.current_stream(dev)
         dt = _lib.TB_F32 if self.X.dtype == torch.float32 else _lib.TB_F64
-        G2 = 2.0 * G
+        lsp = self.lengthscales.ctypes.data_as(ctypes.c_void_p)
+        # --- the O(M^3) tail, differentiated analytically (A = Kuu + Sigma/s2,
+        # w = A^-1 v / s2), dense fp64, in place
+        Sig = s.full_sigma()
+        v = s.v
+        Kuu = kernel_matrix(self.Z, self.Z, self.kernel, var, self.lengthscales)
+        Kuu.diagonal().add_(self.jitter)
+        L = torch.linalg.cholesky(Kuu)
+        Kuu.add_(Sig, alpha=1.0 / s2)                          # A, in place
+        P = torch.linalg.cholesky(Kuu)
+        del Kuu
+        logdet_k = 2.0 * float(torch.log(L.diagonal()).sum())
+        logdet_a = 2.0 * float(torch.log(P.diagonal()).sum())
+        Kinv = torch.cholesky_inverse(L)
+        del L
+        Ainv = torch.cholesky_inverse(P)
+        del P
+        w = Ainv @ v / s2
+        vw = float(v @ w)                                      # v^T A^-1 v / s2
+        tr_ks = float((Kinv * Sig).sum())                      # tr(Kuu^-1 Sigma)
+        tr_as = float((Ainv * Sig).sum())                      # tr(A^-1 Sigma)
+        wsw = float(w @ (Sig @ w))
+        elbo = (-0.5 * N * LOG2PI - 0.5 * (logdet_a - logdet_k) - 0.5 * N * math.log(s2)
+                - 0.5 * s.yy / s2 + 0.5 * vw / s2 - 0.5 * N * var / s2 + 0.5 * tr_ks / s2)
+        d_s2 = (0.5 * tr_as / s2**2 + 0.5 * wsw / s2**2 - vw / s2**2 - 0.5 * N / s2
+                + 0.5 * s.yy / s2**2 + 0.5 * N * var / s2**2 - 0.5 * tr_ks / s2**2)
+        T = Kinv @ Sig
+        del Sig
+        H = T @ Kinv                                           # Kuu^-1 Sigma Kuu^-1
+        del T
+        Gm = Kinv.sub_(Ainv).addr_(w, w, alpha=-1.0)           # Kuu^-1 - A^-1 - w w^T
+        del Ainv
+        # dELBO/dKuu = Gm / 2 - Kuu^-1 Sigma Kuu^-1 / (2 s2)
+        H.mul_(-0.5 / s2).add_(Gm, alpha=0.5)
+        g = w / s2                                             # dELBO/dv
+        G2 = Gm.div_(s2)                                       # 2 G, G = dELBO/dSigma
+        # --- Kuu side: sum_ij H_ij dk(z_i, z_j) (both arguments for Z)
+        grad_hyp_k = torch.zeros(1 + dim, dtype=f64, device=dev)
+        grad_z_k = torch.zeros((M, dim), dtype=f64, device=dev)
+        K0 = kernel_matrix(self.Z, self.Z, self.kernel, var, self.lengthscales)
+        H.mul_(2.0)
+        wsk = torch.empty(max(int(lib.tb_sgpr_kuf_grad_workspace(M, M, dim)), 1),
+                          dtype=torch.uint8, device=dev)
+        rc = lib.tb_sgpr_kuf_grad(self.Z.data_ptr(), self.Z.data_ptr(), H.data_ptr(),
+                                  K0.data_ptr(), M, M, dim, _lib.KERNELS[self.kernel], dt, var,
+                                  lsp, grad_hyp_k.data_ptr(), grad_z_k.data_ptr(), wsk.data_ptr(),
+                                  wsk.numel(), st.cuda_stream)
+        _lib.check(rc, "sgpr_kuf_grad(Kuu)")
+        del H, K0, wsk
+        grad_hyp_k.mul_(0.5)                                   # W = 2H doubled the hyp sums
+        # --- data side, streamed over N: W = 2 G Kuf + g y^T
+        grad_hyp = torch.zeros(1 + dim, dtype=f64, device=dev)
+        grad_z = torch.zeros((M, dim), dtype=f64, device=dev)
+        ws = torch.empty(max(int(lib.tb_sgpr_kuf_grad_workspace(chunk_n, M, dim)), 1),
+                         dtype=torch.uint8, device=dev)
         for n0 in range(0, int(self.X.shape[0]), chunk_n):
             Xc = self.X[n0:n0 + chunk_n].contiguous()
             yc = self.y[n0:n0 + chunk_n].to(f64)
-            K = kernel_matrix(self.Z, Xc, self.kernel, self.variance, self.lengthscales)
+            K = kernel_matrix(self.Z, Xc, self.kernel, var, self.lengthscales)
             W = torch.addr(G2 @ K, g, yc)                   # 2 G K + g y^T
             rc = lib.tb_sgpr_kuf_grad(
                 Xc.data_ptr(), self.Z.data_ptr(), W.data_ptr(), K.data_ptr(), int(Xc.shape[0]),
-                M, dim, _lib.KERNELS[self.kernel], dt, self.variance,
-                self.lengthscales.ctypes.data_as(ctypes.c_void_p), grad_hyp.data_ptr(),
+                M, dim, _lib.KERNELS[self.kernel], dt, var, lsp, grad_hyp.data_ptr(),
                 grad_z.data_ptr(), ws.data_ptr(), ws.numel(), st.cuda_stream)
             _lib.check(rc, "sgpr_kuf_grad")
         if self.group is not None:
             import torch.distributed as dist
             dist.all_reduce(grad_hyp, group=self.group)
             dist.all_reduce(grad_z, group=self.group)
-        grads = {"variance": float(var.grad) + float(grad_hyp[0]),
-                 "lengthscales": (ls.grad + grad_hyp[1:]).cpu().numpy(),
-                 "noise_variance": float(s2.grad),
-                 "Z": (Zd.grad + grad_z).cpu().numpy()}
-        return float(elbo.detach()), grads
+        grad_hyp += grad_hyp_k
+        grad_z += grad_z_k
+        grads = {"variance": -0.5 * N / s2 + float(grad_hyp[0]),
+                 "lengthscales": grad_hyp[1:].cpu().numpy(),
+                 "noise_variance": d_s2,
+                 "Z": grad_z.cpu().numpy()}
+        return float(elbo), grads
 
     def predict_mean(self, Xnew):
         """mu(X*) = K(X*, Z) L^-T LB^-T c (GPflow predict_f mean)."""
@@ -339,12 +382,14 @@ class SGPR:
 def grad_memory_bytes(M: int, dim: int, chunk_n: int = 4096) -> int:
     """Device bytes SGPR.elbo_and_grads needs beyond its inputs (planner-style
     estimate, checked against torch's peak by tests/test_sgpr_gpu.py).  The
-    O(M^3) tail is differentiated densely (torch autograd through
-    cholesky / triangular solves): ~16 live M x M fp64 matrices at its peak.
+    O(M^3) tail is differentiated analytically on dense fp64 matrices: at
+    most ~5 live M x M matrices (Sigma, the two inverses, Kuu^-1 Sigma and
+    its product) besides the packed statistics and cuSOLVER workspace
+    (measured peak 6.4 M^2 fp64 words; budgeted 7).
     The N-streaming pass then holds G (twice) plus three M x chunk_n fp64
     panels (K, G K, W) and the reduction partials.  Independent of N."""
     mm = 8 * M * M
-    tail = 16 * mm
+    tail = 7 * mm + 8 * (-(-M // 128)) * (M * dim + (1 + dim) * (-(-M // 32)))
     stream = 2 * mm + 3 * 8 * M * chunk_n + 8 * (-(-chunk_n // 128)) * (M * dim + (1 + dim) * (-(-M // 32)))
     return int(max(tail, stream)) + (1 << 20)
 
