@@ -347,7 +347,7 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
   // the query prep of tc1 follows the centring decision, which reads the
   // first database rows: it runs once chunk 0 is on the device
   auto query_prep = [&]() -> int {
-    if (f16 && p->metric == TB_METRIC_L2) {
+    if (tc && p->metric == TB_METRIC_L2) {
       const int64_t rows0 = std::min(p->chunk_rows, p->n);
       int r0 = launch_f16_center(p->dtype, x, rows0, p->d, stats, st);
       if (r0) return r0;
@@ -355,7 +355,7 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
     return f16 ? launch_query_prep_f16(p->dtype, p->metric, q, p->m, p->d, qn64, qnorm, qln,
                                        stats, (__half*)qhi, p->m_pad, p->d_pad, st)
                : launch_query_prep(p->dtype, p->metric, q, p->m, p->d, qn64, qnorm, qhi, qlo,
-                                   p->m_pad, p->d_pad, st);
+                                   p->m_pad, p->d_pad, st, tc ? stats : nullptr);
   };
 
   const float* prev_s = nullptr;

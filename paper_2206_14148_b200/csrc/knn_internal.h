@@ -44,7 +44,7 @@ struct KnnDims {
 int launch_query_prep(int dtype, int metric, const void* q, int64_t m, int64_t d,
                       double* qn64, float* qnorm, __nv_bfloat16* qhi,
                       __nv_bfloat16* qlo, int64_t m_pad, int64_t d_pad,
-                      cudaStream_t st);
+                      cudaStream_t st, const unsigned* centre = nullptr);
 int launch_db_prep(int dtype, int metric, const void* x, int64_t rows, int64_t d,
                    float* xn, unsigned* xmax_bits, __nv_bfloat16* xhi,
                    __nv_bfloat16* xlo, int64_t rows_pad, int64_t d_pad,

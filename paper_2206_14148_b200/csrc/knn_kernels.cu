@@ -76,10 +76,14 @@ rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
                   float* __restrict__ norm32, unsigned* __restrict__ max_bits,
                   __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
                   int64_t rows_pad, int64_t d_pad, double scale,
-                  uint8_t* __restrict__ ext) {
+                  uint8_t* __restrict__ ext, const unsigned* __restrict__ centre) {
   __shared__ float wmax[8];
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t r = gt / G;
+  // l2 centring on the sample mean (decided on the device, f16_center_*):
+  // rows become x - mu (fp64) before the split; padding rows stay zero
+  const bool centred = !NORM && centre != nullptr && centre[14] != 0u;
+  const double* mu = centred ? reinterpret_cast<const double*>(centre + 64) : nullptr;
   const int seg = (int)(gt % G);
   double inv = 1.0;
   if (NORM) {
@@ -105,9 +109,14 @@ rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
       for (int j = 0; j < 8; ++j)
         v[j] = (r < rows && c0 + j < d) ? (double)src[r * d + c0 + j] : 0.0;
     }
+    if (centred && r < rows) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (c0 + j < d) v[j] -= mu[c0 + j];
+    }
     __align__(16) __nv_bfloat16 h[8];
     __align__(16) __nv_bfloat16 l[8];
-    if (sizeof(T) == 4 && !NORM && scale == 1.0) {
+    if (sizeof(T) == 4 && !NORM && scale == 1.0 && !centred) {
       // f32 rows: x - bf16(x) is exact in f32, so the split needs no fp64
       // (same bits as the fp64 path); only the norm accumulates in fp64
 #pragma unroll
@@ -179,7 +188,7 @@ static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
                      float* n32, float* norm32, unsigned* max_bits,
                      __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t rows_pad,
                      int64_t d_pad, cudaStream_t st, int metric, double scale = 1.0,
-                     uint8_t* ext = nullptr) {
+                     uint8_t* ext = nullptr, const unsigned* centre = nullptr) {
   const int64_t limit = hi ? rows_pad : rows;
   if (limit <= 0) return TB_OK;
   if (hi && d_pad % 64 == 0) {
@@ -190,7 +199,7 @@ static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
 #define TB_SPLIT(GG, NN)                                                                     \
   rows_split_kernel<T, GG, NN><<<blocks, 256, 0, st>>>((const T*)src, rows, d, n64, n32,     \
                                                        norm32, max_bits, hi, lo, rows_pad,   \
-                                                       d_pad, scale, ext)
+                                                       d_pad, scale, ext, centre)
     if (G == 8) {
       if (norm) TB_SPLIT(8, true); else TB_SPLIT(8, false);
     } else if (G == 16) {
@@ -644,24 +653,25 @@ int launch_db_prep_f16(int dtype, int metric, const void* x, int64_t rows, int64
 int launch_query_prep(int dtype, int metric, const void* q, int64_t m, int64_t d,
                       double* qn64, float* qnorm, __nv_bfloat16* qhi,
                       __nv_bfloat16* qlo, int64_t m_pad, int64_t d_pad,
-                      cudaStream_t st) {
+                      cudaStream_t st, const unsigned* centre) {
   // the tensor-core engines use 2q (exact) so that acc' = 2 q.x - ||x||^2
   if (dtype == TB_F32)
     return rows_prep<float>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st,
-                            metric, 2.0);
+                            metric, 2.0, nullptr, centre);
   return rows_prep<double>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st,
-                           metric, 2.0);
+                           metric, 2.0, nullptr, centre);
 }
 
 int launch_db_prep(int dtype, int metric, const void* x, int64_t rows, int64_t d,
                    float* xn, unsigned* xmax_bits, __nv_bfloat16* xhi,
                    __nv_bfloat16* xlo, int64_t rows_pad, int64_t d_pad,
                    uint8_t* xext, cudaStream_t st) {
+  // xmax_bits is the stats block, which also carries the centring decision
   if (dtype == TB_F32)
     return rows_prep<float>(x, rows, d, nullptr, xn, nullptr, xmax_bits, xhi, xlo, rows_pad, d_pad,
-                            st, metric, 1.0, xext);
+                            st, metric, 1.0, xext, xhi ? xmax_bits : nullptr);
   return rows_prep<double>(x, rows, d, nullptr, xn, nullptr, xmax_bits, xhi, xlo, rows_pad, d_pad,
-                           st, metric, 1.0, xext);
+                           st, metric, 1.0, xext, xhi ? xmax_bits : nullptr);
 }
 
 // ------------------------------------------------- SIMT candidate engine --
