@@ -360,7 +360,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
                 ph ^= 1;
               }
             }
-            if (SQ) mma_commit(&empty[qstage]);   // query k-block consumed
+            if (SQ) {                             // query k-block consumed
+              if (MC) mma_commit_mc(&empty[qstage], 3); else mma_commit(&empty[qstage]);
+            }
           }
           if (MC) mma_commit_mc(&eempty[buf], 3); else mma_commit(&eempty[buf]);  // norm block may be replaced
           mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
@@ -807,7 +809,7 @@ static bool tc_pair_on(int passes, int64_t d_pad, int64_t m) {
 static bool tc_mc_on(int passes, int64_t d_pad, int64_t m) {
   const char* e = std::getenv("TB_TC_MC");
   if (e && *e == '0') return false;
-  return passes == 1 && d_pad <= kTcMaxDpad && m > kTcM;
+  return passes == 1 && m > kTcM;
 }
 
 // units are (query tile, slice) - or (query-tile pair, slice) on `sms`/2
@@ -900,8 +902,8 @@ static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtenso
                      unsigned* gthr, const float* f16p, bool mc, cudaStream_t st) {
   constexpr bool F16 = PASSES == 1;            // engine tc1 is the fp16 single pass
   const size_t smem = TcCfg<PASSES, SQ>::smem_bytes(nkb);
-  if (!SQ && F16 && mc) {
-    auto kern = knn_tc_kernel<PASSES, KC, false, F16, true>;
+  if (F16 && mc) {
+    auto kern = knn_tc_kernel<PASSES, KC, SQ, F16, true>;
     TB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
