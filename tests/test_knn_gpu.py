@@ -166,7 +166,7 @@ def test_cta_pair_tc_kernel(n, m, d, monkeypatch):
     assert op.fallback_count() == 0
 
 
-@pytest.mark.parametrize("n,m,d", [(70000, 300, 128), (9000, 129, 17)])
+@pytest.mark.parametrize("n,m,d", [(70000, 300, 128), (9000, 129, 17), (20000, 130, 300)])
 def test_single_cta_tc1_kernel(n, m, d, monkeypatch):
     """tc1 defaults to multicast clusters of 2 CTAs; TB_TC_MC=0 selects the
     1-CTA kernel, which must give the same exact answers."""
