@@ -424,7 +424,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         const uint32_t taddr =
             tmem + ((uint32_t)(quad * 32) << 16) + buf * kTcN + half * (kTcN / 2);
         const int base = idx_base + t * kTcN + half * (kTcN / 2);
-#pragma unroll 1
+#pragma unroll
         for (int c = 0; c < kTcN / 64; c += 2) {
           uint32_t ra[32], rb[32];
           tmem_ld32(taddr + c * 32, ra);
