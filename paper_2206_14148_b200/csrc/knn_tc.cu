@@ -430,6 +430,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           tmem_ld32(taddr + c * 32, ra);
           tmem_ld32(taddr + (c + 1) * 32, rb);
           tmem_ld_wait();
+          if (c + 2 >= kTcN / 64) {
+            // last columns are in registers: release the accumulator now so
+            // the MMA of tile i+2 may overwrite it while they are processed
+            tc_fence_before();
+            mbar_arrive(&tempty[buf]);
+          }
           if (work.drain_only & 1) continue;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -449,8 +455,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             }
           }
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[buf]);
         // publish the running K'-th score every tile: the other column half
         // and every other CTA on this query tighten their thresholds with it
         if (q < m && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst() * sc_inv));
