@@ -793,7 +793,13 @@ int tc_max_dpad() { return kTcMaxDpadSQ; }
 // first kTcSeedTiles tiles (one unit per query tile) publishes per-query
 // thresholds; the main launch splits the remaining tiles into slices,
 // minimising waves x (tiles per slice + ~2 tiles of per-unit overhead).
-constexpr int kTcSeedTiles = 8;
+// Seed length at C2, tc1 engine, same box: none 2.77 ms, 2-4 tiles 2.71,
+// 8 tiles 2.72, 16 2.73, 32 2.76 (TB_TC_SEED=n overrides, A/B timing).
+constexpr int kTcSeedTiles = 4;
+static int tc_seed_tiles() {
+  const char* e = std::getenv("TB_TC_SEED");
+  return e ? std::max(1, std::atoi(e)) : kTcSeedTiles;
+}
 
 // CTA pairs (knn_tc_pair_kernel): opt-in with TB_TC_PAIR=1 for the 3-pass
 // engine with a resident query tile.  Measured at C2 (tools/tc_ab.py): the
@@ -824,7 +830,7 @@ static void tc_schedule(int64_t m, int64_t rows_pad, int sms, bool pair, TcWork*
   const int qunits = pair ? (qtiles + 1) / 2 : qtiles;
   const int workers = pair ? sms / 2 : sms;
   const int T = (int)(rows_pad / kTcN);
-  const int S = std::min(T, kTcSeedTiles);
+  const int S = std::min(T, tc_seed_tiles());
   const char* dbg = std::getenv("TB_TC_DEBUG");
   const int drain = dbg ? std::atoi(dbg) : 0;
   *seed = TcWork{qtiles, 0, S, 1, S, 0, drain};
