@@ -472,19 +472,38 @@ __global__ void ext_f16_kernel(const float* __restrict__ xn, int64_t rows, int64
   *reinterpret_cast<uint4*>(base + 128) = make_uint4(0u, 0u, 0u, 0u);
 }
 
+// Grid of a grid-stride kernel: at most one full wave of resident blocks
+// (occupancy queried once per kernel), so no partial second wave runs at a
+// fraction of the SMs' bandwidth.
+template <auto Kern>
+static unsigned resident_grid(int threads, int64_t want) {
+  static int cap = 0;
+  if (!cap) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, Kern, threads, 0);
+    cap = std::max(1, per_sm) * sms;
+  }
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, cap));
+}
+
 template <typename T, int MODE>
 static void f16_rows_launch(const void* src, int64_t rows, int64_t d, double* n64, float* n32,
                             float* norm32, float* resid, unsigned* stats, __half* hi,
                             int64_t rows_pad, int64_t d_pad, bool norm, cudaStream_t st) {
   const int G = d_pad == 64 ? 8 : d_pad == 128 ? 16 : 32;
-  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(rows_pad * G, 256), 148 * 8);
+  const int64_t want = ceil_div(rows_pad * G, 256);
 #define TB_F16(GG, NN)                                                                   \
   do {                                                                                     \
-    rows_f16_kernel<T, GG, NN, MODE, false><<<blocks, 256, 0, st>>>(                       \
-        (const T*)src, rows, d, n64, n32, norm32, resid, stats, hi, rows_pad, d_pad);      \
+    rows_f16_kernel<T, GG, NN, MODE, false>                                                \
+        <<<resident_grid<rows_f16_kernel<T, GG, NN, MODE, false>>(256, want), 256, 0, st>>>( \
+            (const T*)src, rows, d, n64, n32, norm32, resid, stats, hi, rows_pad, d_pad);  \
     if (!NN)                                                                               \
-      rows_f16_kernel<T, GG, false, MODE, true><<<blocks, 256, 0, st>>>(                   \
-          (const T*)src, rows, d, n64, n32, norm32, resid, stats, hi, rows_pad, d_pad);    \
+      rows_f16_kernel<T, GG, false, MODE, true>                                            \
+          <<<resident_grid<rows_f16_kernel<T, GG, false, MODE, true>>(256, want), 256, 0,  \
+             st>>>((const T*)src, rows, d, n64, n32, norm32, resid, stats, hi, rows_pad,   \
+                   d_pad);                                                                 \
   } while (0)
   if (G == 8) {
     if (norm) TB_F16(8, true); else TB_F16(8, false);
