@@ -180,6 +180,23 @@ def test_single_cta_tc1_kernel(n, m, d, monkeypatch):
     assert op.fallback_count() == 0
 
 
+@pytest.mark.parametrize("engine", ["tc1", "tc3"])
+@pytest.mark.parametrize("seed_tiles", ["1", "16", "400"])
+def test_seed_launch_length_is_exact(engine, seed_tiles, monkeypatch):
+    """The seed launch only primes the shared thresholds: any length
+    (TB_TC_SEED, including one longer than the database) gives the same exact
+    answers and a consistent candidate-list count."""
+    monkeypatch.setenv("TB_TC_SEED", seed_tiles)
+    n, m, d = 70000, 300, 128
+    x, q = synthetic.gaussian_knn(n, m, d, seed=11)
+    ref_d, ref_i = oknn.exact(x, q, 10)
+    op = neighbors.KnnOperator(n, m, d, 10, engine=engine)
+    import torch
+    dist, idx = op.run(torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda())
+    check(dist.cpu().numpy(), idx.cpu().numpy(), ref_d, ref_i, x, q)
+    assert op.fallback_count() == 0
+
+
 @pytest.mark.parametrize("offset,tail", [(100.0, False), (0.5, False), (0.0, True)])
 def test_fp16_engine_offset_and_heavy_tail_data(offset, tail):
     """tc1 centres l2 data with a large common offset on the sample mean
