@@ -389,9 +389,11 @@ def run_ours(args):
         # the reference-facing call with HOST buffers (tb_knn_run_host): pinned
         # x, q copied in (queries first, then the database chunk by chunk on
         # one copy stream, overlapped with compute) and dist, idx copied out,
-        # every step.  Its plan caps chunks at n/16 so fifteen of the sixteen
+        # every step.  Its plan caps chunks at n/20 so nineteen of the twenty
         # database copies overlap compute (tools/e2e_chunks.py: 4/8/12/16/24
-        # chunks -> 0.89/0.97/0.99/1.00/0.85 M q/s; the bound is PCIe).
+        # chunks -> 0.89/0.97/0.99/1.00/0.85 M q/s on an early build; with the
+        # current engine 12/16/20/24/32 -> 0.998/1.001/1.007/1.008/0.911 M q/s,
+        # 20 keeps a margin below the cliff; the bound is PCIe).
         # N > 1: every rank copies its shard in, the per-shard lists meet on
         # the device (NCCL all_gather + merge) and the global result is copied
         # out on every rank (distributed.knn_sharded_host).
@@ -399,7 +401,7 @@ def run_ours(args):
         qh = q.cpu().pin_memory()
         op_h = neighbors.KnnOperator(rows, M_Q, DIM, K, dtype=np.float32, out_dtype=out_dtype,
                                      engine=args.engine, memory_limit=LIMIT, device=dev,
-                                     max_chunk_rows=-(-rows // 16))
+                                     max_chunk_rows=-(-rows // 20))
         staging = (x, q, out[0], out[1])      # device buffers refilled every step
         dh = torch.empty(out[0].shape, dtype=out[0].dtype).pin_memory()
         ih = torch.empty(out[1].shape, dtype=out[1].dtype).pin_memory()
