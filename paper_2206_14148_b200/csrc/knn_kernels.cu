@@ -1002,17 +1002,56 @@ __global__ void knn_refine_kernel(const float* __restrict__ cs,
     ds[p] = INFINITY;
     js[p] = kInvalidIdx;
   }
-  for (int c = 0; c < KC; ++c) {
-    const int j = ci[r * KC + c];
-    double acc = 0.0;
-    if (j != kInvalidIdx) acc = exact_dist_warp<T, MET>(qr, x + (int64_t)j * d, d, lane);
-    if ((c & 31) == lane) {
+  if (sizeof(T) == 4 && MET == TB_METRIC_L2 && d <= 128 && (d & 3) == 0) {
+    // f32 rows of <= 128 columns: one float4 per lane per row, and the rows
+    // of 8 candidates in flight at once (the generic loop below waits for
+    // each gathered row in turn)
+    const bool act = lane * 4 < d;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 qv = act ? __ldg(reinterpret_cast<const float4*>(qr) + lane) : z4;
+    int jv[PER];
 #pragma unroll
-      for (int p = 0; p < PER; ++p)
-        if (p == (c >> 5)) {
-          ds[p] = j != kInvalidIdx ? acc : INFINITY;
-          js[p] = j;
+    for (int p = 0; p < PER; ++p)
+      jv[p] = p * 32 + lane < KC ? ci[r * KC + p * 32 + lane] : kInvalidIdx;
+    constexpr int B = KC < 8 ? KC : 8;
+#pragma unroll
+    for (int c0 = 0; c0 < KC; c0 += B) {
+      float4 xv[B];
+      int jj[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int c = c0 + u;
+        jj[u] = __shfl_sync(0xffffffffu, jv[c >> 5], c & 31);
+        xv[u] = act && jj[u] != kInvalidIdx
+                    ? __ldg(reinterpret_cast<const float4*>(
+                                reinterpret_cast<const float*>(x) + (int64_t)jj[u] * d) + lane)
+                    : z4;
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int c = c0 + u;
+        const double e0 = (double)qv.x - (double)xv[u].x, e1 = (double)qv.y - (double)xv[u].y;
+        const double e2 = (double)qv.z - (double)xv[u].z, e3 = (double)qv.w - (double)xv[u].w;
+        const double acc = warp_sum(fma(e3, e3, fma(e2, e2, fma(e1, e1, e0 * e0))));
+        if ((c & 31) == lane) {
+          ds[c >> 5] = jj[u] != kInvalidIdx ? acc : INFINITY;
+          js[c >> 5] = jj[u];
         }
+      }
+    }
+  } else {
+    for (int c = 0; c < KC; ++c) {
+      const int j = ci[r * KC + c];
+      double acc = 0.0;
+      if (j != kInvalidIdx) acc = exact_dist_warp<T, MET>(qr, x + (int64_t)j * d, d, lane);
+      if ((c & 31) == lane) {
+#pragma unroll
+        for (int p = 0; p < PER; ++p)
+          if (p == (c >> 5)) {
+            ds[p] = j != kInvalidIdx ? acc : INFINITY;
+            js[p] = j;
+          }
+      }
     }
   }
   double kth = INFINITY;
