@@ -231,6 +231,20 @@ static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
 // error: |q.x - q'.x'| <= ||q|| XL + ||ql|| (X + 3 XL).
 // Scale slots (floats, stats + kF16Slot): [0] s, [1] t, [2] alpha, [3] 1/(s t).
 
+// Block-wide max of non-negative floats, then ONE atomicMax per block (one
+// per warp serialised ~10k atomics on a single word: 10 us for the C2 queries).
+__device__ __forceinline__ void block_atomic_max(float mx, unsigned* bits) {
+  __shared__ float wm[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, wm[w]);
+    if (mx > 0.f) atomicMax(bits, __float_as_uint(mx));
+  }
+}
+
 __global__ void absmax_f32_kernel(const float* __restrict__ src, int64_t n,
                                   unsigned* __restrict__ bits) {
   float mx = 0.f;
@@ -243,9 +257,7 @@ __global__ void absmax_f32_kernel(const float* __restrict__ src, int64_t n,
   for (int64_t e = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x)
     mx = fmaxf(mx, fabsf(src[e]));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(bits, __float_as_uint(mx));
+  block_atomic_max(mx, bits);
 }
 
 __global__ void absmax_f64_kernel(const double* __restrict__ src, int64_t n,
@@ -254,9 +266,7 @@ __global__ void absmax_f64_kernel(const double* __restrict__ src, int64_t n,
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x)
     mx = fmaxf(mx, __double2float_ru(fabs(src[e])));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(bits, __float_as_uint(mx));
+  block_atomic_max(mx, bits);
 }
 
 __device__ __forceinline__ float pow2_floor(float v) {      // largest 2^e <= v
@@ -621,7 +631,7 @@ static int f16_query_prep(const void* q, int64_t m, int64_t d, double* qn64, flo
   TB_CUDA_TRY(cudaMemsetAsync(stats + 3, 0, 4, st));
   if (metric != TB_METRIC_COSINE && m > 0) {
     const int64_t n = m * d;
-    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, 256 * 4), 148 * 8);
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, 256 * 4), 148 * 2);
     if (sizeof(T) == 4)
       absmax_f32_kernel<<<blocks, 256, 0, st>>>((const float*)q, n, stats + 3);
     else
