@@ -32,7 +32,13 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep stdout to the one JSON line
+# NCCL's communicator INIT lines go to a per-process log file (NCCL prints to
+# stdout otherwise, and stdout must stay the one JSON line); each rank
+# forwards them to its stderr when it finishes (_forward_nccl_log).
+if "NCCL_DEBUG" not in os.environ:
+    os.environ["NCCL_DEBUG"] = "INFO"
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/tb_bench_nccl.%h.{os.getpid()}.log")
 
 N_DB, M_Q, DIM, K = 1_000_000, 10_000, 128, 10
 LIMIT = 10**9
@@ -258,6 +264,62 @@ def run_sgpr(args, dev, world, rank, dist):
     return out
 
 
+def _forward_nccl_log():
+    """Copy this process's NCCL debug file (see NCCL_DEBUG_FILE above) to
+    stderr, so the launcher sees the communicator lines (nranks, NVLS)."""
+    import glob
+    pat = os.environ.get("NCCL_DEBUG_FILE", "")
+    if not pat.startswith("/tmp/tb_bench_nccl."):
+        return
+    for path in glob.glob(pat.replace("%h", "*")):
+        try:
+            with open(path) as fh:
+                sys.stderr.write(fh.read())
+            os.remove(path)
+        except OSError:
+            pass
+    sys.stderr.flush()
+
+
+def spawn_ranks(gpus: int, argv) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this script as N ranks
+    (one process per GPU) through torch.distributed.run on 127.0.0.1, the
+    same launch the driver uses; rank 0's JSON line reaches our stdout."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *argv]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.run(cmd, env=env).returncode
+
+
+def run_dry(args):
+    """--dry-run: the launch plumbing only (CPU, gloo): every rank joins the
+    group and all-reduces its rank; rank 0 prints what it saw.  Lets the
+    N-rank spawn be tested without GPUs (tests/test_bench_launch.py)."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([float(rank), 1.0])
+        dist.all_reduce(t)
+        ranks_sum, ranks = int(t[0].item()), int(t[1].item())
+        dist.destroy_process_group()
+    else:
+        ranks_sum, ranks = 0, 1
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "requested_gpus": args.gpus,
+                          "ranks": ranks, "rank_sum": ranks_sum}))
+    return 0
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -337,7 +399,7 @@ def run_ours(args):
     def step(events=None):
         if not use_dist:
             return op.run(x, q, out, events=events)
-        return distributed.knn_sharded(x, q, K, index_base=start, operator=op)
+        return distributed.knn_sharded(x, q, K, index_base=start, operator=op, events=events)
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -350,7 +412,7 @@ def run_ours(args):
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
     for s in range(args.steps):
-        step(ev_sets[s] if not use_dist else None)
+        step(ev_sets[s])
     t1.record()
     torch.cuda.synchronize()
     if use_dist:
@@ -373,14 +435,19 @@ def run_ours(args):
     value = M_Q * args.steps / (ms / 1000.0)
     fb = op.fallback_count()
 
-    # dominant kernel (candidate engine) time, measured inside the timed region
-    eng_ms = None
-    if not use_dist:
-        per = []
-        for evs in ev_sets:
-            per.append(sum(evs[2 * c].elapsed_time(evs[2 * c + 1])
-                           for c in range(int(plan.n_chunks))))
-        eng_ms = sum(per) / len(per)
+    # dominant kernel (candidate engine) time, measured inside the timed
+    # region on every rank; N > 1: the slowest rank's (max over ranks)
+    per = []
+    for evs in ev_sets:
+        per.append(sum(evs[2 * c].elapsed_time(evs[2 * c + 1])
+                       for c in range(int(plan.n_chunks))))
+    eng_ms = sum(per) / len(per)
+    if use_dist:
+        tt = torch.tensor([eng_ms, float(rows)], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        eng_ms, rows_max = float(tt[0].item()), int(tt[1].item())
+    else:
+        rows_max = rows
 
     # end to end through the public operator: pinned host inputs copied in,
     # results copied out, every step
@@ -477,7 +544,7 @@ def run_ours(args):
     peaks, peak_src = _peaks()
     roof = None
     if eng_ms:
-        useful = 2.0 * M_Q * rows * DIM                      # cross-term flops
+        useful = 2.0 * M_Q * rows_max * DIM    # cross-term flops (largest shard)
         engine = {1: "tc3", 2: "simt", 3: "tc1"}[int(plan.engine)]
         passes = {"tc3": 3, "tc1": 1, "simt": 1}[engine]
         achieved = useful / (eng_ms / 1000.0) / 1e12
@@ -557,12 +624,21 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sgpr", action="store_true")
     ap.add_argument("--sgpr-cpu-n", type=int, default=16384)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch plumbing only (gloo, no GPU work)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return spawn_ranks(args.gpus, sys.argv[1:])
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
-    return run_ours(args)
+    try:
+        return run_ours(args)
+    finally:
+        _forward_nccl_log()
 
 
 if __name__ == "__main__":

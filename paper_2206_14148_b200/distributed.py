@@ -59,11 +59,13 @@ def merge_topk(dist_lists, idx_lists, stream=None):
 
 def knn_sharded(x_shard, q, k: int, *, index_base: int, group=None, operator=None,
                 memory_limit=None, engine: str = "auto", local_fn=None, merge_fn=None,
-                out_dtype=None):
+                out_dtype=None, events=None):
     """Global kNN over a database sharded across the ranks of ``group``.
 
     Every rank passes its own shard and the full query set; every rank
     receives the global (dist[m,k], idx[m,k]).  Shards must hold >= k rows.
+    ``events`` (optional torch.cuda.Event pairs) time this rank's candidate
+    engine launches, as in ``KnnOperator.run``.
     """
     torch = _torch()
     import torch.distributed as dist
@@ -75,7 +77,7 @@ def knn_sharded(x_shard, q, k: int, *, index_base: int, group=None, operator=Non
                                    int(q.shape[1]), k, dtype=_np_dtype(x_shard),
                                    out_dtype=np.float64, engine=engine,
                                    memory_limit=memory_limit)
-        d, i = operator.run(x_shard, q, index_base=index_base)
+        d, i = operator.run(x_shard, q, index_base=index_base, events=events)
     else:
         d, i = local_fn(x_shard, q, k, index_base)
     world = dist.get_world_size(group)
@@ -124,6 +126,28 @@ def knn_sharded_host(xh_shard, qh, k: int, *, index_base: int, operator, group=N
     out_host[1].copy_(oi, non_blocking=True)
     torch.cuda.current_stream(od.device).synchronize()
     return out_host
+
+
+def allreduce_statistics(Sigma, v, yy, n_local: int, group=None):
+    """Sum per-rank SGPR sufficient statistics over ``group`` (the north
+    star's N-split: each rank streams its own training rows).  ``Sigma`` is
+    reduced in place in whatever layout the rank's plan produced (full
+    [M, M] or packed lower tiles: an elementwise sum either way, and every
+    rank's plan has the same layout because M and the engine are shared);
+    v, yy and the row count travel together in one small fp64 buffer.
+    Returns (Sigma, v, yy: float, N_total: int).  The fixed order of a ring
+    or tree sum is deterministic for a given world size and backend."""
+    torch = _torch()
+    import torch.distributed as dist
+
+    small = torch.empty(v.numel() + 2, dtype=torch.float64, device=v.device)
+    small[:v.numel()].copy_(v.reshape(-1))
+    small[v.numel()] = yy if not torch.is_tensor(yy) else yy.reshape(-1)[0]
+    small[v.numel() + 1] = float(n_local)
+    dist.all_reduce(Sigma, group=group)
+    dist.all_reduce(small, group=group)
+    v.reshape(-1).copy_(small[:v.numel()])
+    return Sigma, v, float(small[v.numel()].item()), int(round(float(small[-1].item())))
 
 
 def _np_dtype(t):

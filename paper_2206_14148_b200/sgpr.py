@@ -172,16 +172,11 @@ class SGPR:
             st.cuda_stream)
         _lib.check(rc, "sgpr_stats")
         del ws
-        n_total = N
+        n_total, yy_total = N, float(yy.item())
         if self.group is not None:
-            import torch.distributed as dist
-            dist.all_reduce(Sigma, group=self.group)
-            dist.all_reduce(v, group=self.group)
-            dist.all_reduce(yy, group=self.group)
-            nt = torch.tensor([N], dtype=torch.float64, device=self.device)
-            dist.all_reduce(nt, group=self.group)
-            n_total = int(nt.item())
-        self._stats = SgprStats(Sigma, v, float(yy.item()), n_total, p)
+            from .distributed import allreduce_statistics
+            Sigma, v, yy_total, n_total = allreduce_statistics(Sigma, v, yy, N, self.group)
+        self._stats = SgprStats(Sigma, v, yy_total, n_total, p)
         return self._stats
 
     # -- O(M^3) tail --------------------------------------------------------

@@ -34,13 +34,17 @@ def quantized_knn(n: int, m: int, d: int, seed: int = 0, dtype=np.float32):
 
 
 def sgpr_data(N: int, d: int, M: int, seed: int = 0, n_test: int = 0,
-              noise: float = 0.1, dtype=np.float32):
-    """X ~ N(0, I_d), y = sin(sum X) + noise*eps, Z = a random subset of X,
-    X* ~ N(0, I_d)."""
+              noise: float = 0.1, dtype=np.float32, z: str = "subset"):
+    """X ~ N(0, I_d), y = sin(sum X) + noise*eps, Z = a random subset of X
+    (z="subset") or independent N(0, I_d) draws (z="normal", as bench.py's
+    C4 does), X* ~ N(0, I_d)."""
     rng = np.random.default_rng(seed)
     X = rng.standard_normal((N, d)).astype(dtype)
     y = (np.sin(X.astype(np.float64).sum(axis=1))
          + noise * rng.standard_normal(N)).astype(dtype)
-    Z = X[rng.choice(N, size=M, replace=False)].copy()
+    if z == "normal":
+        Z = rng.standard_normal((M, d)).astype(dtype)
+    else:
+        Z = X[rng.choice(N, size=M, replace=False)].copy()
     Xs = rng.standard_normal((n_test, d)).astype(dtype)
     return X, y, Z, Xs

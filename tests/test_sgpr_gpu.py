@@ -225,3 +225,70 @@ def test_whole_elbo_evaluation_within_memory_limit():
     assert peak <= limit, (peak, limit)
     ref, _ = osgpr.elbo(X, y, Z, "matern32", 1.0, 0.6, 0.02)
     assert abs(e - ref) <= 1e-4 * abs(ref)
+
+
+def test_sgpr_c4_shape_matches_golden():
+    """The benchmarked SGPR configuration's shape (BASELINE.json configs[3]:
+    d = 11, M = 1e4, RBF l = 1, variance 1, noise 0.01, memory_limit 1 GB)
+    at N = 3e4 against tests/golden/sgpr_c4_shape.npz (fp64 oracle, made by
+    tests/golden/make_sgpr_c4_golden.py).  Runs the d = 11 instance of the
+    Kuf quantiser, the 79-tile Gram (ragged last 12x12 super-block) over
+    several chunks, and the 79-tile packed tail.  Statistics are held to the
+    exact 24-bit fixed-point Gram; ELBO and mean to the quantised oracle
+    (fp64 rounding of the two tail formulations only) and to the unquantised
+    one (the north-star 1e-4 gate)."""
+    import hashlib
+    import torch
+    g = golden("sgpr_c4_shape.npz")
+    N, d, M = int(g["N"]), int(g["d"]), int(g["M"])
+    X, y, Z, Xs = synthetic.sgpr_data(N, d, M, seed=int(g["seed"]), n_test=300,
+                                      dtype=np.float32, z="normal")
+    h = hashlib.sha256()
+    for a in (X, y, Z, Xs):
+        h.update(np.ascontiguousarray(a).tobytes())
+    assert h.hexdigest() == str(g["x_sha"]), "synthetic generator drifted"
+    var, ls, noise = float(g["variance"]), float(g["lengthscale"]), float(g["noise"])
+    m = tb.SGPR(X, y, Z, "rbf", var, ls, noise, memory_limit="1GB", engine="i8")
+    st = m.statistics()
+    assert int(st.plan.M_pad) == 79 * 128
+    assert int(st.plan.chunk_n) < N                      # several chunks, ragged last
+    assert rel_err(st.v.cpu().numpy(), g["v_q"]) < 1e-11
+    assert abs(st.yy - float(g["yy"])) <= 1e-12 * float(g["yy"])
+    S = st.full_sigma()
+    assert rel_err(S.diagonal().cpu().numpy(), g["diag_q"]) < 1e-11
+    assert rel_err(S[torch.from_numpy(g["rows"]).cuda()].cpu().numpy(), g["rows_q"]) < 1e-11
+    r = torch.from_numpy(np.random.default_rng(7).standard_normal(M)).cuda()
+    assert rel_err((S @ r).cpu().numpy(), g["check_q"]) < 1e-11
+    del S
+    e = m.elbo()
+    scale = N * var / noise                              # size of the cancelling terms
+    assert abs(e - float(g["elbo_q"])) <= 1e-9 * scale, (e, float(g["elbo_q"]))
+    assert abs(e - float(g["elbo"])) <= 1e-4 * abs(float(g["elbo"]))
+    mu = m.predict_mean(Xs)
+    assert rel_err(mu, g["mean_q"]) < 1e-8
+    assert rel_err(mu, g["mean"]) <= 1e-4
+
+
+def test_sgpr_full_c4_i8_engine_matches_fp64_engine():
+    """Full C4 (N = 2e6, d = 11, M = 1e4, RBF, as bench.py generates it):
+    the default fixed-point INT8 engine + packed tail (inside 1 GB) against
+    the fp64 DMMA engine + dense cuSOLVER tail on the same data."""
+    import torch
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(77)
+    X = torch.randn((2_000_000, 11), generator=gen, device=dev)
+    y = (torch.sin(X.double().sum(1)) + 0.1 * torch.randn(X.shape[0], generator=gen, device=dev,
+                                                          dtype=torch.float64)).float()
+    gen.manual_seed(5)
+    Z = torch.randn((10_000, 11), generator=gen, device=dev)
+    Xs = torch.randn((300, 11), generator=gen, device=dev)
+    a = tb.SGPR(X, y, Z, "rbf", 1.0, 1.0, 0.01, memory_limit="1GB", engine="i8")
+    ea = a.elbo()
+    mua = a.predict_mean(Xs)
+    b = tb.SGPR(X, y, Z, "rbf", 1.0, 1.0, 0.01, engine="f64", tail="dense")
+    eb = b.elbo()
+    mub = b.predict_mean(Xs)
+    mua, mub = (t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t) for t in (mua, mub))
+    assert abs(ea - eb) <= 1e-6 * abs(eb), (ea, eb)
+    assert rel_err(mua, mub) <= 1e-4
