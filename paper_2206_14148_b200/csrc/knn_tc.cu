@@ -376,31 +376,28 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     const int quad = warp & 3;           // TMEM lane quadrant this warp may read
     const int half = ew >> 2;            // column half of the 256-wide tile
     const int row = quad * 32 + lane;    // query row within the tile
-    auto load_g = [&](int qq) -> unsigned {
-      return qq < m ? *reinterpret_cast<volatile unsigned*>(gthr + qq) : 0u;
-    };
     TopList<float, KC> L;
     L.init();
-    // per-query pool of K' hashed slots (see insert_masked_acc): its maximum
-    // bounds the K'-th best of everything inserted anywhere.  Read one slot
-    // per tile round-robin; after a full round the running max of the values
-    // read is valid (slots only decrease) and becomes pool_thr.
-    unsigned pk = 0xFFFFFFFFu;
-    float p_max = -INFINITY, pool_thr = INFINITY;
-    int p_slot = 0;
-    auto load_p = [&](int qq, int sl) -> unsigned {
-      return qq < m ? *reinterpret_cast<volatile unsigned*>(pool + (int64_t)qq * KC + sl)
-                    : 0xFFFFFFFFu;
-    };
-    int u = grp;
-    if (u < units) {
-      int slice = u / qunits, qt = qtile_of(u);
-      int t1 = min(work.T, work.t0 + slice * work.tps + work.tps);
-      int t = work.t0 + slice * work.tps;
-      int q = qt * kTcM + row;
-      unsigned gk = load_g(q);
-      pk = load_p(q, 0);
-      for (int i = 0;; ++i) {
+    // Units outer, tiles inner: the per-tile path carries no unit bookkeeping
+    // (it was ~1/3 of the epilogue's issue slots when every tile computed its
+    // successor with integer divisions).  Shared bounds are read with weak
+    // L2 loads (ld.global.cg) one tile ahead of their use.
+    int i = 0;
+    for (int u = grp; u < units; u += ngrp) {
+      const int slice = u / qunits;
+      const int q = qtile_of(u) * kTcM + row;
+      const int tb = work.t0 + slice * work.tps, te = min(work.T, tb + work.tps);
+      const bool qv = q < m;
+      unsigned* const qpool = pool + (int64_t)(qv ? q : 0) * KC;
+      // per-query pool of K' hashed slots (see insert_masked_acc): its maximum
+      // bounds the K'-th best of everything inserted anywhere.  Read one slot
+      // per tile round-robin; after a full round the running max of the values
+      // read is valid (slots only decrease) and becomes pool_thr.
+      float p_max = -INFINITY, pool_thr = INFINITY;
+      int p_slot = 0;
+      unsigned pk = qv ? __ldcg(qpool) : 0xFFFFFFFFu;
+      unsigned gk = qv ? __ldcg(gthr + q) : 0u;
+      for (int t = tb; t < te; ++t, ++i) {
         const int buf = i & 1;
         // candidates must also beat the best K'-th score any list has
         // published for this query and the pool bound (both valid for the union)
@@ -410,15 +407,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           p_max = -INFINITY;
           p_slot = 0;
         }
-        pk = load_p(q, p_slot);
-        const float thr_g = q < m ? fminf(fkey_inv(gk) * sc_mul, pool_thr) : -INFINITY;
-        int nu = u, nt = t + 1;
-        if (nt >= t1) {
-          nu = u + ngrp;
-          nt = work.t0 + (nu / qunits) * work.tps;
+        const float thr_g = qv ? fminf(fkey_inv(gk) * sc_mul, pool_thr) : -INFINITY;
+        if (qv) {
+          pk = __ldcg(qpool + p_slot);
+          gk = __ldcg(gthr + q);
         }
-        const bool more = nu < units;
-        if (more) gk = load_g(qtile_of(nu) * kTcM + row);
         mbar_wait(&tfull[buf], (i >> 1) & 1);
         tc_fence_after();
         const uint32_t taddr =
@@ -450,38 +443,24 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               uint32_t mask = 0;
 #pragma unroll
               for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(r[j]) > nthr ? 1u : 0u) << j;
-              insert_masked_acc(L, r, mask, base + (c + h) * 32, thr_g,
-                                pool + (int64_t)q * KC, sc_inv);
+              insert_masked_acc(L, r, mask, base + (c + h) * 32, thr_g, qpool, sc_inv);
             }
           }
         }
         // publish the running K'-th score every tile: the other column half
         // and every other CTA on this query tighten their thresholds with it
-        if (q < m && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst() * sc_inv));
-        if (nu != u) {
-          // unit done: publish this (slice, column half)'s candidates
-          if (q < m) {
-            const int64_t o = ((int64_t)(work.list0 + slice * 2 + half) * m + q) * KC;
-#pragma unroll
-            for (int p = 0; p < KC; ++p) {
-              cand_s[o + p] = L.s[p] * sc_inv;
-              cand_i[o + p] = L.i[p];
-            }
-          }
-          L.init();
-          if (!more) break;
-          u = nu;
-          slice = u / qunits;
-          qt = qtile_of(u);
-          t1 = min(work.T, work.t0 + slice * work.tps + work.tps);
-          q = qt * kTcM + row;
-          p_max = -INFINITY;
-          pool_thr = INFINITY;
-          p_slot = 0;
-          pk = load_p(q, 0);
-        }
-        t = nt;
+        if (qv && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst() * sc_inv));
       }
+      // unit done: publish this (slice, column half)'s candidates
+      if (qv) {
+        const int64_t o = ((int64_t)(work.list0 + slice * 2 + half) * m + q) * KC;
+#pragma unroll
+        for (int p = 0; p < KC; ++p) {
+          cand_s[o + p] = L.s[p] * sc_inv;
+          cand_i[o + p] = L.i[p];
+        }
+      }
+      L.init();
     }
   }
   tc_fence_before();
