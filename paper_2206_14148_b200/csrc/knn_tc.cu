@@ -293,81 +293,103 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = F16 ? idesc_f16_f32(kTcM, kTcN) : idesc_bf16_f32(kTcM, kTcN);
-      const uint32_t aext_a = smem_u32(aext);
-      int s = 0, i = 0;
-      uint32_t ph = 0, seg = 0;
-      for (int u = grp; u < units; u += ngrp, ++seg) {
-        const int slice = u / qunits;
-        const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
-        if (!SQ) {
-          mbar_wait(a_full, seg & 1);
-          tc_fence_after();
-        }
-        for (int t = t0; t < t1; ++t, ++i) {
-          const int buf = i & 1;
-          mbar_wait(&tempty[buf], ((i >> 1) & 1) ^ 1);
-          mbar_wait(&efull[buf], (i >> 1) & 1);
-          tc_fence_after();
-          const uint32_t d = tmem + buf * kTcN;
-          // acc = -||x||^2  (K = 16 augmented block, initialises the tile)
-          mma_bf16(d, desc_k_inter(aext_a, 128, 256), desc_k_inter(smem_u32(bext + buf * kTcBExt), 128, 256),
-                   idesc, 0);
-          for (int kb = 0; kb < nkb; ++kb) {
-            uint32_t ahi = smem_u32(a_base + (size_t)kb * Cfg::kABlock);
-            uint32_t alo = smem_u32(a_base + (size_t)(nkb + kb) * Cfg::kABlock);
-            int qstage = -1;
-            if (SQ) {
-              mbar_wait(&full[s], ph);
-              ahi = smem_u32(b_base + (size_t)s * Cfg::kBBlock);
-              alo = ahi + Cfg::kABlock;
-              qstage = s;
-              if (++s == S) {
-                s = 0;
-                ph ^= 1;
-              }
-            }
-            // stage x_hi: q_hi.x_hi (+ q_lo.x_hi)
+    // The whole warp runs the loop (waits included) and one elected lane
+    // issues: descriptors stay in uniform registers and every MMA is one
+    // 64-bit add of a precomputed UMMA descriptor (start address = byte
+    // address >> 4) instead of a per-MMA register->uniform broadcast loop.
+    constexpr uint32_t idesc = F16 ? idesc_f16_f32(kTcM, kTcN) : idesc_bf16_f32(kTcM, kTcN);
+    constexpr uint32_t kAStep = Cfg::kABlock >> 4, kBStep = Cfg::kBBlock >> 4;
+    const uint64_t dext_a = desc_k_inter(smem_u32(aext), 128, 256);
+    const uint64_t dext_b = desc_k_inter(smem_u32(bext), 128, 256);
+    const uint64_t da = desc_k_sw128(smem_u32(a_base));
+    const uint64_t db = desc_k_sw128(smem_u32(b_base));
+    const bool mma_on = !(work.drain_only & 4);
+    int s = 0, i = 0;
+    uint32_t ph = 0, seg = 0;
+    for (int u = grp; u < units; u += ngrp, ++seg) {
+      const int slice = u / qunits;
+      const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
+      if (!SQ) {
+        mbar_wait(a_full, seg & 1);
+        tc_fence_after();
+      }
+      for (int t = t0; t < t1; ++t, ++i) {
+        const int buf = i & 1;
+        mbar_wait(&tempty[buf], ((i >> 1) & 1) ^ 1);
+        mbar_wait(&efull[buf], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + buf * kTcN;
+        // acc = -||x||^2  (K = 16 augmented block, initialises the tile)
+        if (elect_one_sync()) mma_bf16(d, dext_a, dext_b + buf * (kTcBExt >> 4), idesc, 0);
+        __syncwarp();
+        for (int kb = 0; kb < nkb; ++kb) {
+          uint64_t ahi = da + (uint64_t)kb * kAStep;
+          uint64_t alo = da + (uint64_t)(nkb + kb) * kAStep;
+          int qstage = -1;
+          if (SQ) {
             mbar_wait(&full[s], ph);
-            tc_fence_after();
-            uint32_t b0 = smem_u32(b_base + (size_t)s * Cfg::kBBlock);
-#pragma unroll
-            for (int kk = 0; kk < kTcKB / 16; ++kk) {
-              const uint32_t ko = kk * 32;  // 16 bf16 = 32 bytes along the swizzled row
-              if (work.drain_only & 4) continue;
-              mma_bf16(d, desc_k_sw128(ahi + ko), desc_k_sw128(b0 + ko), idesc, 1);
-              if (PASSES == 3)
-                mma_bf16(d, desc_k_sw128(alo + ko), desc_k_sw128(b0 + ko), idesc, 1);
-            }
-            if (MC) mma_commit_mc(&empty[s], 3); else mma_commit(&empty[s]);
+            ahi = db + (uint64_t)s * kBStep;
+            alo = ahi + kAStep;
+            qstage = s;
             if (++s == S) {
               s = 0;
               ph ^= 1;
             }
-            if (PASSES == 3) {
-              // stage x_lo: q_hi.x_lo
-              mbar_wait(&full[s], ph);
-              tc_fence_after();
-              b0 = smem_u32(b_base + (size_t)s * Cfg::kBBlock);
+          }
+          // stage x_hi: q_hi.x_hi (+ q_lo.x_hi)
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          uint64_t b0 = db + (uint64_t)s * kBStep;
+          if (elect_one_sync()) {
+            if (mma_on) {
 #pragma unroll
-              for (int kk = 0; kk < kTcKB / 16; ++kk)
-                if (!(work.drain_only & 4))
-                  mma_bf16(d, desc_k_sw128(ahi + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, 1);
-              if (MC) mma_commit_mc(&empty[s], 3); else mma_commit(&empty[s]);
-              if (++s == S) {
-                s = 0;
-                ph ^= 1;
+              for (int kk = 0; kk < kTcKB / 16; ++kk) {   // 16 elements = 32 B = 2 units
+                mma_bf16(d, ahi + 2 * kk, b0 + 2 * kk, idesc, 1);
+                if (PASSES == 3) mma_bf16(d, alo + 2 * kk, b0 + 2 * kk, idesc, 1);
               }
             }
-            if (SQ) {                             // query k-block consumed
-              if (MC) mma_commit_mc(&empty[qstage], 3); else mma_commit(&empty[qstage]);
+            if (MC) mma_commit_mc(&empty[s], 3); else mma_commit(&empty[s]);
+          }
+          __syncwarp();
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+          if (PASSES == 3) {
+            // stage x_lo: q_hi.x_lo
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            b0 = db + (uint64_t)s * kBStep;
+            if (elect_one_sync()) {
+              if (mma_on) {
+#pragma unroll
+                for (int kk = 0; kk < kTcKB / 16; ++kk)
+                  mma_bf16(d, ahi + 2 * kk, b0 + 2 * kk, idesc, 1);
+              }
+              if (MC) mma_commit_mc(&empty[s], 3); else mma_commit(&empty[s]);
+            }
+            __syncwarp();
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
             }
           }
+          if (SQ) {                             // query k-block consumed
+            if (elect_one_sync()) {
+              if (MC) mma_commit_mc(&empty[qstage], 3); else mma_commit(&empty[qstage]);
+            }
+            __syncwarp();
+          }
+        }
+        if (elect_one_sync()) {
           if (MC) mma_commit_mc(&eempty[buf], 3); else mma_commit(&eempty[buf]);  // norm block may be replaced
           mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
         }
-        if (!SQ) mma_commit(a_empty);         // query tile may be replaced
+        __syncwarp();
+      }
+      if (!SQ) {
+        if (elect_one_sync()) mma_commit(a_empty);         // query tile may be replaced
+        __syncwarp();
       }
     }
   } else {
