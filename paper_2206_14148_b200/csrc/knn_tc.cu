@@ -220,20 +220,25 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // (whole warp, one elected lane issues; see the MMA issuer below)
+    if (elect_one_sync()) {
       tma_prefetch(&tm_qhi);
       tma_prefetch(&tm_xhi);
       if (Cfg::kMats == 2) {
         tma_prefetch(&tm_qlo);
         tma_prefetch(&tm_xlo);
       }
-      int s = 0, i = 0;
-      uint32_t ph = 0, seg = 0;
-      for (int u = grp; u < units; u += ngrp, ++seg) {
-        const int slice = u / qunits, qt = qtile_of(u);
-        const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
-        if (!SQ) {
-          mbar_wait(a_empty, (seg & 1) ^ 1);           // previous query tile retired
+    }
+    __syncwarp();
+    const bool loads_on = !(work.drain_only & 2);
+    int s = 0, i = 0;
+    uint32_t ph = 0, seg = 0;
+    for (int u = grp; u < units; u += ngrp, ++seg) {
+      const int slice = u / qunits, qt = qtile_of(u);
+      const int t0 = work.t0 + slice * work.tps, t1 = min(work.T, t0 + work.tps);
+      if (!SQ) {
+        mbar_wait(a_empty, (seg & 1) ^ 1);           // previous query tile retired
+        if (elect_one_sync()) {
           mbar_expect_tx(a_full, Cfg::kMats * nkb * Cfg::kABlock);
           for (int kb = 0; kb < nkb; ++kb) {
             tma_load_2d(a_base + (size_t)kb * Cfg::kABlock, &tm_qhi, a_full, kb * kTcKB,
@@ -243,9 +248,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
                           kb * kTcKB, qt * kTcM);
           }
         }
-        for (int t = t0; t < t1; ++t, ++i) {
-          const int e = i & 1;
-          mbar_wait(&eempty[e], ((i >> 1) & 1) ^ 1);
+        __syncwarp();
+      }
+      for (int t = t0; t < t1; ++t, ++i) {
+        const int e = i & 1;
+        mbar_wait(&eempty[e], ((i >> 1) & 1) ^ 1);
+        if (elect_one_sync()) {
           mbar_expect_tx(&efull[e], kTcBExt);
           if (MC)
             bulk_load_mc(bext + e * kTcBExt + rank * (kTcBExt / 2),
@@ -253,24 +261,30 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
                          &efull[e], 3);
           else
             bulk_load(bext + e * kTcBExt, xext + (size_t)t * kTcBExt, kTcBExt, &efull[e]);
-          for (int kb = 0; kb < nkb; ++kb) {
-            if (SQ) {
-              // query k-block (hi, lo) into one ring stage
-              mbar_wait(&empty[s], ph ^ 1);
+        }
+        __syncwarp();
+        for (int kb = 0; kb < nkb; ++kb) {
+          if (SQ) {
+            // query k-block (hi, lo) into one ring stage
+            mbar_wait(&empty[s], ph ^ 1);
+            if (elect_one_sync()) {
               mbar_expect_tx(&full[s], Cfg::kMats * Cfg::kABlock);
               uint8_t* qs = b_base + (size_t)s * Cfg::kBBlock;
               tma_load_2d(qs, &tm_qhi, &full[s], kb * kTcKB, qt * kTcM);
               if (Cfg::kMats == 2)
                 tma_load_2d(qs + Cfg::kABlock, &tm_qlo, &full[s], kb * kTcKB, qt * kTcM);
-              if (++s == S) {
-                s = 0;
-                ph ^= 1;
-              }
             }
+            __syncwarp();
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
 #pragma unroll
-            for (int mat = 0; mat < Cfg::kMats; ++mat) {
-              mbar_wait(&empty[s], ph ^ 1);
-              if (work.drain_only & 2) {
+          for (int mat = 0; mat < Cfg::kMats; ++mat) {
+            mbar_wait(&empty[s], ph ^ 1);
+            if (elect_one_sync()) {
+              if (!loads_on) {
                 mbar_arrive(&full[s]);
               } else {
                 mbar_expect_tx(&full[s], Cfg::kBBlock);
@@ -282,10 +296,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
                   tma_load_2d(b_base + (size_t)s * Cfg::kBBlock, mat ? &tm_xlo : &tm_xhi,
                               &full[s], kb * kTcKB, t * kTcN);
               }
-              if (++s == S) {
-                s = 0;
-                ph ^= 1;
-              }
+            }
+            __syncwarp();
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
             }
           }
         }
