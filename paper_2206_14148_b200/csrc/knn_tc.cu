@@ -40,7 +40,7 @@ constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
 constexpr int kTcMaxDpad = 128;  // up to here the query tile stays resident in smem
 constexpr int kTcMaxDpadSQ = 1024;  // beyond: query k-blocks streamed with the database
 constexpr int kTcStages = 4;     // 32 KB database k-blocks in flight
-constexpr int kTcStagesSQ = 6;   // streamed-query ring: [q hi|lo], [x hi], [x lo] per k-block
+constexpr int kTcStagesSQ = 5;   // streamed-query ring: [q hi|lo], [x hi], [x lo] per k-block
 constexpr int kTcExtK = 16;      // augmented K block carrying -||x||^2
 constexpr uint32_t kTcAExt = kTcM * kTcExtK * 2;   // 4 KB  [128 x 16] bf16
 constexpr uint32_t kTcBExt = kTcN * kTcExtK * 2;   // 8 KB  [256 x 16] bf16
@@ -52,10 +52,13 @@ struct TcCfg {
   static constexpr int kMats = PASSES == 3 ? 2 : 1;            // hi (+ lo)
   static constexpr uint32_t kABlock = kTcM * 128;               // 16 KB
   static constexpr uint32_t kBBlock = kTcN * 128;               // 32 KB (one ring stage)
-  static constexpr int kStages = SQ ? kTcStagesSQ : kTcStages;
+  // (tc3 keeps two resident query planes: three stages fit beside them)
+  static constexpr int kStages = SQ ? kTcStagesSQ : (PASSES == 3 ? 3 : kTcStages);
+  // every ring stage has an 8 KB slot for the tile's -||x||^2 block, which
+  // rides with the tile's first database stage (one barrier pair for both)
   static size_t smem_bytes(int nkb) {
     return 1024 + (SQ ? 0 : (size_t)kMats * nkb * kABlock) + kTcAExt +
-           (size_t)kStages * kBBlock + 2 * kTcBExt + (2 * kStages + 10) * 8 + 16;
+           (size_t)kStages * (kBBlock + kTcBExt) + (2 * kStages + 6) * 8 + 16;
   }
 };
 
@@ -142,8 +145,21 @@ struct TcWork {
 // MC: clusters of 2 CTAs on query tiles 2p, 2p+1 of the same database
 // slice; each CTA loads HALF of every database stage (and of the -||x||^2
 // block) and multicasts it to both, halving the L2->SM stream per CTA; a
-// stage is refilled only after both CTAs' MMAs released it (empty/eempty
+// stage is refilled only after both CTAs' MMAs released it (empty
 // count 2, multicast commits).  Accumulators and epilogues stay per CTA.
+// Timing study build (make TRACE=1 -> -DTB_TC_TRACE; never the product
+// library): clock64 stamps of the MMA issuer and of epilogue warp 2 for 64
+// tiles of each CTA's main launch, starting at tile TB_TC_DEBUG >> 8
+// (debug bit 16 enables), read back with tb_debug_tc_trace (tools/tc_trace.py).
+#ifdef TB_TC_TRACE
+__device__ unsigned long long g_tc_trace[148 * 2048];
+#define TB_TR(off, tile, k)                                                   \
+  if (trace && (tile) >= tr0 && (tile) < tr0 + 64)                            \
+  trace[(off) + ((tile) - tr0) * 8 + (k)] = (unsigned long long)clock64()
+#else
+#define TB_TR(off, tile, k)
+#endif
+
 template <int PASSES, int KC, bool SQ, bool F16, bool MC>
 __global__ void __launch_bounds__(kTcThreads, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
@@ -160,17 +176,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_base = smem;
   uint8_t* b_base = a_base + (SQ ? 0 : (size_t)Cfg::kMats * nkb * Cfg::kABlock);
-  uint8_t* bext = b_base + (size_t)S * Cfg::kBBlock;          // 2 x 8 KB
-  uint8_t* aext = bext + 2 * kTcBExt;                          // 4 KB
+  uint8_t* bext = b_base + (size_t)S * Cfg::kBBlock;          // S x 8 KB, one per stage
+  uint8_t* aext = bext + (size_t)S * kTcBExt;                  // 4 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(aext + kTcAExt);
   uint64_t* empty = full + S;
   uint64_t* a_full = empty + S;
   uint64_t* a_empty = a_full + 1;
   uint64_t* tfull = a_empty + 1;
   uint64_t* tempty = tfull + 2;
-  uint64_t* efull = tempty + 2;
-  uint64_t* eempty = efull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(eempty + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = MC ? (int)cluster_ctarank() : 0;
@@ -206,8 +220,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 32 * kTcEpiWarps);
-      mbar_init(&efull[b], 1);
-      mbar_init(&eempty[b], MC ? 2 : 1);
     }
     fence_mbar_init();
   }
@@ -217,6 +229,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   if (MC) cluster_sync();           // both CTAs' barriers exist before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#ifdef TB_TC_TRACE
+  unsigned long long* trace =
+      (work.drain_only & 16) && work.list0 == 2 ? g_tc_trace + (size_t)blockIdx.x * 2048 : nullptr;
+  const int tr0 = work.drain_only >> 8;
+#endif
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
@@ -251,18 +268,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         __syncwarp();
       }
       for (int t = t0; t < t1; ++t, ++i) {
-        const int e = i & 1;
-        mbar_wait(&eempty[e], ((i >> 1) & 1) ^ 1);
-        if (elect_one_sync()) {
-          mbar_expect_tx(&efull[e], kTcBExt);
-          if (MC)
-            bulk_load_mc(bext + e * kTcBExt + rank * (kTcBExt / 2),
-                         xext + (size_t)t * kTcBExt + rank * (kTcBExt / 2), kTcBExt / 2,
-                         &efull[e], 3);
-          else
-            bulk_load(bext + e * kTcBExt, xext + (size_t)t * kTcBExt, kTcBExt, &efull[e]);
-        }
-        __syncwarp();
         for (int kb = 0; kb < nkb; ++kb) {
           if (SQ) {
             // query k-block (hi, lo) into one ring stage
@@ -284,10 +289,23 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           for (int mat = 0; mat < Cfg::kMats; ++mat) {
             mbar_wait(&empty[s], ph ^ 1);
             if (elect_one_sync()) {
-              if (!loads_on) {
-                mbar_arrive(&full[s]);
-              } else {
+              // the tile's -||x||^2 block rides with its first database stage
+              const bool ext = kb == 0 && mat == 0;
+              if (ext) {
+                mbar_expect_tx(&full[s], kTcBExt + (loads_on ? Cfg::kBBlock : 0));
+                uint8_t* dst = bext + (size_t)s * kTcBExt;
+                if (MC)
+                  bulk_load_mc(dst + rank * (kTcBExt / 2),
+                               xext + (size_t)t * kTcBExt + rank * (kTcBExt / 2), kTcBExt / 2,
+                               &full[s], 3);
+                else
+                  bulk_load(dst, xext + (size_t)t * kTcBExt, kTcBExt, &full[s]);
+              } else if (loads_on) {
                 mbar_expect_tx(&full[s], Cfg::kBBlock);
+              } else {
+                mbar_arrive(&full[s]);
+              }
+              if (loads_on) {
                 if (MC)
                   tma_load_2d_mc(b_base + (size_t)s * Cfg::kBBlock + rank * (Cfg::kBBlock / 2),
                                  mat ? &tm_xlo : &tm_xhi, &full[s], kb * kTcKB,
@@ -330,13 +348,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       }
       for (int t = t0; t < t1; ++t, ++i) {
         const int buf = i & 1;
+        if (lane == 0) { TB_TR(0, i, 0); }
         mbar_wait(&tempty[buf], ((i >> 1) & 1) ^ 1);
-        mbar_wait(&efull[buf], (i >> 1) & 1);
-        tc_fence_after();
+        if (lane == 0) { TB_TR(0, i, 1); }
         const uint32_t d = tmem + buf * kTcN;
-        // acc = -||x||^2  (K = 16 augmented block, initialises the tile)
-        if (elect_one_sync()) mma_bf16(d, dext_a, dext_b + buf * (kTcBExt >> 4), idesc, 0);
-        __syncwarp();
         for (int kb = 0; kb < nkb; ++kb) {
           uint64_t ahi = da + (uint64_t)kb * kAStep;
           uint64_t alo = da + (uint64_t)(nkb + kb) * kAStep;
@@ -353,9 +368,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           }
           // stage x_hi: q_hi.x_hi (+ q_lo.x_hi)
           mbar_wait(&full[s], ph);
+          if (lane == 0) { TB_TR(0, i, 3 + kb); }
           tc_fence_after();
           uint64_t b0 = db + (uint64_t)s * kBStep;
           if (elect_one_sync()) {
+            // kb 0: acc = -||x||^2 first (K = 16 augmented block from this
+            // stage's ext slot, initialises the tile)
+            if (kb == 0) mma_bf16(d, dext_a, dext_b + (uint64_t)s * (kTcBExt >> 4), idesc, 0);
             if (mma_on) {
 #pragma unroll
               for (int kk = 0; kk < kTcKB / 16; ++kk) {   // 16 elements = 32 B = 2 units
@@ -396,11 +415,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             __syncwarp();
           }
         }
-        if (elect_one_sync()) {
-          if (MC) mma_commit_mc(&eempty[buf], 3); else mma_commit(&eempty[buf]);  // norm block may be replaced
-          mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
-        }
+        if (elect_one_sync()) mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
         __syncwarp();
+        if (lane == 0) { TB_TR(0, i, 7); }
       }
       if (!SQ) {
         if (elect_one_sync()) mma_commit(a_empty);         // query tile may be replaced
@@ -449,7 +466,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           pk = __ldcg(qpool + p_slot);
           gk = __ldcg(gthr + q);
         }
+        if (ew == 0 && lane == 0) { TB_TR(1024, i, 0); }
         mbar_wait(&tfull[buf], (i >> 1) & 1);
+        if (ew == 0 && lane == 0) { TB_TR(1024, i, 1); }
         tc_fence_after();
         const uint32_t taddr =
             tmem + ((uint32_t)(quad * 32) << 16) + buf * kTcN + half * (kTcN / 2);
@@ -465,6 +484,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             // the MMA of tile i+2 may overwrite it while they are processed
             tc_fence_before();
             mbar_arrive(&tempty[buf]);
+            if (ew == 0 && lane == 0) { TB_TR(1024, i, 2); }
           }
           if (work.drain_only & 1) continue;
 #pragma unroll
@@ -486,6 +506,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         }
         // publish the running K'-th score every tile: the other column half
         // and every other CTA on this query tighten their thresholds with it
+        if (ew == 0 && lane == 0) { TB_TR(1024, i, 3); }
         if (qv && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst() * sc_inv));
       }
       // unit done: publish this (slice, column half)'s candidates
@@ -1042,3 +1063,9 @@ int tc_dispatch(int passes, int cand, const CUtensorMap& mqh, const CUtensorMap&
 }
 
 }  // namespace tb
+
+#ifdef TB_TC_TRACE
+extern "C" __attribute__((visibility("default"))) int tb_debug_tc_trace(void* out) {
+  return (int)cudaMemcpyFromSymbol(out, tb::g_tc_trace, sizeof(tb::g_tc_trace));
+}
+#endif

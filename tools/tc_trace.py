@@ -10,6 +10,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
+import paper_2206_14148_b200._lib as _L
+_L.LIB_PATH = os.path.join(os.path.dirname(_L.LIB_PATH), "libtb_pairwise_trace.so")   # make -C ... trace
+
 extra = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 t0 = int(sys.argv[2]) if len(sys.argv) > 2 else 0       # first traced tile of each CTA
 os.environ["TB_TC_DEBUG"] = str(16 | extra | (t0 << 8))
