@@ -39,8 +39,8 @@ ee = epi[:, sl]
 per_tile = np.diff(mma[:, sl, 0], axis=1)
 print(f"debug={16 | extra} tiles {t0}..{t0 + 63}  MMA issuer, cycles per tile (median over CTAs): "
       f"{np.median(per_tile):.0f}")
-names = ["wait tempty", "wait efull", "wait full kb0", "kb0->full kb1", "kb1->end(commit)"]
-segs = [mm[..., 1] - mm[..., 0], mm[..., 2] - mm[..., 1], mm[..., 3] - mm[..., 2],
+names = ["wait tempty", "wait full kb0", "kb0->full kb1", "kb1->end(commit)"]
+segs = [mm[..., 1] - mm[..., 0], mm[..., 3] - mm[..., 1],
         mm[..., 4] - mm[..., 3], mm[..., 7] - mm[..., 4]]
 for nm, sg in zip(names, segs):
     print(f"  {nm:18s} median {np.median(sg):7.0f}  mean {np.mean(sg):7.0f}")
