@@ -233,19 +233,22 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
     // phase A stage = one k-block, tiles [A2 B2 A1 B1 A0 B0];
-    // phase B stage = plane 0 of up to 3 k-blocks, tiles [A0 B0] x 3
-    if (lane == 0) {
-      tma_prefetch(&tm);
-      int s = 0;
-      uint32_t ph = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int ta, tb;
-        tile_of_unit(u, nt, ta, tb);
-        const int ra = ta * kI8Tile, rb = tb * kI8Tile;
-        for (int phase = 0; phase < 2; ++phase) {
-          const int step = phase ? 3 : 1;
-          for (int kb = 0; kb < nkb; kb += step) {
-            mbar_wait(&empty[s], ph ^ 1);
+    // phase B stage = plane 0 of up to 3 k-blocks, tiles [A0 B0] x 3.
+    // The whole warp runs the loop and one elected lane issues (uniform
+    // registers, no per-instruction broadcast loop), as in the issuer below.
+    if (elect_one_sync()) tma_prefetch(&tm);
+    __syncwarp();
+    int s = 0;
+    uint32_t ph = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int ta, tb;
+      tile_of_unit(u, nt, ta, tb);
+      const int ra = ta * kI8Tile, rb = tb * kI8Tile;
+      for (int phase = 0; phase < 2; ++phase) {
+        const int step = phase ? 3 : 1;
+        for (int kb = 0; kb < nkb; kb += step) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (elect_one_sync()) {
             if (dbg == 1) {
               mbar_arrive(&full[s]);
             } else {
@@ -267,39 +270,41 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
                 }
               }
             }
-            if (++s == S) {
-              s = 0;
-              ph ^= 1;
-            }
+          }
+          __syncwarp();
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
           }
         }
       }
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
-    // The issuing thread is the bottleneck of this kernel (a UTCIMMA issue
-    // costs about one MMA time, and every barrier wait + commit ~70 cycles
-    // on top), so: descriptors are precomputed (one 64-bit add per MMA) and
-    // each barrier handshake covers 16 MMAs (phase A) or 6 (phase B).
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_u8_s32(kI8Tile, kI8Tile);
-      const uint32_t acc0 = tmem, acc1 = tmem + 128, acc2 = tmem + 256, acc3 = tmem + 384;
-      // UMMA descriptor of stage s, tile j: d0 + s * kStageD + j * kTileD
-      // (16-byte units); the second K=32 step of a 64-byte row is +2
-      const uint64_t d0 = desc_k_sw64(smem_u32(smem));
-      constexpr uint64_t kStageD = kI8StageBytes >> 4, kTileD = kI8TileBytes >> 4;
-      int s = 0;
-      uint32_t ph = 0;
-      int i = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-        mbar_wait(tempty, (i & 1) ^ 1);
+    // Issue rate is this kernel's limiter (64-cycle MMAs), so: the whole
+    // warp runs the loop (waits included) and one elected lane issues from
+    // uniform registers - each MMA is one 64-bit add of a precomputed UMMA
+    // descriptor, with no per-instruction register->uniform broadcast loop -
+    // and each barrier handshake covers 16 MMAs (phase A) or 6 (phase B).
+    constexpr uint32_t idesc = idesc_u8_s32(kI8Tile, kI8Tile);
+    const uint32_t acc0 = tmem, acc1 = tmem + 128, acc2 = tmem + 256, acc3 = tmem + 384;
+    // UMMA descriptor of stage s, tile j: d0 + s * kStageD + j * kTileD
+    // (16-byte units); the second K=32 step of a 64-byte row is +2
+    const uint64_t d0 = desc_k_sw64(smem_u32(smem));
+    constexpr uint64_t kStageD = kI8StageBytes >> 4, kTileD = kI8TileBytes >> 4;
+    int s = 0;
+    uint32_t ph = 0;
+    int i = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      mbar_wait(tempty, (i & 1) ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint64_t a2 = d0 + (uint64_t)s * kStageD, b2 = a2 + kTileD;
-          const uint64_t a1 = a2 + 2 * kTileD, b1 = a2 + 3 * kTileD;
-          const uint64_t a0 = a2 + 4 * kTileD, b0 = a2 + 5 * kTileD;
+        const uint64_t a2 = d0 + (uint64_t)s * kStageD, b2 = a2 + kTileD;
+        const uint64_t a1 = a2 + 2 * kTileD, b1 = a2 + 3 * kTileD;
+        const uint64_t a0 = a2 + 4 * kTileD, b0 = a2 + 5 * kTileD;
+        if (elect_one_sync()) {
           if (dbg != 2) {
             const uint32_t acc = kb ? 1u : 0u;
             mma_i8(acc0, a2, b2, idesc, acc);
@@ -320,19 +325,23 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
             mma_i8(acc3, a0 + 2, b1 + 2, idesc, 1);
           }
           mma_commit(&empty[s]);
-          if (++s == S) {
-            s = 0;
-            ph ^= 1;
-          }
         }
-        mma_commit(tfull_a);
-        mbar_wait(acc0_free, i & 1);
+        __syncwarp();
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      if (elect_one_sync()) mma_commit(tfull_a);
+      __syncwarp();
+      mbar_wait(acc0_free, i & 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; kb += 3) {
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        for (int kb = 0; kb < nkb; kb += 3) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint64_t a = d0 + (uint64_t)s * kStageD;
-          const int nk = min(3, nkb - kb);
+        const uint64_t a = d0 + (uint64_t)s * kStageD;
+        const int nk = min(3, nkb - kb);
+        if (elect_one_sync()) {
           if (dbg != 2) {
             for (int j = 0; j < nk; ++j) {
               const uint64_t aj = a + 2 * j * kTileD, bj = aj + kTileD;
@@ -341,13 +350,15 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
             }
           }
           mma_commit(&empty[s]);
-          if (++s == S) {
-            s = 0;
-            ph ^= 1;
-          }
         }
-        mma_commit(tfull_b);
+        __syncwarp();
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
       }
+      if (elect_one_sync()) mma_commit(tfull_b);
+      __syncwarp();
     }
   } else {
     // ---------------------------------------------------------- epilogue
