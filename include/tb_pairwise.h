@@ -110,7 +110,8 @@ TB_API int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int
                 int64_t max_chunk_rows, tb_knn_plan* plan);
 
 /* Replaces evaluate(knn_graph, [x, q], budget) (interpreter.py:522-551) for
- * the kNN graph family: x[n,d], q[m,d] (plan dtype) -> out_dist[m,k]
+ * the kNN graph family: x[n,d], q[m,d] (plan dtype, C-contiguous, 16-byte
+ * aligned base pointers; TB_ERR_ARG otherwise) -> out_dist[m,k]
  * (plan out_dtype, squared L2 as the reference's rewritten graph computes,
  * match_replace.py:149-155) and out_idx[m,k] (int64, + index_base so a
  * database shard reports global indices).  Asynchronous on `stream`. */

@@ -313,6 +313,10 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
   if (p->m == 0) return TB_OK;
   if (!x || !q || !out_dist || !out_idx || !workspace)
     return fail(TB_ERR_ARG, "null buffer passed to tb_knn_run");
+  // the row kernels read x and q with 16-byte vector loads; a misaligned
+  // view (e.g. buf[1:] of a float tensor) would fault the whole context
+  if (((uintptr_t)x | (uintptr_t)q) & 15)
+    return fail(TB_ERR_ARG, "x and q must be 16-byte aligned (copy the view into a fresh buffer)");
   if (workspace_bytes < p->workspace_bytes)
     return fail(TB_ERR_ARG, "workspace smaller than plan->workspace_bytes");
   std::string why;

@@ -1421,19 +1421,21 @@ __global__ void topk_merge_kernel(const T* __restrict__ dl,
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= m) return;
-  TopList<T, KC> L;
+  // int64 global indices end to end: index_base + local may pass 2^31 on a
+  // sharded database, and ties must still resolve to the lower global index
+  TopList<T, KC, int64_t> L;
   L.init();
   for (int l = lane; l < lists; l += 32) {
     const T* s = dl + ((int64_t)l * m + r) * k;
     const int64_t* ix = il + ((int64_t)l * m + r) * k;
     for (int p = 0; p < k; ++p) {
       const T v = s[p];
-      const int j = (int)ix[p];
+      const int64_t j = ix[p];
       if (!lex_less(v, j, L.worst(), L.worst_idx())) break;
       L.insert(v, j);
     }
   }
-  warp_drain(L, k, [&](int t, T v, int j) {
+  warp_drain(L, k, [&](int t, T v, int64_t j) {
     od[r * k + t] = v;
     oi[r * k + t] = j;
   });

@@ -33,45 +33,51 @@ int fail(int code, const std::string& msg);
   } while (0)
 
 constexpr int kInvalidIdx = INT_MAX;
+// invalid-slot marker per index type (the cross-shard merge keeps int64
+// global indices: index_base + local can pass 2^31 on a sharded database)
+template <typename I>
+__host__ __device__ constexpr I invalid_idx() {
+  return sizeof(I) == 8 ? (I)INT64_MAX : (I)INT_MAX;
+}
 
 // ------------------------------------------------------- (score, index) --
 // Ordering used everywhere: ascending score, ties -> lower index
 // (the reference TopK's stable argsort, interpreter.py:379-381).
-template <typename S>
-__device__ __forceinline__ bool lex_less(S a, int ia, S b, int ib) {
+template <typename S, typename I>
+__device__ __forceinline__ bool lex_less(S a, I ia, S b, I ib) {
   // non-short-circuit: compiles to compares + one predicate op, no branches
   return (a < b) | ((a == b) & (ia < ib));
 }
 
 // Sorted top-K list held in registers (fully unrolled -> no local memory).
-template <typename S, int K>
+template <typename S, int K, typename I = int>
 struct TopList {
   S s[K];
-  int i[K];
+  I i[K];
 
   __device__ __forceinline__ void init() {
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       s[p] = (S)INFINITY;
-      i[p] = kInvalidIdx;
+      i[p] = invalid_idx<I>();
     }
   }
   __device__ __forceinline__ S worst() const { return s[K - 1]; }
-  __device__ __forceinline__ int worst_idx() const { return i[K - 1]; }
+  __device__ __forceinline__ I worst_idx() const { return i[K - 1]; }
 
   // Insert (v, j); caller guarantees (v, j) < (s[K-1], i[K-1]).
   // Branch-free parallel network on the OLD list: c[p] = (v,j) < entry p;
   // slot p takes entry p-1 if c[p-1] (shift down), else (v,j) if c[p],
   // else keeps its entry.  All K compares are independent (ILP, no
   // divergence-serialised branch chain).
-  __device__ __forceinline__ void insert(S v, int j) {
+  __device__ __forceinline__ void insert(S v, I j) {
     bool c[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) c[p] = lex_less(v, j, s[p], i[p]);
 #pragma unroll
     for (int p = K - 1; p > 0; --p) {
       const S ns = c[p - 1] ? s[p - 1] : (c[p] ? v : s[p]);
-      const int ni = c[p - 1] ? i[p - 1] : (c[p] ? j : i[p]);
+      const I ni = c[p - 1] ? i[p - 1] : (c[p] ? j : i[p]);
       s[p] = ns;
       i[p] = ni;
     }
@@ -83,14 +89,14 @@ struct TopList {
   // Insert (v, j) when j is larger than every index in the list (columns
   // scanned in ascending order): a score tie then ranks after the entry,
   // so the lexicographic compare reduces to one strict float compare.
-  __device__ __forceinline__ void insert_after(S v, int j) {
+  __device__ __forceinline__ void insert_after(S v, I j) {
     bool c[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) c[p] = v < s[p];
 #pragma unroll
     for (int p = K - 1; p > 0; --p) {
       const S ns = c[p - 1] ? s[p - 1] : (c[p] ? v : s[p]);
-      const int ni = c[p - 1] ? i[p - 1] : (c[p] ? j : i[p]);
+      const I ni = c[p - 1] ? i[p - 1] : (c[p] ? j : i[p]);
       s[p] = ns;
       i[p] = ni;
     }
@@ -99,7 +105,7 @@ struct TopList {
       i[0] = j;
     }
   }
-  __device__ __forceinline__ void offer(S v, int j) {
+  __device__ __forceinline__ void offer(S v, I j) {
     if (lex_less(v, j, s[K - 1], i[K - 1])) insert(v, j);
   }
   // remove the head (smallest); shifts the rest up
@@ -110,7 +116,7 @@ struct TopList {
       i[p] = i[p + 1];
     }
     s[K - 1] = (S)INFINITY;
-    i[K - 1] = kInvalidIdx;
+    i[K - 1] = invalid_idx<I>();
   }
 };
 
@@ -135,12 +141,12 @@ __device__ __forceinline__ void insert_masked(TopList<float, K>& L, const float 
 
 // Warp-wide lexicographic argmin of per-lane (v, j); returns the winner in
 // every lane.
-template <typename S>
-__device__ __forceinline__ void warp_lex_min(S& v, int& j) {
+template <typename S, typename I>
+__device__ __forceinline__ void warp_lex_min(S& v, I& j) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const S ov = __shfl_xor_sync(0xffffffffu, v, o);
-    const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+    const I oj = __shfl_xor_sync(0xffffffffu, j, o);
     if (lex_less(ov, oj, v, j)) {
       v = ov;
       j = oj;
@@ -150,14 +156,14 @@ __device__ __forceinline__ void warp_lex_min(S& v, int& j) {
 
 // Drains `count` smallest entries of the per-lane sorted lists (warp-wide
 // k-way merge).  out(t, v, j) is called by lane 0 for t = 0..count-1.
-template <typename S, int K, typename Out>
-__device__ __forceinline__ void warp_drain(TopList<S, K>& L, int count, Out out) {
+template <typename S, int K, typename I, typename Out>
+__device__ __forceinline__ void warp_drain(TopList<S, K, I>& L, int count, Out out) {
   const int lane = threadIdx.x & 31;
   for (int t = 0; t < count; ++t) {
     S v = L.s[0];
-    int j = L.i[0];
+    I j = L.i[0];
     warp_lex_min(v, j);
-    if (L.i[0] == j && L.s[0] == v && j != kInvalidIdx) L.pop();
+    if (L.i[0] == j && L.s[0] == v && j != invalid_idx<I>()) L.pop();
     if (lane == 0) out(t, v, j);
   }
 }

@@ -143,6 +143,9 @@ class KnnOperator:
                 raise EvaluationError(f"{name} dtype {t.dtype} != planned {self.dtype}")
             if not t.is_cuda or not t.is_contiguous():
                 raise EvaluationError(f"{name} must be a contiguous CUDA tensor")
+            if t.data_ptr() % 16:
+                raise EvaluationError(f"{name} must start on a 16-byte boundary "
+                                      "(clone() the view)")
         self._check_cosine(x, q)
         dist, idx = out if out is not None else self.alloc_outputs()
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -240,7 +243,10 @@ def knn(x, q, k: int, *, metric: str = "l2", memory_limit=None, engine: str = "a
         xs = torch.from_numpy(np.ascontiguousarray(x)).to(op.device)
         qs = torch.from_numpy(np.ascontiguousarray(q)).to(op.device)
     else:
-        xs, qs = x.contiguous(), q.contiguous()
+        # the kernels need 16-byte aligned rows bases (tb_pairwise.h); a view
+        # with an odd storage offset is copied into a fresh allocation
+        xs, qs = (t.contiguous() for t in (x, q))
+        xs, qs = (t if t.data_ptr() % 16 == 0 else t.clone() for t in (xs, qs))
     dist, idx = op.run(xs, qs, index_base=index_base)
     if host:
         dist, idx = dist.cpu().numpy(), idx.cpu().numpy()

@@ -325,6 +325,49 @@ def test_topk_merge_abi():
     assert rel_err(od.cpu().numpy(), ref_d) < 1e-12
 
 
+def test_topk_merge_keeps_int64_global_indices():
+    """Shards far into an 8-GPU database: global indices past 2^31 survive
+    the merge unchanged and exact-score ties still resolve to the lower
+    global index (reference TopK tie rule, interpreter.py:379-381)."""
+    torch = _torch()
+    from paper_2206_14148_b200 import distributed
+    m, k, L = 7, 5, 3
+    base = np.array([3_000_000_000, 2_147_483_000, 5_000_000_123], np.int64)
+    rng = np.random.default_rng(12)
+    d = np.sort(rng.integers(0, 6, size=(L, m, k)).astype(np.float64), axis=2)   # many ties
+    i = np.empty((L, m, k), np.int64)
+    for l in range(L):
+        i[l] = base[l] + np.sort(rng.choice(1000, size=(m, k), replace=True), axis=1) * 3 + \
+            np.arange(k)
+    od, oi = distributed.merge_topk(torch.from_numpy(d).cuda(), torch.from_numpy(i).cuda())
+    dd = d.transpose(1, 0, 2).reshape(m, L * k)
+    ii = i.transpose(1, 0, 2).reshape(m, L * k)
+    for r in range(m):
+        order = np.lexsort((ii[r], dd[r]))[:k]
+        assert np.array_equal(oi.cpu().numpy()[r], ii[r, order])
+        assert np.array_equal(od.cpu().numpy()[r], dd[r, order])
+
+
+def test_misaligned_views_are_rejected_or_copied():
+    """Row kernels read x, q with 16-byte vector loads: the operator rejects
+    a view that does not start on a 16-byte boundary (instead of faulting
+    the context) and the functional knn() copies it."""
+    torch = _torch()
+    rng = np.random.default_rng(13)
+    x = rng.standard_normal((2000, 32)).astype(np.float32)
+    q = rng.standard_normal((40, 32)).astype(np.float32)
+    buf = torch.empty(2000 * 32 + 1, dtype=torch.float32, device="cuda")
+    xv = buf[1:].view(2000, 32)
+    xv.copy_(torch.from_numpy(x))
+    qd = torch.from_numpy(q).cuda()
+    op = neighbors.KnnOperator(2000, 40, 32, 5)
+    with pytest.raises(tb.EvaluationError):
+        op.run(xv, qd)
+    d, i = tb.knn(xv, qd, 5)
+    ref_d, ref_i = oknn.exact(x, q, 5)
+    check(d.cpu().numpy(), i.cpu().numpy(), ref_d, ref_i, x, q)
+
+
 @pytest.mark.parametrize("chunk", [0, 2048, 777])
 def test_run_host_pipelined_matches_device_run(chunk):
     """tb_knn_run_host (host buffers, per-chunk H2D overlapped with compute)
@@ -470,3 +513,69 @@ def test_nccl_process_group_world1():
         check(dh.numpy(), ih.numpy() - 4000, sd, si, x[4000:], q)
     finally:
         dist.destroy_process_group()
+
+
+def _near_margin_case(d, seed, n_bg=40000, m=48, planted=40):
+    """Background N(0, 1) rows plus, for every query, `planted` rows at
+    controlled squared distances r0 + j * delta (j = 0..planted-1) below the
+    query's nearest background distance, with delta swept over six decades
+    (1e-6 .. 10 of r0): the k-th and K'-th candidate scores are then placed
+    from far inside to far outside the engine's error bound E, and with
+    small delta many candidates fall inside one rounding interval."""
+    rng = np.random.default_rng(seed)
+    xb = rng.standard_normal((n_bg, d)).astype(np.float32)
+    q = rng.standard_normal((m, d)).astype(np.float32)
+    bg_d, _ = oknn.exact(xb, q, 1)
+    rows = []
+    for r in range(m):
+        r0 = 0.25 * float(bg_d[r, 0])
+        delta = r0 * 10.0 ** (-6 + (r % 7))
+        delta = min(delta, 0.5 * (float(bg_d[r, 0]) - r0) / planted)
+        u = rng.standard_normal((planted, d))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        rad = np.sqrt(r0 + delta * np.arange(planted))
+        rows.append(q[r].astype(np.float64) + rad[:, None] * u)
+    x = np.concatenate([xb, np.concatenate(rows).astype(np.float32)])
+    perm = rng.permutation(x.shape[0])           # planted rows spread over all tiles
+    return x[perm], q
+
+
+@pytest.mark.parametrize("engine", ["tc1", "tc3"])
+@pytest.mark.parametrize("d", [16, 128, 784])
+def test_certification_near_margin_is_exact(engine, d):
+    """Adversarial certification (capi.cu error model): candidates placed at
+    controlled gaps around the bound E.  Every returned answer - certified
+    by T* - E > exact k-th or recomputed by the exact fallback - must equal
+    the fp64 oracle exactly (indices, ties to the lower index), and the
+    near-tie queries must actually take the fallback (the bound is live)."""
+    x, q = _near_margin_case(d, seed=100 + d, n_bg=40000 if d < 784 else 12000)
+    k = 10
+    ref_d, ref_i = oknn.exact(x, q, k)
+    res = tb.knn(x, q, k, engine=engine, return_result=True)
+    assert np.array_equal(res.idx, ref_i), np.nonzero((res.idx != ref_i).any(axis=1))
+    assert rel_err(res.dist, ref_d) < 1e-6
+    assert res.fallback_queries > 0            # the 1e-6 r0 spacings cannot be certified
+    assert res.fallback_queries < q.shape[0]   # the wide ones are
+
+
+@pytest.mark.parametrize("engine", ["tc1", "tc3"])
+def test_certification_scaled_duplicates(engine):
+    """Groups of rows at exactly equal distance (mirror images q +- v and
+    exact duplicates) straddling the k-th position: certification must hand
+    back the lower indices of the tie group, on both engines."""
+    rng = np.random.default_rng(21)
+    d, m = 64, 32
+    xb = rng.standard_normal((30000, d)).astype(np.float32)
+    q = np.round(rng.standard_normal((m, d)) * 8).astype(np.float32) / 8
+    rows = []
+    for r in range(m):
+        v = np.round(rng.standard_normal((6, d)) * 4) / 64      # exact in f32
+        rows += [q[r] + v, q[r] - v, q[r] + v]                  # 18 rows, 6 distances x 3
+    x = np.concatenate([xb, np.concatenate(rows).astype(np.float32)])
+    perm = rng.permutation(x.shape[0])
+    x = x[perm]
+    ref_d, ref_i = oknn.exact(x, q, 10)
+    d_, i_ = tb.knn(x, q, 10, engine=engine)
+    assert np.array_equal(i_, ref_i)
+    assert np.array_equal(d_.astype(np.float64), ref_d.astype(np.float32).astype(np.float64)) or \
+        rel_err(d_, ref_d) < 1e-7
