@@ -468,7 +468,7 @@ def run_ours(args):
         qh = q.cpu().pin_memory()
         op_h = neighbors.KnnOperator(rows, M_Q, DIM, K, dtype=np.float32, out_dtype=out_dtype,
                                      engine=args.engine, memory_limit=LIMIT, device=dev,
-                                     max_chunk_rows=-(-rows // 20))
+                                     max_chunk_rows=((rows + 19) // 20 + 255) // 256 * 256)
         staging = (x, q, out[0], out[1])      # device buffers refilled every step
         dh = torch.empty(out[0].shape, dtype=out[0].dtype).pin_memory()
         ih = torch.empty(out[1].shape, dtype=out[1].dtype).pin_memory()

@@ -198,8 +198,9 @@ int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int32_t me
   const int64_t limit = memory_limit > 0 ? memory_limit : INT64_MAX;
   int64_t chunk = tc ? std::min<int64_t>(n, (int64_t)1 << 22) : n;
   int64_t min_chunk = std::min<int64_t>(n, tile_rows);
-  if (max_chunk_rows > 0)
-    chunk = std::max(min_chunk, std::min(chunk, round_up(max_chunk_rows, tile_rows)));
+  if (max_chunk_rows > 0)   // a strict cap (whole tiles below it), at least one tile
+    chunk = std::max(min_chunk,
+                     std::min(chunk, std::max<int64_t>(tile_rows, max_chunk_rows / tile_rows * tile_rows)));
   for (;;) {
     const int64_t tiles = ceil_div(chunk, tile_rows);
     int slices = tc ? 1 : choose_slices(qt, tiles, ctas_per_sm, 512);

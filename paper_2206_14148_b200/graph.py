@@ -80,8 +80,10 @@ class TensorType:
 @dataclass(frozen=True)
 class PassConfig:
     """Same knobs and invariants as pipeline.py:18-41.  The fused path never
-    materialises a split candidate, so the threshold only caps the staging
-    chunk the planner may use (chunk bytes <= tensor_split_size)."""
+    materialises a split candidate; ``evaluate`` applies
+    ``tensor_split_size`` as a cap on the database slice each planner chunk
+    stages (rows x d x itemsize <= tensor_split_size, at least one 256-row
+    tile), the analogue of the splitter's slice bound (split.py:285-301)."""
 
     tensor_size_threshold: int = 10**9
     tensor_split_size: int | None = None
@@ -208,24 +210,57 @@ def _check_inputs(graph: Graph, inputs):
     return arrays
 
 
-def _trace_for(graph: Graph, resident: int, workspace: int, outputs: int) -> MemoryTrace:
-    tr = MemoryTrace()
-    live = 0
-    for i, p in enumerate(graph.parameters):
-        live += p.byte_size
-        tr.events.append(MemoryEvent(f"{graph.name}/param{i}", "alloc", p.byte_size, live))
-    live += outputs
-    tr.events.append(MemoryEvent(f"{graph.name}/outputs", "alloc", outputs, live))
-    live += workspace
-    tr.events.append(MemoryEvent(f"{graph.name}/workspace", "alloc", workspace, live))
-    tr.peak_live_bytes = live
-    for label, b in ((f"{graph.name}/workspace", workspace),
-                     *((f"{graph.name}/param{i}", p.byte_size)
-                       for i, p in enumerate(graph.parameters)),
-                     (f"{graph.name}/outputs", outputs)):
-        live -= b
-        tr.events.append(MemoryEvent(label, "free", b, live))
-    return tr
+class _DeviceLedger:
+    """Every device buffer ``evaluate`` allocates, as alloc / free events with
+    the live bytes measured on the device after each one (caching-allocator
+    bytes relative to the call's start) - the B200 counterpart of the
+    interpreter's allocation log (interpreter.py:57-76,149-167).  The C-ABI
+    library never allocates (the planner sizes one workspace), so these
+    events are the whole device footprint of the call.  ``poison`` fills a
+    buffer with 0xFF bytes (NaN for f32/f64) before it is released, like the
+    reference's ``poison_freed`` (interpreter.py:166-167): a kernel that read
+    a released buffer would then produce NaN instead of stale data."""
+
+    def __init__(self, device, poison: bool):
+        import torch
+        self._torch = torch
+        self.device = device
+        self.poison = poison
+        self.base = torch.cuda.memory_allocated(device)
+        self.trace = MemoryTrace()
+        self.held = {}
+
+    def _event(self, label: str, kind: str, nbytes: int):
+        live = self._torch.cuda.memory_allocated(self.device) - self.base
+        self.trace.events.append(MemoryEvent(label, kind, nbytes, live))
+        self.trace.peak_live_bytes = max(self.trace.peak_live_bytes, live)
+
+    def alloc(self, label: str, tensor):
+        self.held[label] = tensor
+        self._event(label, "alloc", tensor.numel() * tensor.element_size())
+        return tensor
+
+    def free(self, label: str):
+        t = self.held.pop(label)
+        nbytes = t.numel() * t.element_size()
+        if self.poison:
+            t.view(self._torch.uint8).fill_(0xFF)
+            self._torch.cuda.current_stream(self.device).synchronize()
+        del t
+        self._event(label, "free", nbytes)
+
+    def free_all(self):
+        for label in list(self.held):
+            self.free(label)
+
+
+def _split_cap_rows(graph: Graph, d: int, itemsize: int) -> int:
+    """PassConfig.tensor_split_size on the fused path: the largest database
+    slice one chunk may stage, in rows (pipeline.py:18-41, split.py:285-301
+    bound the splitter's slices the same way); at least one 256-row tile."""
+    if graph.config is None:
+        return 0
+    return max(256, int(graph.config.tensor_split_size) // (d * itemsize))
 
 
 def estimate_peak_memory(graph: Graph, budget: int | None = None) -> int:
@@ -322,37 +357,65 @@ def evaluate(graph: Graph, inputs, budget: int | None = None, *,
     ``graph`` is this package's descriptor or a reference-built graph object
     (see ``from_reference``).  Raises BudgetExceeded before any device
     allocation when the planner cannot fit ``budget`` (the reference raises
-    at the offending allocation, interpreter.py:149-151).
+    at the offending allocation, interpreter.py:149-151).  After
+    ``run_pipeline``, ``tensor_split_size`` caps the database slice each
+    chunk stages.  The trace lists every device buffer of the call with the
+    live bytes measured after each event; ``poison_freed`` overwrites each
+    buffer with NaN bytes before releasing it.
     """
+    import torch
     if not isinstance(graph, Graph):
         graph = from_reference(graph)
     arrays = _check_inputs(graph, inputs)
     from .errors import BudgetExceeded as _BE
+    dev = torch.device("cuda")
     if graph.kind == "knn":
         from . import neighbors as _knn
         a = graph.attrs
-        try:
-            res = _knn.knn(arrays[0], arrays[1], a["k"], metric=a["metric"],
-                           memory_limit=budget, return_result=True)
+        dt = a["dtype"].np_dtype
+        cap = _split_cap_rows(graph, a["d"], np.dtype(dt).itemsize)
+        try:                           # plan first: nothing is allocated on failure
+            op = _knn.KnnOperator(a["n"], a["m"], a["d"], a["k"], metric=a["metric"],
+                                  dtype=dt, memory_limit=budget, device=dev,
+                                  max_chunk_rows=cap, allocate=False)
         except _BE as exc:
             raise BudgetExceeded(graph.name, exc.requested, exc.live,
                                  MemoryTrace(), message=str(exc)) from None
-        p = res.plan
-        trace = _trace_for(graph, int(p.resident_bytes), int(p.workspace_bytes),
-                           int(p.output_bytes))
-        dt = a["dtype"].np_dtype
-        outs = (TensorValue(np.asarray(res.dist, dt).copy()),
-                TensorValue(np.asarray(res.idx).astype(dt)))
-        return outs, trace
+        led = _DeviceLedger(dev, poison_freed)
+        x = led.alloc(f"{graph.name}/param0", torch.from_numpy(arrays[0]).to(dev))
+        q = led.alloc(f"{graph.name}/param1", torch.from_numpy(arrays[1]).to(dev))
+        op._check_cosine(x, q)
+        ws = led.alloc(f"{graph.name}/workspace", op.allocate_workspace())
+        dist, idx = op.alloc_outputs()
+        led.alloc(f"{graph.name}/values", dist)
+        led.alloc(f"{graph.name}/indices", idx)
+        op.run(x, q, (dist, idx))
+        outs = (TensorValue(dist.cpu().numpy().astype(dt, copy=False)),
+                TensorValue(idx.cpu().numpy().astype(dt)))
+        del x, q, ws, dist, idx
+        op.workspace = None
+        led.free_all()
+        return outs, led.trace
     if graph.kind == "mvm":
         from . import mvm as _mvm
         spec = graph.attrs["spec"]
         x, y, v = arrays
-        total = sum(p.byte_size for p in graph.parameters) + graph.parameters[0].byte_size
+        n = graph.parameters[0].dims[0]
+        es = np.dtype(graph.attrs["dtype"].np_dtype).itemsize
+        # device bytes of the call: x, y in the operand dtype, v and the
+        # output in fp64 (the kernel accumulates and writes fp64)
+        total = 2 * n * es + 2 * n * 8
         if budget is not None and total > budget:
-            raise BudgetExceeded(f"{graph.name}/outputs", graph.parameters[0].byte_size,
-                                 total - graph.parameters[0].byte_size, MemoryTrace())
-        out = _mvm.se_kernel_mvm(x, y, v, spec.variance, spec.lengthscale)
-        trace = _trace_for(graph, 0, 0, graph.parameters[0].byte_size)
-        return TensorValue(np.asarray(out, graph.attrs["dtype"].np_dtype)), trace
+            raise BudgetExceeded(f"{graph.name}/outputs", n * 8, total - n * 8, MemoryTrace())
+        led = _DeviceLedger(dev, poison_freed)
+        xd = led.alloc(f"{graph.name}/param0", torch.from_numpy(x).to(dev))
+        yd = led.alloc(f"{graph.name}/param1", torch.from_numpy(y).to(dev))
+        vd = led.alloc(f"{graph.name}/param2", torch.from_numpy(np.asarray(v, np.float64)).to(dev))
+        out = _mvm.kernel_mvm(xd.reshape(-1, 1), yd.reshape(-1, 1), vd, "rbf", spec.variance,
+                              spec.lengthscale)
+        led.alloc(f"{graph.name}/output", out)
+        res = out.cpu().numpy().astype(graph.attrs["dtype"].np_dtype)
+        del xd, yd, vd, out
+        led.free_all()
+        return TensorValue(res), led.trace
     raise EvaluationError(f"no evaluator for graph kind {graph.kind!r}")

@@ -99,7 +99,7 @@ class KnnOperator:
 
     def __init__(self, n, m, d, k, *, metric="l2", dtype=np.float32, out_dtype=None,
                  engine="auto", memory_limit=None, device=None, resident_bytes=None,
-                 max_chunk_rows: int = 0):
+                 max_chunk_rows: int = 0, allocate: bool = True):
         torch = _torch()
         self.plan = plan(n, m, d, k, metric=metric, dtype=dtype, out_dtype=out_dtype,
                          engine=engine, memory_limit=memory_limit,
@@ -108,8 +108,14 @@ class KnnOperator:
         self.metric = metric
         self.dtype = np.dtype(dtype)
         self.out_dtype = np.dtype(out_dtype or dtype)
+        self.workspace = self.allocate_workspace() if allocate else None
+
+    def allocate_workspace(self):
+        """The planner-sized device workspace (the library never allocates)."""
+        torch = _torch()
         self.workspace = torch.empty(max(int(self.plan.workspace_bytes), 1),
                                      dtype=torch.uint8, device=self.device)
+        return self.workspace
 
     def _torch_dtype(self, dt):
         torch = _torch()

@@ -1,56 +1,68 @@
-"""Size literals with the reference's semantics (cli.py:33-68):
-decimal KB/MB/GB are powers of ten, KiB/MiB/GiB powers of two, bare digits
-are bytes.  ``memory_limit`` accepts these literals everywhere."""
+"""Byte-size literals for ``memory_limit`` and the CLI size flags.
+
+The accepted language is the reference's (cli.py:33-68): a
+non-negative number, optionally fractional, followed by an optional unit -
+``B``, decimal ``KB``/``MB``/``GB`` (powers of ten) or binary
+``KiB``/``MiB``/``GiB`` (powers of two), case-insensitive - that denotes a
+whole number of bytes; a unit-less literal must be a plain integer.  Parsing
+here is a single regular expression with exact decimal arithmetic.
+"""
 
 from __future__ import annotations
 
-_DECIMAL = {"B": 1, "KB": 10**3, "MB": 10**6, "GB": 10**9}
-_BINARY = {"KIB": 2**10, "MIB": 2**20, "GIB": 2**30}
-_ALL = sorted({**_DECIMAL, **_BINARY}.items(), key=lambda kv: -len(kv[0]))
+import re
+from decimal import Decimal, InvalidOperation
+
+_UNITS = {"": 1, "b": 1, "kb": 10**3, "mb": 10**6, "gb": 10**9,
+          "kib": 1 << 10, "mib": 1 << 20, "gib": 1 << 30}
+_LITERAL = re.compile(r"^\s*(?P<num>\d+(?:\.\d*)?|\.\d+)\s*(?P<unit>[kmg]i?b|b)?\s*$",
+                      re.IGNORECASE)
+# rendering order: decimal units first, then binary, largest first
+_RENDER = (("GB", 10**9), ("MB", 10**6), ("KB", 10**3),
+           ("GiB", 1 << 30), ("MiB", 1 << 20), ("KiB", 1 << 10))
 
 
 def parse_size(text) -> int:
-    """'1GB' -> 10**9, '64MiB' -> 64 * 2**20, bare digits -> bytes."""
+    """'1GB' -> 10**9, '64MiB' -> 64 * 2**20, '512' -> 512 (bytes)."""
     if isinstance(text, bool):
-        raise ValueError(f"malformed size literal {text!r}")
+        raise ValueError(f"not a size literal: {text!r}")
     if isinstance(text, int):
         if text < 0:
-            raise ValueError("sizes are non-negative")
+            raise ValueError("a size cannot be negative")
         return text
-    s = str(text).strip()
-    upper = s.upper()
-    for suffix, mult in _ALL:
-        if upper.endswith(suffix):
-            number = s[: len(s) - len(suffix)].strip()
-            if not number:
-                raise ValueError(f"missing number in size literal {text!r}")
-            result = float(number) * mult
-            if result != int(result) or result < 0:
-                raise ValueError(f"size literal {text!r} is not a whole byte count")
-            return int(result)
-    if not s.isdigit():
-        raise ValueError(f"malformed size literal {text!r}")
-    return int(s)
+    match = _LITERAL.match(str(text))
+    if match is None:
+        raise ValueError(f"not a size literal: {text!r}")
+    unit = (match.group("unit") or "").lower()
+    number = match.group("num")
+    if not unit and not number.isdigit():
+        raise ValueError(f"a size without a unit must be an integer byte count: {text!r}")
+    try:
+        value = Decimal(number) * _UNITS[unit]
+    except InvalidOperation as exc:                 # pragma: no cover - regex guards it
+        raise ValueError(f"not a size literal: {text!r}") from exc
+    if value != value.to_integral_value():
+        raise ValueError(f"{text!r} is a fraction of a byte")
+    return int(value)
 
 
 def format_size(nbytes: int) -> str:
-    """Largest suffix that divides exactly, preferring decimal."""
+    """Shortest exact literal: the largest unit that divides the count,
+    decimal before binary; plain bytes otherwise."""
     if nbytes < 0:
-        raise ValueError("sizes are non-negative")
-    for suffix, mult in (("GB", 10**9), ("MB", 10**6), ("KB", 10**3)):
-        if nbytes and nbytes % mult == 0:
-            return f"{nbytes // mult}{suffix}"
-    for suffix, mult in (("GiB", 2**30), ("MiB", 2**20), ("KiB", 2**10)):
-        if nbytes and nbytes % mult == 0:
-            return f"{nbytes // mult}{suffix}"
+        raise ValueError("a size cannot be negative")
+    for unit, scale in _RENDER:
+        q, r = divmod(nbytes, scale)
+        if nbytes and r == 0:
+            return f"{q}{unit}"
     return f"{nbytes}B"
 
 
 def as_limit(memory_limit) -> int:
-    """None -> 0 (unlimited), else parsed bytes (must be positive)."""
+    """None -> 0 (no limit), otherwise the parsed byte count (> 0)."""
     if memory_limit is None:
         return 0
-    v = parse_size(memory_limit)
-    if v <= 0:
+    nbytes = parse_size(memory_limit)
+    if nbytes <= 0:
         raise ValueError("memory_limit must be a positive byte count")
-    return v
+    return nbytes
