@@ -88,6 +88,36 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
                         void* workspace, int64_t workspace_bytes, cudaStream_t st,
                         void** events, int32_t n_events, void** ready, int32_t n_ready);
 
+namespace tb {
+int set_smem_once(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> done;   // (kernel, dev) -> bytes
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : done)
+    if (e.first.first == kernel && e.first.second == dev) {
+      if (e.second >= bytes) return TB_OK;
+      TB_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      e.second = bytes;
+      return TB_OK;
+    }
+  TB_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.push_back({{kernel, dev}, bytes});
+  return TB_OK;
+}
+}  // namespace tb
+
+// Per-device copy stream and event pool of tb_knn_run_host, created on first
+// use and kept for the process (stream and event creation are driver round
+// trips; the pool is held only while one call enqueues its work).
+struct HostCopyRes {
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> events;
+};
+static std::mutex g_copy_mu;
+static HostCopyRes g_copy_res[64];
+
 extern "C" {
 
 const char* tb_last_error(void) { return g_last_error.c_str(); }
@@ -260,17 +290,21 @@ int tb_knn_run_host(const tb_knn_plan* p, const void* x_host, const void* q_host
   const int64_t es = elem_size(p->dtype);
   // database chunk c is copied on a side stream; chunk c's compute waits only
   // for its own rows, so chunk c+1's host->device copy overlaps chunk c
-  cudaStream_t cp;
-  TB_CUDA_TRY(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
-  std::vector<cudaEvent_t> ready((size_t)p->n_chunks + 1);
-  int rc = TB_OK;
-  for (auto& e : ready) {
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
-      rc = fail(TB_ERR_CUDA, "cudaEventCreate failed");
-      break;
-    }
+  int dev = 0;
+  TB_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(TB_ERR_ARG, "device ordinal out of range");
+  std::lock_guard<std::mutex> lock(g_copy_mu);
+  HostCopyRes& res = g_copy_res[dev];
+  if (!res.stream) TB_CUDA_TRY(cudaStreamCreateWithFlags(&res.stream, cudaStreamNonBlocking));
+  while (res.events.size() < (size_t)p->n_chunks + 1) {
+    cudaEvent_t e;
+    TB_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    res.events.push_back(e);
   }
-  if (rc == TB_OK) {
+  cudaStream_t cp = res.stream;
+  std::vector<cudaEvent_t> ready(res.events.begin(), res.events.begin() + p->n_chunks + 1);
+  int rc = TB_OK;
+  {
     // the copy stream starts after the caller's prior work on `stream`
     cudaEventRecord(ready[p->n_chunks], st);
     cudaStreamWaitEvent(cp, ready[p->n_chunks], 0);
@@ -298,9 +332,6 @@ int tb_knn_run_host(const tb_knn_plan* p, const void* x_host, const void* q_host
                                                        cudaGetErrorString(e));
     }
   }
-  for (auto& e : ready)
-    if (e) cudaEventDestroy(e);
-  cudaStreamDestroy(cp);
   return rc;
 }
 

@@ -24,6 +24,8 @@
 // merge (knn_kernels.cu), so results are exact.
 #include <cudaTypedefs.h>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "tb_common.cuh"
 #include "knn_internal.h"
@@ -805,9 +807,33 @@ knn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_qhi,
 
 // ---------------------------------------------------------------- host --
 
+// Encoded maps are cached by (address, shape, box, type): the host-buffer
+// path launches the engine once per database chunk on the same workspace.
+struct MapKey {
+  const void* base;
+  uint64_t rows, cols;
+  uint32_t box_rows;
+  bool f16;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && rows == o.rows && cols == o.cols && box_rows == o.box_rows &&
+           f16 == o.f16;
+  }
+};
+static std::mutex g_map_mu;
+static std::vector<std::pair<MapKey, CUtensorMap>> g_maps;   // small LRU, newest last
+
 // bf16 [rows, cols] row-major, box [box_rows, 64], 128-B swizzle
 static int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                     uint32_t box_rows, bool f16 = false) {
+  const MapKey key{base, rows, cols, box_rows, f16};
+  {
+    std::lock_guard<std::mutex> lock(g_map_mu);
+    for (size_t i = 0; i < g_maps.size(); ++i)
+      if (g_maps[i].first == key) {
+        *map = g_maps[i].second;
+        return TB_OK;
+      }
+  }
   auto fn = tensor_map_encoder();
   if (!fn) return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {cols, rows};
@@ -821,6 +847,9 @@ static int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(TB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  std::lock_guard<std::mutex> lock(g_map_mu);
+  if (g_maps.size() >= 32) g_maps.erase(g_maps.begin());
+  g_maps.push_back({key, *map});
   return TB_OK;
 }
 
@@ -951,7 +980,7 @@ static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtenso
   const size_t smem = TcCfg<PASSES, SQ>::smem_bytes(nkb);
   if (F16 && mc) {
     auto kern = knn_tc_kernel<PASSES, KC, SQ, F16, true>;
-    TB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (int rc = set_smem_once((const void*)kern, (int)smem)) return rc;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kTcThreads);
@@ -967,8 +996,8 @@ static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtenso
     TB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, qh, ql, xh, xl, xext, work, (int)m, nkb, idx_base,
                                    cs, ci, gthr, f16p, gthr + m));
   } else {
-    TB_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<PASSES, KC, SQ, F16, false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (int rc = set_smem_once((const void*)knn_tc_kernel<PASSES, KC, SQ, F16, false>, (int)smem))
+      return rc;
     knn_tc_kernel<PASSES, KC, SQ, F16, false><<<grid, kTcThreads, smem, st>>>(
         qh, ql, xh, xl, xext, work, (int)m, nkb, idx_base, cs, ci, gthr, f16p, gthr + m);
   }

@@ -191,4 +191,9 @@ inline int64_t alloc_bytes(int64_t b) {
   return b <= ((int64_t)1 << 20) ? round_up(b, 512) : round_up(b, (int64_t)2 << 20);
 }
 
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device,
+// size): cudaFuncSetAttribute is a driver round trip, and the host-buffer
+// path launches the engines once per database chunk.
+int set_smem_once(const void* kernel, int bytes);
+
 }  // namespace tb
