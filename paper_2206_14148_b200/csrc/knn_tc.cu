@@ -42,7 +42,7 @@ constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
 constexpr int kTcMaxDpad = 128;  // up to here the query tile stays resident in smem
 constexpr int kTcMaxDpadSQ = 1024;  // beyond: query k-blocks streamed with the database
 constexpr int kTcStages = 4;     // 32 KB database k-blocks in flight
-constexpr int kTcStagesSQ = 5;   // streamed-query ring: [q hi|lo], [x hi], [x lo] per k-block
+constexpr int kTcStagesSQ = 6;   // streamed-query ring: [q hi|lo], [x hi], [x lo] per k-block
 constexpr int kTcExtK = 16;      // augmented K block carrying -||x||^2
 constexpr uint32_t kTcAExt = kTcM * kTcExtK * 2;   // 4 KB  [128 x 16] bf16
 constexpr uint32_t kTcBExt = kTcN * kTcExtK * 2;   // 8 KB  [256 x 16] bf16
@@ -56,11 +56,15 @@ struct TcCfg {
   static constexpr uint32_t kBBlock = kTcN * 128;               // 32 KB (one ring stage)
   // (tc3 keeps two resident query planes: three stages fit beside them)
   static constexpr int kStages = SQ ? kTcStagesSQ : (PASSES == 3 ? 3 : kTcStages);
-  // every ring stage has an 8 KB slot for the tile's -||x||^2 block, which
-  // rides with the tile's first database stage (one barrier pair for both)
+  // Resident queries: every ring stage has an 8 KB slot for the tile's
+  // -||x||^2 block, which rides with the tile's first database stage (one
+  // barrier pair for both).  Streamed queries keep the deeper 6-stage ring
+  // and a separate double-buffered ring for the norm block (kExtRing).
+  static constexpr bool kExtRing = SQ;
+  static constexpr int kExtSlots = kExtRing ? 2 : kStages;
   static size_t smem_bytes(int nkb) {
     return 1024 + (SQ ? 0 : (size_t)kMats * nkb * kABlock) + kTcAExt +
-           (size_t)kStages * (kBBlock + kTcBExt) + (2 * kStages + 6) * 8 + 16;
+           (size_t)kStages * kBBlock + (size_t)kExtSlots * kTcBExt + (2 * kStages + 10) * 8 + 16;
   }
 };
 
@@ -178,15 +182,17 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_base = smem;
   uint8_t* b_base = a_base + (SQ ? 0 : (size_t)Cfg::kMats * nkb * Cfg::kABlock);
-  uint8_t* bext = b_base + (size_t)S * Cfg::kBBlock;          // S x 8 KB, one per stage
-  uint8_t* aext = bext + (size_t)S * kTcBExt;                  // 4 KB
+  uint8_t* bext = b_base + (size_t)S * Cfg::kBBlock;          // kExtSlots x 8 KB
+  uint8_t* aext = bext + (size_t)Cfg::kExtSlots * kTcBExt;     // 4 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(aext + kTcAExt);
   uint64_t* empty = full + S;
   uint64_t* a_full = empty + S;
   uint64_t* a_empty = a_full + 1;
   uint64_t* tfull = a_empty + 1;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* efull = tempty + 2;       // kExtRing only
+  uint64_t* eempty = efull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(eempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = MC ? (int)cluster_ctarank() : 0;
@@ -222,6 +228,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 32 * kTcEpiWarps);
+      mbar_init(&efull[b], 1);
+      mbar_init(&eempty[b], MC ? 2 : 1);
     }
     fence_mbar_init();
   }
@@ -270,6 +278,20 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         __syncwarp();
       }
       for (int t = t0; t < t1; ++t, ++i) {
+        if (Cfg::kExtRing) {
+          const int e = i & 1;
+          mbar_wait(&eempty[e], ((i >> 1) & 1) ^ 1);
+          if (elect_one_sync()) {
+            mbar_expect_tx(&efull[e], kTcBExt);
+            if (MC)
+              bulk_load_mc(bext + e * kTcBExt + rank * (kTcBExt / 2),
+                           xext + (size_t)t * kTcBExt + rank * (kTcBExt / 2), kTcBExt / 2,
+                           &efull[e], 3);
+            else
+              bulk_load(bext + e * kTcBExt, xext + (size_t)t * kTcBExt, kTcBExt, &efull[e]);
+          }
+          __syncwarp();
+        }
         for (int kb = 0; kb < nkb; ++kb) {
           if (SQ) {
             // query k-block (hi, lo) into one ring stage
@@ -292,7 +314,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             mbar_wait(&empty[s], ph ^ 1);
             if (elect_one_sync()) {
               // the tile's -||x||^2 block rides with its first database stage
-              const bool ext = kb == 0 && mat == 0;
+              const bool ext = !Cfg::kExtRing && kb == 0 && mat == 0;
               if (ext) {
                 mbar_expect_tx(&full[s], kTcBExt + (loads_on ? Cfg::kBBlock : 0));
                 uint8_t* dst = bext + (size_t)s * kTcBExt;
@@ -354,6 +376,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         mbar_wait(&tempty[buf], ((i >> 1) & 1) ^ 1);
         if (lane == 0) { TB_TR(0, i, 1); }
         const uint32_t d = tmem + buf * kTcN;
+        if (Cfg::kExtRing) {
+          // acc = -||x||^2 from the norm-block ring (K = 16, initialises the tile)
+          mbar_wait(&efull[buf], (i >> 1) & 1);
+          tc_fence_after();
+          if (elect_one_sync()) mma_bf16(d, dext_a, dext_b + buf * (kTcBExt >> 4), idesc, 0);
+          __syncwarp();
+        }
         for (int kb = 0; kb < nkb; ++kb) {
           uint64_t ahi = da + (uint64_t)kb * kAStep;
           uint64_t alo = da + (uint64_t)(nkb + kb) * kAStep;
@@ -376,7 +405,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           if (elect_one_sync()) {
             // kb 0: acc = -||x||^2 first (K = 16 augmented block from this
             // stage's ext slot, initialises the tile)
-            if (kb == 0) mma_bf16(d, dext_a, dext_b + (uint64_t)s * (kTcBExt >> 4), idesc, 0);
+            if (!Cfg::kExtRing && kb == 0)
+              mma_bf16(d, dext_a, dext_b + (uint64_t)s * (kTcBExt >> 4), idesc, 0);
             if (mma_on) {
 #pragma unroll
               for (int kk = 0; kk < kTcKB / 16; ++kk) {   // 16 elements = 32 B = 2 units
@@ -417,7 +447,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             __syncwarp();
           }
         }
-        if (elect_one_sync()) mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
+        if (elect_one_sync()) {
+          if (Cfg::kExtRing) {                 // norm block may be replaced
+            if (MC) mma_commit_mc(&eempty[buf], 3); else mma_commit(&eempty[buf]);
+          }
+          mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
+        }
         __syncwarp();
         if (lane == 0) { TB_TR(0, i, 7); }
       }
