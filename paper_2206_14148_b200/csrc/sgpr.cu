@@ -327,6 +327,10 @@ kernel_mvm_fixed_kernel(const T* __restrict__ X, const T* __restrict__ Z,
   constexpr int TZ = 128;
   __shared__ double zs[TZ * D];
   __shared__ double ws[TZ];
+  // RBF: inputs pre-scaled by sqrt(1/2)/l so r2 is already -log of the
+  // kernel, and the variance multiplies the finished sum (17 fp64
+  // instructions per kernel evaluation instead of 19)
+  const double pre = KERN == TB_KERNEL_RBF ? 0.70710678118654752440 : 1.0;
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x * R + threadIdx.x;
   double xs[R][D], acc[R];
 #pragma unroll
@@ -334,12 +338,13 @@ kernel_mvm_fixed_kernel(const T* __restrict__ X, const T* __restrict__ Z,
     const int64_t i = i0 + (int64_t)r * blockDim.x;
     acc[r] = 0.0;
 #pragma unroll
-    for (int t = 0; t < D; ++t) xs[r][t] = i < n ? (double)X[i * D + t] * p.inv_ls[t] : 0.0;
+    for (int t = 0; t < D; ++t)
+      xs[r][t] = i < n ? (double)X[i * D + t] * (p.inv_ls[t] * pre) : 0.0;
   }
   for (int64_t z0 = 0; z0 < M; z0 += TZ) {
     __syncthreads();
     for (int e = threadIdx.x; e < TZ * D; e += blockDim.x)
-      zs[e] = z0 + e / D < M ? (double)Z[z0 * D + e] * p.inv_ls[e % D] : 0.0;
+      zs[e] = z0 + e / D < M ? (double)Z[z0 * D + e] * (p.inv_ls[e % D] * pre) : 0.0;
     for (int e = threadIdx.x; e < TZ; e += blockDim.x) ws[e] = z0 + e < M ? w[z0 + e] : 0.0;
     __syncthreads();
     const int lim = (int)((M - z0) < TZ ? (M - z0) : TZ);
@@ -358,7 +363,7 @@ kernel_mvm_fixed_kernel(const T* __restrict__ X, const T* __restrict__ Z,
         }
         double k;
         if (KERN == TB_KERNEL_RBF) {
-          k = p.variance * exp(-0.5 * r2);
+          k = exp(-r2);
         } else {
           const double rr = sqrt(fmax(r2, 1e-36));
           const double s3 = 1.7320508075688772 * rr;
@@ -371,14 +376,14 @@ kernel_mvm_fixed_kernel(const T* __restrict__ X, const T* __restrict__ Z,
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t i = i0 + (int64_t)r * blockDim.x;
-    if (i < n) out[i] = acc[r];
+    if (i < n) out[i] = KERN == TB_KERNEL_RBF ? p.variance * acc[r] : acc[r];
   }
 }
 
 template <typename T, int D>
 static bool launch_mvm_fixed(const void* X, const void* Z, const double* w, int64_t n, int64_t M,
                              const KernParams& kp, double* out, cudaStream_t st) {
-  constexpr int R = 2;
+  constexpr int R = D <= 4 ? 4 : 2;
   const unsigned blocks = (unsigned)ceil_div(n, 256 * R);
   if (kp.kernel == TB_KERNEL_RBF)
     kernel_mvm_fixed_kernel<T, D, TB_KERNEL_RBF, R><<<blocks, 256, 0, st>>>(
