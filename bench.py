@@ -145,6 +145,37 @@ def cpu_baseline(x: np.ndarray, q: np.ndarray, k: int, n_queries: int, threads: 
     return n_queries / dt, dt
 
 
+def _profile_json(name: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
+
+
+def host_info() -> dict:
+    """CPU model and the BLAS thread pool numpy uses (BASELINE.md §2 asks
+    for both next to a CPU number)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        pools = [p for p in threadpool_info() if p.get("user_api") == "blas"]
+        if pools:
+            blas = {"library": pools[0].get("internal_api"), "threads": pools[0].get("num_threads")}
+    except Exception:          # pragma: no cover - threadpoolctl missing
+        pass
+    return {"cpu_model": model, "blas": blas}
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -175,6 +206,7 @@ def sgpr_cpu_baseline(n_sample: int, threads: int):
     t_tail = time.perf_counter() - t0
     per_eval = t_stats * SG_N / n_sample + t_tail
     return {"value": 1.0 / per_eval, "unit": "elbo_evals/s", "cores": threads, "kind": "port",
+            **host_info(),
             "sample": f"Sigma/v/yy over {n_sample} of N={SG_N} points ({t_stats:.1f}s, "
                       f"linear in N) + fp64 tail ({t_tail:.1f}s): oracle/sgpr.py (GPflow 2.3.1 "
                       "SGPR restatement, numpy/OpenBLAS fp64)"}
@@ -224,12 +256,15 @@ def run_sgpr(args, dev, world, rank, dist):
         stats_ms, total_ms = (float(v) for v in t.tolist())
     useful = SG_N * SG_M * (SG_M + 1)
     achieved = useful / (stats_ms / 1e3) / 1e12
-    # denominator: INT8 dense MMA rate = 2x bf16 on sm_100 (tcgen05 kind::i8
-    # K=32 vs kind::f16 K=16 per instruction, verified by tools/probes/
-    # mma_probe.cu) of the measured bf16 sustained figure, / 9 u8 x u8 slice
-    # products per useful MAC (exact 24-bit fixed-point Gram)
-    peaks, peak_src = _peaks()
-    peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / 9.0
+    # denominator: the MEASURED sustained tcgen05 kind::i8 rate of the Gram's
+    # own instruction on all SMs (profiles/r02_i8_peak.json, tools/probes/
+    # i8_peak.py: >= 4 s under the power cap), / 9 u8 x u8 slice products per
+    # useful MAC (exact 24-bit fixed-point Gram); also against the i8 floor
+    # (16384 ops/cycle/SM) at the SM clock sampled during this run
+    i8 = _profile_json("r02_i8_peak.json") or {}
+    peak = i8.get("i8_tops_sustained", 3926.7) / 9.0
+    sm_mhz = (clocks or {}).get("sm_mhz") or 0.0
+    floor_at_clock = 16384 * 148 * sm_mhz * 1e6 / 1e12 / 9.0 if sm_mhz else None
     traffic, alg_bytes, rep = _traffic("sgpr_gram_i8")
     out = {"metric": "sgpr_elbo_evals_per_s", "value": 1e3 / total_ms, "unit": "elbo_evals/s",
            "ms_per_eval": total_ms, "stats_ms": stats_ms, "tail_ms": total_ms - stats_ms,
@@ -254,14 +289,103 @@ def run_sgpr(args, dev, world, rank, dist):
                         f"{alg_bytes} B",
                         "kernel": "sgpr_gram_i8 (exact fixed-point Gram on INT8 tcgen05) + "
                                   "overlapped kuf_quant; time = whole statistics pass",
-                        "peak_source": f"2 x {peak_src} bf16 sustained (INT8 rate) / 9 slice "
-                                       "products per useful MAC",
+                        "peak_source": "measured sustained tcgen05 kind::i8 "
+                                       f"({i8.get('i8_tops_sustained', 3926.7):.0f} TOPS, "
+                                       "profiles/r02_i8_peak.json) / 9 slice products per "
+                                       "useful MAC",
+                        "frac_of_i8_floor_at_run_clock": (achieved / floor_at_clock
+                                                          if floor_at_clock else None),
+                        "i8_issued_tops": 9.0 * achieved,
                         "frac_of_nominal": achieved / (4500.0 / 9.0),
                         "useful_flops": useful}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = sgpr_cpu_baseline(args.sgpr_cpu_n, host_cores())
     del m, X, y, Z
     return out
+
+
+# ---------------------------------------------------------------------------
+# Kernel MVM (the paper's §5.1 workload; reference
+# build_kernel_mvm, frontend.py:34-54): y = K v, K the n x n SE kernel over
+# 1-D inputs, n = 1e6, fp64.  Rows of K (x) are sharded over ranks.
+
+MV_N = 1_000_000
+MV_FP64_INST_PER_EVAL = 17     # counted in the SASS of kernel_mvm_fixed_kernel<double,1,RBF>
+
+
+def mvm_cpu_baseline(n_rows: int, threads: int):
+    """The reference's op order (oracle.mvm.se_mvm_reference, numpy) on a
+    bounded sample of rows against all n columns; rows are independent, so
+    MVM/s = evals/s / n^2."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import mvm as omvm
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, n_rows)
+    y = rng.uniform(-1, 1, MV_N)
+    v = rng.uniform(-1, 1, MV_N)
+    parts = [p for p in np.array_split(x, threads) if len(p)]
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=len(parts)) as ex:
+        list(ex.map(lambda p: omvm.se_mvm_reference(p, y, v, 1.0, 0.1, chunk=16), parts))
+    dt = time.perf_counter() - t0
+    evals = n_rows * MV_N / dt
+    return {"value": evals / MV_N ** 2, "unit": "mvm/s", "cores": len(parts), "kind": "port",
+            **host_info(),
+            "sample": f"{n_rows} of {MV_N} rows x all {MV_N} columns in {dt:.1f}s "
+                      f"({evals:.3e} kernel evaluations/s): oracle/mvm.py se_mvm_reference "
+                      "(reference op order, numpy fp64)"}
+
+
+def run_mvm(args, dev, world, rank, dist):
+    import torch
+
+    from paper_2206_14148_b200 import mvm
+    from paper_2206_14148_b200.distributed import shard_range
+    start, stop = shard_range(MV_N, rank, world)
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    x = (torch.rand((MV_N, 1), generator=g, device=dev, dtype=torch.float64) * 2 - 1)[start:stop]
+    y = torch.rand((MV_N, 1), generator=g, device=dev, dtype=torch.float64) * 2 - 1
+    v = torch.rand(MV_N, generator=g, device=dev, dtype=torch.float64) * 2 - 1
+    mvm.kernel_mvm(x[:4096].contiguous(), y, v, "rbf", 1.0, 0.1)          # warm-up
+    xs = x.contiguous()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record()
+    out = mvm.kernel_mvm(xs, y, v, "rbf", 1.0, 0.1)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    rows = stop - start
+    if dist is not None:
+        t = torch.tensor([ms, float(rows)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, rows = float(t[0].item()), int(t[1].item())
+    evals = rows * MV_N / (ms / 1e3)
+    fp64 = _profile_json("r02_fp64_peak.json") or {}
+    peak_inst = fp64.get("fp64_tflops", 36.97) / 2.0       # DFMA instructions/s (T)
+    achieved_inst = evals * MV_FP64_INST_PER_EVAL / 1e12
+    res = {"metric": "kernel_mvm_per_s", "value": 1e3 / ms, "unit": "mvm/s", "ms_per_mvm": ms,
+           "kernel_evals_per_s": evals, "checksum": float(out.sum().item()),
+           "config": {"workload": "se_kernel_mvm_n1e6_d1_f64", "n": MV_N, "dtype": "f64",
+                      "kernel": "squared exponential, variance 1, lengthscale 0.1",
+                      "parallelism": f"row-shard{world}",
+                      "memory": "O(n): K is never formed (the reference materialises 8 TB "
+                                "naive, 125-row slices at a 1 GB split)"},
+           "roofline": {"bound": "fp64", "achieved": achieved_inst, "peak": peak_inst,
+                        "unit": "T fp64-pipe instructions/s", "frac": achieved_inst / peak_inst,
+                        "kernel": "kernel_mvm_fixed_kernel<double, 1, RBF, 4>",
+                        "per_unit": f"{MV_FP64_INST_PER_EVAL} fp64 instructions per kernel "
+                                    "evaluation (SASS count: difference, square, exp range "
+                                    "reduction + 11-term polynomial, accumulate)",
+                        "peak_source": "measured DFMA rate (profiles/r02_fp64_peak.json, "
+                                       "tools/probes/fp64_peak_probe.cu)"}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = mvm_cpu_baseline(args.mvm_cpu_rows, host_cores())
+    return res
 
 
 def _forward_nccl_log():
@@ -345,6 +469,7 @@ def run_reference(args):
         "config": {"workload": WORKLOAD, "n": N_DB, "m": M_Q, "d": DIM, "k": K,
                    "memory_limit": LIMIT, "step_sample_queries": per_step},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         **host_info(),
                          "sample": f"{per_step} queries/step vs the full 1e6x128 db: "
                                    "tensorbudget pipelined kNN (expanded-form GEMM + full "
                                    "stable argsort, oracle/knn.py reference_port)"},
@@ -569,7 +694,7 @@ def run_ours(args):
         qs = q.cpu().numpy()
         nq = max(threads, args.cpu_queries)
         v, dt = cpu_baseline(xs, qs, K, nq, threads)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", **host_info(),
                "sample": f"{nq} queries vs the full 1e6x128 db in {dt:.1f}s "
                          "(tensorbudget pipelined kNN algorithm, oracle/knn.py)"}
 
@@ -578,6 +703,10 @@ def run_ours(args):
         del op
         torch.cuda.empty_cache()
         sgpr = run_sgpr(args, dev, world, rank, dist if use_dist else None)
+    mvm_line = None
+    if not args.no_mvm:
+        torch.cuda.empty_cache()
+        mvm_line = run_mvm(args, dev, world, rank, dist if use_dist else None)
 
     if rank == 0:
         line = {
@@ -604,6 +733,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "sgpr": sgpr,
+            "mvm": mvm_line,
         }
         print(json.dumps(line))
     if use_dist:
@@ -624,6 +754,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sgpr", action="store_true")
     ap.add_argument("--sgpr-cpu-n", type=int, default=16384)
+    ap.add_argument("--no-mvm", action="store_true")
+    ap.add_argument("--mvm-cpu-rows", type=int, default=2048)
     ap.add_argument("--dry-run", action="store_true",
                     help="launch plumbing only (gloo, no GPU work)")
     args = ap.parse_args()
