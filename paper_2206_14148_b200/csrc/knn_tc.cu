@@ -61,6 +61,10 @@ struct TcCfg {
   // barrier pair for both).  Streamed queries keep the deeper 6-stage ring
   // and a separate double-buffered ring for the norm block (kExtRing).
   static constexpr bool kExtRing = SQ;
+  // tc1 with resident queries: one barrier pair per TILE (all k-blocks of the
+  // tile and its norm block complete on the first stage's barriers), which
+  // halves the issuer's waits and commits at d_pad = 128; needs S % nkb == 0
+  static constexpr bool kTileBar = !SQ && PASSES == 1;
   static constexpr int kExtSlots = kExtRing ? 2 : kStages;
   static size_t smem_bytes(int nkb) {
     return 1024 + (SQ ? 0 : (size_t)kMats * nkb * kABlock) + kTcAExt +
@@ -278,6 +282,36 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         __syncwarp();
       }
       for (int t = t0; t < t1; ++t, ++i) {
+        if constexpr (Cfg::kTileBar) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (elect_one_sync()) {
+            mbar_expect_tx(&full[s], kTcBExt + (loads_on ? nkb * Cfg::kBBlock : 0));
+            uint8_t* dst = bext + (size_t)s * kTcBExt;
+            if (MC)
+              bulk_load_mc(dst + rank * (kTcBExt / 2),
+                           xext + (size_t)t * kTcBExt + rank * (kTcBExt / 2), kTcBExt / 2,
+                           &full[s], 3);
+            else
+              bulk_load(dst, xext + (size_t)t * kTcBExt, kTcBExt, &full[s]);
+            if (loads_on) {
+              for (int kb = 0; kb < nkb; ++kb) {
+                uint8_t* st = b_base + (size_t)(s + kb) * Cfg::kBBlock;
+                if (MC)
+                  tma_load_2d_mc(st + rank * (Cfg::kBBlock / 2), &tm_xhi, &full[s], kb * kTcKB,
+                                 t * kTcN + rank * (kTcN / 2), 3);
+                else
+                  tma_load_2d(st, &tm_xhi, &full[s], kb * kTcKB, t * kTcN);
+              }
+            }
+          }
+          __syncwarp();
+          s += nkb;
+          if (s >= S) {
+            s -= S;
+            ph ^= 1;
+          }
+          continue;
+        }
         if (Cfg::kExtRing) {
           const int e = i & 1;
           mbar_wait(&eempty[e], ((i >> 1) & 1) ^ 1);
@@ -376,6 +410,34 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         mbar_wait(&tempty[buf], ((i >> 1) & 1) ^ 1);
         if (lane == 0) { TB_TR(0, i, 1); }
         const uint32_t d = tmem + buf * kTcN;
+        if constexpr (Cfg::kTileBar) {
+          mbar_wait(&full[s], ph);
+          if (lane == 0) { TB_TR(0, i, 3); }
+          tc_fence_after();
+          if (elect_one_sync()) {
+            // acc = -||x||^2 (K = 16 augmented block, initialises the tile)
+            mma_bf16(d, dext_a, dext_b + (uint64_t)s * (kTcBExt >> 4), idesc, 0);
+            if (mma_on) {
+              for (int kb = 0; kb < nkb; ++kb) {
+                const uint64_t a0 = da + (uint64_t)kb * kAStep;
+                const uint64_t b0 = db + (uint64_t)(s + kb) * kBStep;
+#pragma unroll
+                for (int kk = 0; kk < kTcKB / 16; ++kk)
+                  mma_bf16(d, a0 + 2 * kk, b0 + 2 * kk, idesc, 1);
+              }
+            }
+            if (MC) mma_commit_mc(&empty[s], 3); else mma_commit(&empty[s]);
+            mma_commit(&tfull[buf]);   // accumulator ready for the epilogue
+          }
+          __syncwarp();
+          if (lane == 0) { TB_TR(0, i, 7); }
+          s += nkb;
+          if (s >= S) {
+            s -= S;
+            ph ^= 1;
+          }
+          continue;
+        }
         if (Cfg::kExtRing) {
           // acc = -||x||^2 from the norm-block ring (K = 16, initialises the tile)
           mbar_wait(&efull[buf], (i >> 1) & 1);
