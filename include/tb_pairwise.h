@@ -228,6 +228,27 @@ TB_API int tb_sgpr_tail_run(const tb_sgpr_plan* plan, const void* Z, double vari
                             double* Sigma, const double* v, double* w_out, double* out4,
                             void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---------------- SGPR ELBO gradient inside memory_limit -----------------
+ * The whole GPflow 2.3.1 SGPR training gradient (paper §5.3, Table 2) from
+ * the packed statistics (TB_SIGMA_TILES, consumed: Sigma becomes the factor
+ * P of Kuu + Sigma/s2 in place).  Only L = chol(Kuu) and P stay resident;
+ * 2 dELBO/dKuu and 2 dELBO/dSigma are produced one 128-column panel at a
+ * time and consumed at once (the data side streams all N rows of X, y
+ * through a fused generate-Kuf / DMMA / derivative kernel), so the device
+ * footprint is two packed M x M triangles + 3 column panels.
+ * out8: [0] sum log diag L, [1] sum log diag P, [2] |P^-1 v|^2,
+ * [3] tr(Kuu^-1 A), [4] tr(A^-1 Kuu), [5] w^T Kuu w (A = Kuu + Sigma/s2,
+ * w = A^-1 v / s2).  grad_hyp[2 (1 + dim)]: data-side (variance,
+ * lengthscales) then Kuu-side sums (the latter doubled: halve them);
+ * grad_Z[2 M dim]: data side then Kuu side.  Both are accumulated into
+ * (zero them first).  dim <= 16.  No reference counterpart. */
+TB_API int64_t tb_sgpr_grad_workspace(const tb_sgpr_plan* plan);
+TB_API int tb_sgpr_grad_run(const tb_sgpr_plan* plan, const void* X, const void* y, const void* Z,
+                            double variance, const double* lengthscales, double jitter,
+                            double noise_variance, double* Sigma, const double* v, double* out8,
+                            double* grad_hyp, double* grad_Z, void* workspace,
+                            int64_t workspace_bytes, void* stream);
+
 /* ---------------- SGPR ELBO gradient (N-streaming half) ------------------
  * GPflow 2.3.1 SGPR training-loss gradient (paper §5.3).  With
  * G = dELBO/dSigma and g = dELBO/dv from the O(M^3) tail (autodiff), the

@@ -79,6 +79,10 @@ _SIGS = {
     "tb_sgpr_tail_run": (ctypes.c_int, [ctypes.POINTER(SgprPlan), _vp, ctypes.c_double, _vp,
                                         ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _vp,
                                         _vp, _i64, _vp]),
+    "tb_sgpr_grad_workspace": (_i64, [ctypes.POINTER(SgprPlan)]),
+    "tb_sgpr_grad_run": (ctypes.c_int, [ctypes.POINTER(SgprPlan), _vp, _vp, _vp, ctypes.c_double,
+                                        _vp, ctypes.c_double, ctypes.c_double, _vp, _vp, _vp,
+                                        _vp, _vp, _vp, _i64, _vp]),
     "tb_sgpr_kuf_grad_workspace": (_i64, [_i64, _i64, _i64]),
     "tb_sgpr_kuf_grad": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _i32,
                                         ctypes.c_double, _vp, _vp, _vp, _vp, _i64, _vp]),

@@ -698,6 +698,35 @@ int tb_sgpr_tail_run(const tb_sgpr_plan* p, const void* Z, double variance,
                   workspace, (cudaStream_t)stream);
 }
 
+int64_t tb_sgpr_grad_workspace(const tb_sgpr_plan* p) {
+  if (!p || p->sigma_layout != TB_SIGMA_TILES) return -1;
+  return grad_tail_workspace_bytes(p->M, p->M_pad, p->dim);
+}
+
+int tb_sgpr_grad_run(const tb_sgpr_plan* p, const void* X, const void* y, const void* Z,
+                     double variance, const double* lengthscales, double jitter,
+                     double noise_variance, double* Sigma, const double* v, double* out8,
+                     double* grad_hyp, double* grad_Z, void* workspace, int64_t workspace_bytes,
+                     void* stream) {
+  if (!p) return fail(TB_ERR_ARG, "plan pointer is null");
+  if (p->sigma_layout != TB_SIGMA_TILES)
+    return fail(TB_ERR_ARG, "tb_sgpr_grad_run needs the packed-tile Sigma (TB_SIGMA_TILES)");
+  if (!X || !y || !Z || !Sigma || !v || !out8 || !grad_hyp || !grad_Z || !workspace)
+    return fail(TB_ERR_ARG, "null buffer passed to tb_sgpr_grad_run");
+  if (!(noise_variance > 0) || !(jitter >= 0))
+    return fail(TB_ERR_ARG, "noise_variance must be > 0 and jitter >= 0");
+  if (workspace_bytes < grad_tail_workspace_bytes(p->M, p->M_pad, p->dim))
+    return fail(TB_ERR_ARG, "workspace smaller than tb_sgpr_grad_workspace()");
+  if (p->dim > 16) return fail(TB_ERR_UNSUPPORTED, "tb_sgpr_grad_run supports dim <= 16");
+  KernParams kp;
+  int rc = make_params(p->kernel, p->dim, variance, lengthscales, &kp);
+  if (rc) return rc;
+  std::string why;
+  if (!sm100(&why)) return fail(TB_ERR_NO_DEVICE, why);
+  return grad_tail_run(p->M, p->M_pad, Z, X, y, p->N, p->dtype, kp, jitter, noise_variance,
+                       Sigma, v, out8, grad_hyp, grad_Z, workspace, (cudaStream_t)stream);
+}
+
 int64_t tb_sgpr_kuf_grad_workspace(int64_t nc, int64_t M, int64_t dim) {
   if (nc < 0 || M < 1 || dim < 1 || dim > kMaxDim) return -1;
   return kuf_grad_bytes(nc, M, dim);

@@ -56,7 +56,6 @@ sgpr_kuf_grad_kernel(const T* __restrict__ Xc, const T* __restrict__ Z,
     double gz[DMAX];
     const bool on = valid && i < M;
     const double w = on ? W[i * nc + c] : 0.0;
-    const double k = on ? K[i * nc + c] : 0.0;
     double r2 = 0.0;
 #pragma unroll
     for (int t = 0; t < DMAX; ++t)
@@ -64,6 +63,8 @@ sgpr_kuf_grad_kernel(const T* __restrict__ Xc, const T* __restrict__ Z,
         const double df = zs[r][t] - xs[t];
         r2 = fma(df, df, r2);
       }
+    // K == nullptr: the kernel value is recomputed from r^2 (no M x nc panel)
+    const double k = !on ? 0.0 : (K ? K[i * nc + c] : kern_from_r2(p, r2));
     const double wd = on ? w * dk_dr2(p, r2, k) : 0.0;
     gv = fma(w, k, gv);
 #pragma unroll

@@ -54,6 +54,12 @@ int64_t tail_workspace_bytes(int64_t M, int64_t M_pad, int64_t dim);
 int tail_run(int64_t M, int64_t M_pad, const void* Z, int dtype, const KernParams& kp,
              double jitter, double noise, double* sigma, const double* v, double* w_out,
              double* out4, void* workspace, cudaStream_t st);
+// in-budget ELBO gradient on the packed factors (sgpr_tail.cu)
+int64_t grad_tail_workspace_bytes(int64_t M, int64_t M_pad, int64_t dim);
+int grad_tail_run(int64_t M, int64_t M_pad, const void* Z, const void* X, const void* y,
+                  int64_t N, int dtype, const KernParams& kp, double jitter, double noise,
+                  double* sigma, const double* v, double* out8, double* grad_hyp,
+                  double* grad_z, void* workspace, cudaStream_t st);
 // ELBO gradient, N-streaming half (sgpr_grad.cu)
 int64_t kuf_grad_bytes(int64_t nc, int64_t M, int64_t dim);
 int launch_kuf_grad(const void* Xc, const void* Z, const double* W, const double* K,

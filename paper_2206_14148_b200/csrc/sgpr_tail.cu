@@ -19,6 +19,7 @@
 // reductions.
 #include <cmath>
 #include <string>
+#include <cooperative_groups.h>
 
 #include "sgpr_internal.h"
 
@@ -614,6 +615,642 @@ int tail_run(int64_t M, int64_t M_pad, const void* Z, int dtype, const KernParam
   TB_CUDA_TRY(cudaStreamSynchronize(st));
   if (h_info)
     return fail(TB_ERR_ARG, "sgpr tail: Cholesky failed at row " + std::to_string(h_info - 1) +
+                                " (matrix not positive definite)");
+  return TB_OK;
+}
+
+// ======================================================= gradient tail ==
+// The GPflow training gradient of the ELBO inside memory_limit (DESIGN.md §4
+// "Gradient").  With Kuu = L L^T, A = Kuu + Sigma/s2 = P P^T, w = A^-1 v / s2:
+//   G2 = 2 dELBO/dSigma = (Kuu^-1 - A^-1 - w w^T) / s2
+//   H2 = 2 dELBO/dKuu   = 2 Kuu^-1 - A^-1 - Kuu^-1 A Kuu^-1 - w w^T
+// Only the two packed factors L and P stay resident; both M x M matrices are
+// produced one 128-column panel at a time (E_P = identity columns of tile P):
+//   Kuu^-1[:,P] = L^-T L^-1 E_P,   A^-1[:,P] = P^-T P^-1 E_P,
+//   (Kuu^-1 A Kuu^-1)[:,P] = L^-T L^-1 P P^T Kuu^-1[:,P]
+// and consumed at once: H2[:,P] against the kernel derivatives over Z x Z_P
+// (tb_sgpr_kuf_grad with K recomputed), G2[:,P] by the fused data kernel
+// below, which streams all N points, generating the Kuf tiles it multiplies
+// on the fly (W[P,:] = G2[:,P]^T Kuf + g_P y^T never exists in memory) and
+// contracting W with the kernel derivatives in its epilogue.
+namespace cg = cooperative_groups;
+
+// acc(r, c) += sum_k opA(r, k) opB(k, c) over one 128 x 128 x 128 tile
+// product, column-major tiles, the DMMA fragment layout of tail_gemm_kernel:
+//   opA(r, k) = ta ? A[r*128 + k] : A[k*128 + r]
+//   opB(k, c) = tb ? B[k*128 + c] : B[c*128 + k]
+// GEN (data kernel): opB is generated by gen(k, c) instead of loaded.
+template <typename Gen>
+__device__ __forceinline__ void tile_mma_impl(double (&acc)[8][4][2], const double* A, bool ta,
+                                              const double* B, bool tb, double* sm, Gen gen,
+                                              bool use_gen) {
+  double* As = sm;
+  double* Bs = sm + 2 * kGKc * kGLd;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wr = warp >> 2, wc = warp & 3, g = lane >> 2, tg = lane & 3;
+  const int cr = tid & 127, ck = (tid >> 7) * 8;      // "column" pattern (row fastest)
+  const int rr = tid >> 1, rk = (tid & 1) * 8;        // "row" pattern (k fastest)
+  double ra[8], rb[8];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      ra[q] = ta ? A[(int64_t)rr * kTT + k0 + rk + q] : A[(int64_t)(k0 + ck + q) * kTT + cr];
+      if (use_gen) rb[q] = gen(k0 + ck + q, cr);
+      else rb[q] = tb ? B[(int64_t)(k0 + ck + q) * kTT + cr] : B[(int64_t)rr * kTT + k0 + rk + q];
+    }
+  };
+  const bool bcol = use_gen || tb;
+  load(0);
+  int stage = 0;
+  for (int k0 = 0; k0 < kTT; k0 += kGKc) {
+    double* as = As + stage * kGKc * kGLd;
+    double* bs = Bs + stage * kGKc * kGLd;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (ta) as[(rk + q) * kGLd + rr] = ra[q];
+      else as[(ck + q) * kGLd + cr] = ra[q];
+      if (bcol) bs[(ck + q) * kGLd + cr] = rb[q];
+      else bs[(rk + q) * kGLd + rr] = rb[q];
+    }
+    __syncthreads();
+    if (k0 + kGKc < kTT) load(k0 + kGKc);
+#pragma unroll
+    for (int ks = 0; ks < kGKc / 4; ++ks) {
+      double af[8], bf[4];
+      const double* ak = as + (ks * 4 + tg) * kGLd + wr * 64 + g;
+      const double* bk2 = bs + (ks * 4 + tg) * kGLd + wc * 32 + g;
+#pragma unroll
+      for (int a = 0; a < 8; ++a) af[a] = ak[a * 8];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = bk2[b * 8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    stage ^= 1;
+  }
+  __syncthreads();
+}
+struct NoGen {
+  __device__ double operator()(int, int) const { return 0.0; }
+};
+__device__ __forceinline__ void tile_mma(double (&acc)[8][4][2], const double* A, bool ta,
+                                         const double* B, bool tb, double* sm) {
+  tile_mma_impl(acc, A, ta, B, tb, sm, NoGen{}, false);
+}
+__device__ __forceinline__ void acc_zero(double (&acc)[8][4][2]) {
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+}
+// C (column-major tile) = acc (mode 0) or C -= acc (mode 1)
+__device__ __forceinline__ void acc_store(const double (&acc)[8][4][2], double* C, int mode) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wr = warp >> 2, wc = warp & 3, g = lane >> 2, tg = lane & 3;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int r = wr * 64 + a * 8 + g;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = wc * 32 + b * 8 + 2 * tg + e;
+        if (mode) C[(int64_t)c * kTT + r] -= acc[a][b][e];
+        else C[(int64_t)c * kTT + r] = acc[a][b][e];
+      }
+  }
+}
+
+// Panel triangular solve in place, one cooperative launch:
+//   TRANS = 0: L Y = B (forward from tile row i0; the rows above are zero)
+//   TRANS = 1: L^T Y = B (backward over all tile rows)
+// step i: CTA 0 applies the diagonal inverse, grid sync, every CTA updates
+// its share of the remaining tile rows, grid sync.
+template <int TRANS>
+__global__ void __launch_bounds__(256, 1)
+gp_trsm_kernel(const double* __restrict__ L, const double* __restrict__ inv, double* Y, int nt,
+               int i0) {
+  extern __shared__ __align__(16) double gsm[];
+  cg::grid_group grid = cg::this_grid();
+  double acc[8][4][2];
+  const int steps = TRANS ? nt : nt - i0;
+  for (int s = 0; s < steps; ++s) {
+    const int i = TRANS ? nt - 1 - s : i0 + s;
+    double* Yi = Y + (int64_t)i * kTE;
+    if (blockIdx.x == 0) {
+      acc_zero(acc);
+      tile_mma(acc, inv + (int64_t)i * kTE, TRANS, Yi, false, gsm);
+      acc_store(acc, Yi, 0);
+    }
+    grid.sync();
+    const int cnt = TRANS ? i : nt - 1 - i;
+    for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
+      const int k = TRANS ? q : i + 1 + q;
+      acc_zero(acc);
+      tile_mma(acc, L + (TRANS ? tslot(i, k) : tslot(k, i)) * kTE, TRANS, Yi, false, gsm);
+      acc_store(acc, Y + (int64_t)k * kTE, 1);
+    }
+    grid.sync();
+  }
+}
+
+// out = L Y (TRANS = 0) or L^T Y (TRANS = 1), out of place; CTA = out tile row
+template <int TRANS>
+__global__ void __launch_bounds__(256, 1)
+gp_trmm_kernel(const double* __restrict__ L, const double* __restrict__ Y,
+               double* __restrict__ out, int nt) {
+  extern __shared__ __align__(16) double gsm[];
+  const int k = blockIdx.x;
+  double acc[8][4][2];
+  acc_zero(acc);
+  if (!TRANS) {
+    for (int j = 0; j <= k; ++j)
+      tile_mma(acc, L + tslot(k, j) * kTE, false, Y + (int64_t)j * kTE, false, gsm);
+  } else {
+    for (int j = k; j < nt; ++j)
+      tile_mma(acc, L + tslot(j, k) * kTE, true, Y + (int64_t)j * kTE, false, gsm);
+  }
+  acc_store(acc, out + (int64_t)k * kTE, 0);
+}
+
+// Y = E_P (identity columns of tile P; padding included, like the packed
+// identity padding of the factors)
+__global__ void gp_identity_kernel(double* __restrict__ Y, int P, int64_t n) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / kTE;
+    const int c = (int)((e % kTE) / kTT), r = (int)(e % kTT);
+    Y[e] = (t == P && r == c) ? 1.0 : 0.0;
+  }
+}
+
+// panel element (i, c), i = global row, c = panel column
+__device__ __forceinline__ int64_t pidx(int64_t i, int c) {
+  return (i / kTT) * kTE + (int64_t)c * kTT + (i % kTT);
+}
+
+// G2*s2 = Kinv - Ainv - w w^T -> Kinv buffer;  H2 = 2 Kinv - Ainv - KAK - w w^T -> KAK buffer
+__global__ void gp_combine_kernel(double* __restrict__ kinv, const double* __restrict__ ainv,
+                                  double* __restrict__ kak, const double* __restrict__ w, int P,
+                                  int64_t M, int64_t M_pad) {
+  const int64_t n = M_pad * kTT;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / kTE;
+    const int c = (int)((e % kTE) / kTT), r = (int)(e % kTT);
+    const int64_t i = t * kTT + r, j = (int64_t)P * kTT + c;
+    const double ww = (i < M && j < M) ? w[i] * w[j] : 0.0;
+    const double k1 = kinv[e], a1 = ainv[e];
+    kinv[e] = k1 - a1 - ww;
+    kak[e] = 2.0 * k1 - a1 - kak[e] - ww;
+  }
+}
+
+// part[P] = sum over the valid columns c of T(P*128 + c, c)  (trace block)
+__global__ void gp_diag_trace_kernel(const double* __restrict__ T, int P, int64_t M,
+                                     double* __restrict__ part) {
+  double s = 0.0;
+  for (int c = threadIdx.x; c < kTT; c += 32)
+    if ((int64_t)P * kTT + c < M) s += T[(int64_t)P * kTE + (int64_t)c * kTT + c];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) part[P] = s;
+}
+
+// Per block b: part[b] = (sum_ic Kuu(i, Pc) Ainv(i, c), sum_ic Kuu(i, Pc) w_i w_Pc)
+// over the valid entries; Kuu generated on the fly (no panel)
+__global__ void __launch_bounds__(256)
+gp_kuu_dot_kernel(const double* __restrict__ Zs, const double* __restrict__ ainv,
+                  const double* __restrict__ w, int P, int64_t M, KernParams p, double jitter,
+                  double* __restrict__ part) {
+  __shared__ double red[2][8];
+  double s1 = 0.0, s2 = 0.0;
+  const int64_t n = M * kTT;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / kTT;
+    const int c = (int)(e % kTT);
+    const int64_t j = (int64_t)P * kTT + c;
+    if (j >= M) continue;
+    double r2 = 0.0;
+    for (int d = 0; d < p.dim; ++d) {
+      const double df = Zs[i * p.dim + d] - Zs[j * p.dim + d];
+      r2 = fma(df, df, r2);
+    }
+    const double k = kern_from_r2(p, r2) + (i == j ? jitter : 0.0);
+    s1 = fma(k, ainv[pidx(i, c)], s1);
+    s2 = fma(k, w[i] * w[j], s2);
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = s1;
+    red[1][threadIdx.x >> 5] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double v = 0.0;
+    for (int q = 0; q < 8; ++q) v += red[threadIdx.x][q];
+    part[2 * blockIdx.x + threadIdx.x] = v;
+  }
+}
+
+// out1[P] = sum_b part[2b], out2[P] = sum_b part[2b+1] (fixed order, one warp)
+__global__ void gp_pair_sum_kernel(const double* __restrict__ part, int nb, int P,
+                                   double* __restrict__ out1, double* __restrict__ out2) {
+  double a = 0.0, b = 0.0;
+  for (int q = threadIdx.x; q < nb; q += 32) {
+    a += part[2 * q];
+    b += part[2 * q + 1];
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (threadIdx.x == 0) {
+    out1[P] = a;
+    out2[P] = b;
+  }
+}
+
+// dense row-major [M x nc] copy of panel columns 0..nc-1 (tb_sgpr_kuf_grad's W)
+__global__ void gp_to_rowmajor_kernel(const double* __restrict__ Y, int64_t M, int nc,
+                                      double* __restrict__ out) {
+  const int64_t n = M * nc;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = Y[pidx(e / nc, (int)(e % nc))];
+}
+
+// Fused data side for panel P: for every block of 128 training points,
+//   W(p, n) = (sum_i G2s2(i, P*128+p) Kuf(i, n)) / s2 + (w_p / s2) y_n
+// (DMMA over the inducing tiles; Kuf tiles generated in the operand loader),
+// then the kernel-derivative contraction of tb_sgpr_kuf_grad in the
+// epilogue: dvariance += W k / var, dl_t += W k' (-2 (x_t - z_t)^2 / l_t^3),
+// dz_pt += W k' (2 (z_t - x_t) / l_t^2).  Work items (point blocks) are dealt
+// round-robin to a fixed grid and every CTA accumulates in a fixed order;
+// per-CTA partials are reduced in a fixed order afterwards (deterministic).
+template <typename T, int DMAX>
+__global__ void __launch_bounds__(256, 1)
+gp_data_kernel(const T* __restrict__ X, const T* __restrict__ y, const double* __restrict__ Zs,
+               const double* __restrict__ G, const double* __restrict__ w, double inv_s2, int P,
+               int nt, int64_t M, int64_t N, KernParams p, double* __restrict__ part_hyp,
+               double* __restrict__ part_z) {
+  extern __shared__ __align__(16) double gsm[];
+  double* mma_sm = gsm;                                   // 2 * 2 * kGKc * kGLd
+  double* zt = gsm + 4 * kGKc * kGLd;                     // [128][DMAX] inducing tile (scaled)
+  double* zp = zt + kTT * DMAX;                           // [128][DMAX] panel rows
+  double* xb = zp + kTT * DMAX;                           // [128][DMAX] point block
+  double* yb = xb + kTT * DMAX;                           // [128]
+  double* gp_s = yb + kTT;                                // [128] w_p / s2
+  double* zacc = gp_s + kTT;                              // [128][DMAX] dz accumulators
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wr = warp >> 2, wc = warp & 3, g = lane >> 2, tg = lane & 3;
+  const int dim = p.dim;
+  for (int e = tid; e < kTT * DMAX; e += blockDim.x) {
+    const int r = e / DMAX, t = e % DMAX;
+    const int64_t i = (int64_t)P * kTT + r;
+    zp[e] = (t < dim && i < M) ? Zs[i * dim + t] : 0.0;
+    zacc[e] = 0.0;
+  }
+  for (int r = tid; r < kTT; r += blockDim.x) {
+    const int64_t i = (int64_t)P * kTT + r;
+    gp_s[r] = i < M ? w[i] * inv_s2 : 0.0;
+  }
+  double gv = 0.0, gl[DMAX];
+#pragma unroll
+  for (int t = 0; t < DMAX; ++t) gl[t] = 0.0;
+  const int64_t nblk = (N + kTT - 1) / kTT;
+  const int cr = tid & 127;
+  double xr[DMAX];
+  for (int64_t nb = blockIdx.x; nb < nblk; nb += gridDim.x) {
+    __syncthreads();
+    for (int e = tid; e < kTT * DMAX; e += blockDim.x) {
+      const int r = e / DMAX, t = e % DMAX;
+      const int64_t n = nb * kTT + r;
+      xb[e] = (t < dim && n < N) ? (double)X[n * dim + t] * p.inv_ls[t] : 0.0;
+    }
+    for (int r = tid; r < kTT; r += blockDim.x) {
+      const int64_t n = nb * kTT + r;
+      yb[r] = n < N ? (double)y[n] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < DMAX; ++t) xr[t] = xb[cr * DMAX + t];     // this thread's loader point
+    const bool pvalid = nb * kTT + cr < N;
+    double acc[8][4][2];
+    acc_zero(acc);
+    for (int kt = 0; kt < nt; ++kt) {
+      for (int e = tid; e < kTT * DMAX; e += blockDim.x) {
+        const int r = e / DMAX, t = e % DMAX;
+        const int64_t i = (int64_t)kt * kTT + r;
+        zt[e] = (t < dim && i < M) ? Zs[i * dim + t] : 0.0;
+      }
+      __syncthreads();
+      const int64_t ibase = (int64_t)kt * kTT;
+      auto gen = [&](int k, int c) -> double {      // Kuf(inducing ibase + k, point c = cr)
+        if (!pvalid || ibase + k >= M) return 0.0;
+        double r2 = 0.0;
+#pragma unroll
+        for (int t = 0; t < DMAX; ++t)
+          if (t < dim) {
+            const double df = zt[k * DMAX + t] - xr[t];
+            r2 = fma(df, df, r2);
+          }
+        return kern_from_r2(p, r2);
+      };
+      tile_mma_impl(acc, G + (int64_t)kt * kTE, true, nullptr, true, mma_sm, gen, true);
+    }
+    // epilogue: W and the kernel-derivative contraction
+    double* red = mma_sm;                                  // [4 wc][128][DMAX] (reuse)
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int r = wr * 64 + a * 8 + g;
+      double gz[DMAX];
+#pragma unroll
+      for (int t = 0; t < DMAX; ++t) gz[t] = 0.0;
+      const bool rvalid = (int64_t)P * kTT + r < M;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = wc * 32 + b * 8 + 2 * tg + e;
+          if (!rvalid || nb * kTT + c >= N) continue;
+          const double W = acc[a][b][e] * inv_s2 + gp_s[r] * yb[c];
+          double r2 = 0.0;
+#pragma unroll
+          for (int t = 0; t < DMAX; ++t)
+            if (t < dim) {
+              const double df = zp[r * DMAX + t] - xb[c * DMAX + t];
+              r2 = fma(df, df, r2);
+            }
+          const double k = kern_from_r2(p, r2);
+          double dk;
+          if (p.kernel == TB_KERNEL_RBF) {
+            dk = -0.5 * k;
+          } else {
+            const double rr = sqrt(fmax(r2, 1e-36));
+            dk = -1.5 * p.variance * exp(-1.7320508075688772 * rr);
+          }
+          const double wd = W * dk;
+          gv = fma(W, k, gv);
+#pragma unroll
+          for (int t = 0; t < DMAX; ++t)
+            if (t < dim) {
+              const double df = zp[r * DMAX + t] - xb[c * DMAX + t];
+              gl[t] = fma(wd * df * df, -2.0 * p.inv_ls[t], gl[t]);
+              gz[t] = fma(wd * df, 2.0 * p.inv_ls[t], gz[t]);
+            }
+        }
+      // sum over the 4 lanes sharing row r (tg), then stage per wc
+#pragma unroll
+      for (int t = 0; t < DMAX; ++t) {
+        double v = gz[t];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (tg == 0) red[((int64_t)wc * kTT + r) * DMAX + t] = v;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < kTT * DMAX; e += blockDim.x) {
+      const int r = e / DMAX, t = e % DMAX;
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v += red[((int64_t)q * kTT + r) * DMAX + t];
+      zacc[e] += v;
+    }
+  }
+  __syncthreads();
+  // per-CTA partials: dz rows of panel P, then (variance, lengthscales)
+  for (int e = tid; e < kTT * DMAX; e += blockDim.x) part_z[(int64_t)blockIdx.x * kTT * DMAX + e] = zacc[e];
+  double* hred = mma_sm;                                  // [8 warps][1 + DMAX]
+  __syncthreads();
+  gv = warp_sum(gv);
+  if (lane == 0) hred[warp * (1 + DMAX)] = gv;
+#pragma unroll
+  for (int t = 0; t < DMAX; ++t) {
+    const double v = warp_sum(gl[t]);
+    if (lane == 0) hred[warp * (1 + DMAX) + 1 + t] = v;
+  }
+  __syncthreads();
+  if (tid < 1 + DMAX) {
+    double v = 0.0;
+    for (int q = 0; q < 8; ++q) v += hred[q * (1 + DMAX) + tid];
+    part_hyp[(int64_t)blockIdx.x * (1 + DMAX) + tid] = tid == 0 ? v / p.variance : v;
+  }
+}
+
+// grad_hyp[j] += sum_b part_hyp[b][j] (j < 1 + dim); grad_z[(P*128 + r)*dim + t]
+// += sum_b part_z[b][r][t]  (fixed order)
+__global__ void gp_data_reduce_kernel(const double* __restrict__ part_hyp,
+                                      const double* __restrict__ part_z, int nb, int dmax,
+                                      int dim, int P, int64_t M, double* __restrict__ grad_hyp,
+                                      double* __restrict__ grad_z) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < kTT * dmax) {
+    const int r = e / dmax, t = e % dmax;
+    const int64_t i = (int64_t)P * kTT + r;
+    if (t < dim && i < M) {
+      double s = 0.0;
+      for (int b = 0; b < nb; ++b) s += part_z[((int64_t)b * kTT + r) * dmax + t];
+      grad_z[i * dim + t] += s;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x <= dim) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part_hyp[(int64_t)b * (1 + dmax) + threadIdx.x];
+    grad_hyp[threadIdx.x] += s;
+  }
+}
+
+constexpr int kGpGrid = 148;
+static size_t gp_data_smem(int dmax) {
+  return (size_t)(4 * kGKc * kGLd + 4 * kTT * dmax + 2 * kTT) * sizeof(double);
+}
+
+int64_t grad_tail_workspace_bytes(int64_t M, int64_t M_pad, int64_t dim) {
+  const int64_t nt = M_pad / kTT, tiles = nt * (nt + 1) / 2;
+  const int64_t dmax = dim <= 4 ? 4 : 16;
+  return round_up(tiles * kTE * 8, 256)                 // L (packed)
+         + round_up(2 * nt * kTE * 8, 256)              // diagonal inverses of L, P
+         + 3 * round_up(M_pad * kTT * 8, 256)           // three column panels
+         + round_up(M * dim * 8, 256)                   // scaled Z
+         + round_up(4 * M_pad * 8, 256)                 // u, w, v copy, solve scratch
+         + round_up((tiles + 16 + 3 * nt + 2 * 1024) * 8, 256)   // partials, scalars
+         + round_up((int64_t)kGpGrid * (kTT * dmax + 1 + dmax) * 8, 256)   // data partials
+         + kuf_grad_bytes(kTT, M, dim) + 1024;
+}
+
+static int gp_trsm(const double* L, const double* inv, double* Y, int nt, int i0, int trans,
+                   cudaStream_t st) {
+  void* args[] = {(void*)&L, (void*)&inv, (void*)&Y, (void*)&nt, (void*)&i0};
+  const void* fn = trans ? (const void*)gp_trsm_kernel<1> : (const void*)gp_trsm_kernel<0>;
+  TB_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(kGpGrid), dim3(256), args, kGSmem, st));
+  return TB_OK;
+}
+
+int grad_tail_run(int64_t M, int64_t M_pad, const void* Z, const void* X, const void* y,
+                  int64_t N, int dtype, const KernParams& kp, double jitter, double noise,
+                  double* sigma, const double* v, double* out8, double* grad_hyp,
+                  double* grad_z, void* workspace, cudaStream_t st) {
+  const int nt = (int)(M_pad / kTT);
+  const int tiles = nt * (nt + 1) / 2;
+  const int dim = kp.dim;
+  const int dmax = dim <= 4 ? 4 : 16;
+  char* ws = (char*)workspace;
+  auto take = [&](int64_t bytes) { char* q = ws; ws += round_up(bytes, 256); return q; };
+  double* L = (double*)take((int64_t)tiles * kTE * 8);
+  double* invL = (double*)take(2 * (int64_t)nt * kTE * 8);
+  double* invP = invL + (int64_t)nt * kTE;
+  double* B0 = (double*)take(M_pad * kTT * 8);
+  double* B1 = (double*)take(M_pad * kTT * 8);
+  double* B2 = (double*)take(M_pad * kTT * 8);
+  double* Zs = (double*)take(M * dim * 8);
+  double* vec = (double*)take(4 * M_pad * 8);
+  double* u = vec;
+  double* w = u + M_pad;
+  double* vv = w + M_pad;
+  double* scratch = vv + M_pad;
+  double* part = (double*)take((int64_t)(tiles + 16 + 3 * nt + 2 * 1024) * 8);
+  double* scal = part + tiles;            // [0] logdet L [1] logdet P [2] |u|^2 [3..5] traces
+  int* info = (int*)(scal + 8);
+  double* tr_part = scal + 16;            // [nt] trace blocks of A Kuu^-1
+  double* ak_part = tr_part + nt;         // [nt] blocks of tr(A^-1 Kuu)
+  double* wk_part = ak_part + nt;         // [nt] blocks of w^T Kuu w
+  double* kd_part = wk_part + nt;         // [1024][2] per-CTA Kuu dots
+  double* ph = (double*)take((int64_t)kGpGrid * (kTT * dmax + 1 + dmax) * 8);
+  double* pz = ph + (int64_t)kGpGrid * (1 + dmax);
+  void* kg_ws = ws;
+  const double s2 = noise;
+  TB_CUDA_TRY(cudaFuncSetAttribute(tail_potrf_inv_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)((size_t)kTT * kTLd * 8)));
+  TB_CUDA_TRY(cudaFuncSetAttribute(tail_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kGSmem));
+  for (const void* f : {(const void*)gp_trsm_kernel<0>, (const void*)gp_trsm_kernel<1>,
+                        (const void*)gp_trmm_kernel<0>, (const void*)gp_trmm_kernel<1>})
+    TB_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
+  TB_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int), st));
+  const unsigned zb = (unsigned)ceil_div(std::max<int64_t>(M * dim, 1), 256);
+  if (dtype == TB_F32)
+    scale_z_kernel<float><<<zb, 256, 0, st>>>((const float*)Z, M, kp, Zs);
+  else
+    scale_z_kernel<double><<<zb, 256, 0, st>>>((const double*)Z, M, kp, Zs);
+  TB_LAUNCH_CHECK("scale_z");
+  cudaStream_t side = nullptr;
+  cudaEvent_t e_col = nullptr, e_diag = nullptr;
+  int lo_p = 0, hi_p = 0;
+  TB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p));
+  TB_CUDA_TRY(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi_p));
+  TB_CUDA_TRY(cudaEventCreateWithFlags(&e_col, cudaEventDisableTiming));
+  TB_CUDA_TRY(cudaEventCreateWithFlags(&e_diag, cudaEventDisableTiming));
+  struct Cleanup {
+    cudaStream_t s;
+    cudaEvent_t a, b;
+    ~Cleanup() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      cudaStreamDestroy(s);
+    }
+  } cleanup{side, e_col, e_diag};
+  // L = chol(Kuu), P = chol(Kuu + Sigma / s2) in place over Sigma
+  tail_kuu_kernel<<<tiles, 256, 0, st>>>(Zs, M, kp, jitter, 0.0, L);
+  TB_LAUNCH_CHECK("tail_kuu");
+  int rc = tail_cholesky(L, invL, nt, info, st, side, e_col, e_diag);
+  if (rc) return rc;
+  tail_kuu_kernel<<<tiles, 256, 0, st>>>(Zs, M, kp, jitter, 1.0 / s2, sigma);
+  TB_LAUNCH_CHECK("tail_kuu_add");
+  if ((rc = tail_cholesky(sigma, invP, nt, info, st, side, e_col, e_diag))) return rc;
+  double* Pf = sigma;
+  tail_reduce_kernel<<<tiles, 256, 0, st>>>(L, 0, part);
+  sum_kernel<<<1, 32, 0, st>>>(part, tiles, scal + 0);
+  tail_reduce_kernel<<<tiles, 256, 0, st>>>(Pf, 0, part);
+  sum_kernel<<<1, 32, 0, st>>>(part, tiles, scal + 1);
+  TB_LAUNCH_CHECK("grad_logdet");
+  // u = P^-1 v, |u|^2, w = P^-T u / s2
+  scale_copy_kernel<<<(unsigned)ceil_div(M_pad, 256), 256, 0, st>>>(v, M, M_pad, 1.0, vv);
+  if ((rc = tail_solve(Pf, invP, nt, vv, scratch, u, 0, st))) return rc;
+  dot_kernel<<<1, 256, 0, st>>>(u, M_pad, scal + 2);
+  if ((rc = tail_solve(Pf, invP, nt, u, scratch, w, 1, st))) return rc;
+  scale_copy_kernel<<<(unsigned)ceil_div(M_pad, 256), 256, 0, st>>>(w, M, M_pad, 1.0 / s2, w);
+  TB_LAUNCH_CHECK("grad_vec");
+  TB_CUDA_TRY(cudaFuncSetAttribute(dmax == 4 ? (const void*)gp_data_kernel<float, 4>
+                                             : (const void*)gp_data_kernel<float, 16>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)gp_data_smem(dmax)));
+  TB_CUDA_TRY(cudaFuncSetAttribute(dmax == 4 ? (const void*)gp_data_kernel<double, 4>
+                                             : (const void*)gp_data_kernel<double, 16>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)gp_data_smem(dmax)));
+  const int64_t pn = M_pad * kTT;
+  const unsigned eb = (unsigned)std::min<int64_t>(ceil_div(pn, 256), 4096);
+  const int kd_blocks = 256;
+  for (int P = 0; P < nt; ++P) {
+    // B0 = Kuu^-1[:, P]
+    gp_identity_kernel<<<eb, 256, 0, st>>>(B0, P, pn);
+    if ((rc = gp_trsm(L, invL, B0, nt, P, 0, st))) return rc;
+    if ((rc = gp_trsm(L, invL, B0, nt, 0, 1, st))) return rc;
+    // B2 = A Kuu^-1[:, P] = P (P^T B0)  (its block P gives tr(Kuu^-1 A)),
+    // then B2 = Kuu^-1 A Kuu^-1[:, P]
+    gp_trmm_kernel<1><<<nt, 256, kGSmem, st>>>(Pf, B0, B1, nt);
+    gp_trmm_kernel<0><<<nt, 256, kGSmem, st>>>(Pf, B1, B2, nt);
+    TB_LAUNCH_CHECK("grad_trmm");
+    gp_diag_trace_kernel<<<1, 32, 0, st>>>(B2, P, M, tr_part);
+    if ((rc = gp_trsm(L, invL, B2, nt, 0, 0, st))) return rc;
+    if ((rc = gp_trsm(L, invL, B2, nt, 0, 1, st))) return rc;
+    // B1 = A^-1[:, P]
+    gp_identity_kernel<<<eb, 256, 0, st>>>(B1, P, pn);
+    if ((rc = gp_trsm(Pf, invP, B1, nt, P, 0, st))) return rc;
+    if ((rc = gp_trsm(Pf, invP, B1, nt, 0, 1, st))) return rc;
+    // tr(A^-1 Kuu) and w^T Kuu w, block P (Kuu generated on the fly)
+    gp_kuu_dot_kernel<<<kd_blocks, 256, 0, st>>>(Zs, B1, w, P, M, kp, jitter, kd_part);
+    gp_pair_sum_kernel<<<1, 32, 0, st>>>(kd_part, kd_blocks, P, ak_part, wk_part);
+    TB_LAUNCH_CHECK("grad_kuu_dot");
+    // B0 = G2 s2, B2 = H2
+    gp_combine_kernel<<<eb, 256, 0, st>>>(B0, B1, B2, w, P, M, M_pad);
+    TB_LAUNCH_CHECK("grad_combine");
+    // Kuu side: sum_{i, c in P} H2(i, c) dk(z_i, z_c) (tb_sgpr_kuf_grad, K recomputed)
+    const int nc = (int)std::min<int64_t>(kTT, M - (int64_t)P * kTT);
+    if (nc > 0) {
+      gp_to_rowmajor_kernel<<<eb, 256, 0, st>>>(B2, M, nc, B1);
+      TB_LAUNCH_CHECK("grad_rowmajor");
+      const char* zp = (const char*)Z + (int64_t)P * kTT * dim * (dtype == TB_F32 ? 4 : 8);
+      if ((rc = launch_kuf_grad(zp, Z, B1, nullptr, nc, M, dtype, kp, grad_hyp + 1 + dim,
+                                grad_z + M * dim, kg_ws, st)))
+        return rc;
+    }
+    // data side: all N points against G2[:, P]
+    if (dtype == TB_F32) {
+      if (dmax == 4)
+        gp_data_kernel<float, 4><<<kGpGrid, 256, gp_data_smem(4), st>>>(
+            (const float*)X, (const float*)y, Zs, B0, w, 1.0 / s2, P, nt, M, N, kp, ph, pz);
+      else
+        gp_data_kernel<float, 16><<<kGpGrid, 256, gp_data_smem(16), st>>>(
+            (const float*)X, (const float*)y, Zs, B0, w, 1.0 / s2, P, nt, M, N, kp, ph, pz);
+    } else {
+      if (dmax == 4)
+        gp_data_kernel<double, 4><<<kGpGrid, 256, gp_data_smem(4), st>>>(
+            (const double*)X, (const double*)y, Zs, B0, w, 1.0 / s2, P, nt, M, N, kp, ph, pz);
+      else
+        gp_data_kernel<double, 16><<<kGpGrid, 256, gp_data_smem(16), st>>>(
+            (const double*)X, (const double*)y, Zs, B0, w, 1.0 / s2, P, nt, M, N, kp, ph, pz);
+    }
+    TB_LAUNCH_CHECK("grad_data");
+    gp_data_reduce_kernel<<<(unsigned)ceil_div(kTT * dmax, 256), 256, 0, st>>>(
+        ph, pz, kGpGrid, dmax, dim, P, M, grad_hyp, grad_z);
+    TB_LAUNCH_CHECK("grad_data_reduce");
+  }
+  // scalars: [0] sum log diag L, [1] sum log diag P, [2] |u|^2, [3] tr(Kuu^-1 A),
+  // [4] tr(A^-1 Kuu), [5] w^T Kuu w  (valid entries only)
+  sum_kernel<<<1, 32, 0, st>>>(tr_part, nt, scal + 3);
+  sum_kernel<<<1, 32, 0, st>>>(ak_part, nt, scal + 4);
+  sum_kernel<<<1, 32, 0, st>>>(wk_part, nt, scal + 5);
+  TB_LAUNCH_CHECK("grad_scalars");
+  TB_CUDA_TRY(cudaMemcpyAsync(out8, scal, 6 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  int h_info = 0;
+  TB_CUDA_TRY(cudaMemcpyAsync(&h_info, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TB_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h_info)
+    return fail(TB_ERR_ARG, "sgpr grad tail: Cholesky failed at row " + std::to_string(h_info - 1) +
                                 " (matrix not positive definite)");
   return TB_OK;
 }

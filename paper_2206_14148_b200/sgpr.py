@@ -30,6 +30,12 @@ from .sizes import as_limit
 LOG2PI = math.log(2.0 * math.pi)
 
 
+def _alloc_bytes(b: int) -> int:
+    """What the caching allocator charges for one b-byte buffer (512-B
+    granules up to 1 MiB, 2 MiB above; tb_common.cuh alloc_bytes)."""
+    return -(-b // 512) * 512 if b <= (1 << 20) else -(-b // (2 << 20)) * (2 << 20)
+
+
 def _torch():
     import torch
     return torch
@@ -250,10 +256,36 @@ class SGPR:
         return self._tail()
 
     # -- gradient (GPflow 2.3.1 SGPR training loss; paper §5.3 Table 2) -------
+    def grad_peak_bytes(self) -> int:
+        """Device bytes of elbo_and_grads on the packed path (inputs included):
+        the larger of the statistics pass's plan and the gradient tail (the
+        packed statistics + two column panels of vectors + its workspace)."""
+        torch = _torch()
+        N, M = int(self.X.shape[0]), int(self.Z.shape[0])
+        es = self.X.element_size()
+        p = plan(N, M, self.dim, kernel=self.kernel,
+                 dtype=np.float32 if self.X.dtype == torch.float32 else np.float64,
+                 memory_limit=self.memory_limit,
+                 resident_bytes=(N * self.dim + N + M * self.dim) * es, engine=self.engine)
+        if p.sigma_layout != _lib.TB_SIGMA_TILES:
+            return -1
+        lib = _lib.load()
+        ab = _alloc_bytes
+        resident = sum(ab(t.numel() * t.element_size()) for t in (self.X, self.y, self.Z))
+        tail = (resident + ab(int(p.sigma_bytes)) + ab(M * 8) + ab(8)
+                + ab(int(lib.tb_sgpr_grad_workspace(ctypes.byref(p))))
+                + ab(8 * 8) + ab(2 * (1 + self.dim) * 8) + ab(2 * M * self.dim * 8))
+        return max(int(p.peak_bytes), tail)
+
     def elbo_and_grads(self, chunk_n: int = 4096):
         """ELBO and its gradient w.r.t. kernel variance, lengthscales (ARD),
         likelihood noise variance and the inducing points Z (the quantities
         GPflow trains; values are w.r.t. the constrained parameters).
+
+        With the packed statistics (engine "i8", the default) and tail
+        "packed", the gradient runs inside memory_limit through
+        ``tb_sgpr_grad_run`` (``_elbo_and_grads_packed``); otherwise the dense
+        path below (fp64 engines, or tail="dense").
 
         The O(M^3) tail is differentiated analytically on dense fp64
         matrices (cuSOLVER Cholesky / inverse, cuBLAS; at most ~4 M x M live):
@@ -268,6 +300,8 @@ class SGPR:
         all-reduced like the statistics.  Returns (elbo, dict of gradients)."""
         torch = _torch()
         M, dim = int(self.Z.shape[0]), self.dim
+        if self.tail == "packed" and dim <= 16 and self.grad_peak_bytes() >= 0:
+            return self._elbo_and_grads_packed()
         if self.memory_limit is not None:
             limit = as_limit(self.memory_limit)
             resident = (self.X.numel() + self.y.numel() + self.Z.numel()) * self.X.element_size()
@@ -361,6 +395,68 @@ class SGPR:
                  "lengthscales": grad_hyp[1:].cpu().numpy(),
                  "noise_variance": d_s2,
                  "Z": grad_z.cpu().numpy()}
+        return float(elbo), grads
+
+    def _elbo_and_grads_packed(self):
+        """tb_sgpr_grad_run: only the packed factors L = chol(Kuu) and
+        P = chol(Kuu + Sigma/s2) stay resident; 2 dELBO/dKuu and
+        2 dELBO/dSigma are produced and consumed one 128-column panel at a
+        time (DESIGN.md §4 "Gradient").  Consumes the statistics."""
+        torch = _torch()
+        M, dim = int(self.Z.shape[0]), self.dim
+        if self.memory_limit is not None:
+            limit = as_limit(self.memory_limit)
+            need = self.grad_peak_bytes()
+            if need > limit:
+                resident = (self.X.numel() + self.y.numel() + self.Z.numel()) * \
+                    self.X.element_size()
+                raise BudgetExceeded(
+                    "sgpr_elbo_and_grads", need, resident,
+                    message=f"sgpr_elbo_and_grads: needs {need} bytes on the device "
+                            f"(memory_limit={limit})")
+        s = self._stats if self._stats is not None and self._stats.Sigma is not None \
+            else self.statistics()
+        p = s.plan
+        f64 = torch.float64
+        dev = self.device
+        lib = _lib.load()
+        st = torch.cuda.current_stream(dev)
+        wsb = int(lib.tb_sgpr_grad_workspace(ctypes.byref(p)))
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        out8 = torch.zeros(8, dtype=f64, device=dev)
+        gh = torch.zeros(2 * (1 + dim), dtype=f64, device=dev)
+        gz = torch.zeros(2 * M * dim, dtype=f64, device=dev)
+        rc = lib.tb_sgpr_grad_run(ctypes.byref(p), self.X.data_ptr(), self.y.data_ptr(),
+                                  self.Z.data_ptr(), self.variance,
+                                  self.lengthscales.ctypes.data_as(ctypes.c_void_p), self.jitter,
+                                  self.noise_variance, s.Sigma.data_ptr(), s.v.data_ptr(),
+                                  out8.data_ptr(), gh.data_ptr(), gz.data_ptr(), ws.data_ptr(),
+                                  ws.numel(), st.cuda_stream)
+        s.Sigma = None                         # overwritten by the factor P
+        self._w = None
+        _lib.check(rc, "sgpr_grad_run")
+        del ws
+        if self.group is not None:             # data-side sums over the ranks' rows
+            import torch.distributed as dist
+            dist.all_reduce(gh[:1 + dim], group=self.group)
+            dist.all_reduce(gz[:M * dim], group=self.group)
+        sl, sp, uu, tr_ka, tr_ak, wkw = (float(t) for t in out8[:6].tolist())
+        N, s2, var, yy = float(s.N), self.noise_variance, self.variance, s.yy
+        logdet_k, logdet_a = 2.0 * sl, 2.0 * sp
+        vw = uu / s2                                 # v^T A^-1 v / s2
+        tr_ks = s2 * (tr_ka - M)                     # tr(Kuu^-1 Sigma)
+        tr_as = s2 * (M - tr_ak)                     # tr(A^-1 Sigma)
+        wsw = vw - s2 * wkw                          # w^T Sigma w
+        elbo = (-0.5 * N * LOG2PI - 0.5 * (logdet_a - logdet_k) - 0.5 * N * math.log(s2)
+                - 0.5 * yy / s2 + 0.5 * vw / s2 - 0.5 * N * var / s2 + 0.5 * tr_ks / s2)
+        d_s2 = (0.5 * tr_as / s2**2 + 0.5 * wsw / s2**2 - vw / s2**2 - 0.5 * N / s2
+                + 0.5 * yy / s2**2 + 0.5 * N * var / s2**2 - 0.5 * tr_ks / s2**2)
+        hyp = gh[:1 + dim] + 0.5 * gh[1 + dim:]
+        gzs = (gz[:M * dim] + gz[M * dim:]).reshape(M, dim)
+        grads = {"variance": -0.5 * N / s2 + float(hyp[0]),
+                 "lengthscales": hyp[1:].cpu().numpy(),
+                 "noise_variance": d_s2,
+                 "Z": gzs.cpu().numpy()}
         return float(elbo), grads
 
     def predict_mean(self, Xnew):

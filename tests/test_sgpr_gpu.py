@@ -162,7 +162,7 @@ def test_gradient_memory_estimate_and_budget():
     from paper_2206_14148_b200.sgpr import grad_memory_bytes
     N, d, M, chunk = 30000, 4, 1536, 2048
     X, y, Z, _ = synthetic.sgpr_data(N, d, M, seed=5, dtype=np.float32)
-    m = tb.SGPR(X, y, Z, "rbf", 1.0, 0.7, 0.05)
+    m = tb.SGPR(X, y, Z, "rbf", 1.0, 0.7, 0.05, tail="dense")
     m.statistics()
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats()
@@ -173,7 +173,8 @@ def test_gradient_memory_estimate_and_budget():
     est = grad_memory_bytes(M, d, chunk)
     assert peak <= est <= 2.0 * peak, (peak, est)
     resident = (X.size + y.size + Z.size) * 4
-    small = tb.SGPR(X, y, Z, "rbf", 1.0, 0.7, 0.05, memory_limit=resident + est // 2)
+    small = tb.SGPR(X, y, Z, "rbf", 1.0, 0.7, 0.05, memory_limit=resident + est // 2,
+                    tail="dense")
     with pytest.raises(tb.BudgetExceeded):
         small.elbo_and_grads(chunk_n=chunk)
 
@@ -292,3 +293,58 @@ def test_sgpr_full_c4_i8_engine_matches_fp64_engine():
     mua, mub = (t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t) for t in (mua, mub))
     assert abs(ea - eb) <= 1e-6 * abs(eb), (ea, eb)
     assert rel_err(mua, mub) <= 1e-4
+
+
+@pytest.mark.parametrize("N,d,M,kind", [(3000, 3, 25, "rbf"), (5000, 3, 300, "matern32"),
+                                        (4000, 11, 200, "rbf")])
+def test_packed_gradient_matches_finite_differences_and_dense(N, d, M, kind):
+    """The in-budget gradient (tb_sgpr_grad_run: packed factors, column
+    panels, fused data kernel) against central differences of the fp64
+    oracle ELBO and against the dense autograd-free path on the same
+    fixed-point statistics; M = 300 pads to 3 tiles, d = 11 takes the
+    16-wide instance of the data kernel."""
+    X, y, Z, _ = synthetic.sgpr_data(N, d, M, seed=17, dtype=np.float32)
+    ls = [0.9, 1.3, 0.7, 1.1, 0.8, 1.2, 1.0, 0.95, 1.05, 1.15, 0.85][:d]
+    e1, g1 = tb.SGPR(X, y, Z, kind, 1.4, ls, 0.05).elbo_and_grads()
+    e2, g2 = tb.SGPR(X, y, Z, kind, 1.4, ls, 0.05, tail="dense").elbo_and_grads(chunk_n=1024)
+    assert abs(e1 - e2) <= 1e-9 * abs(e2)
+    for key in ("variance", "noise_variance", "lengthscales", "Z"):
+        a, b = np.asarray(g1[key], np.float64), np.asarray(g2[key], np.float64)
+        assert np.max(np.abs(a - b)) <= 1e-6 * max(np.max(np.abs(b)), 1.0), key
+    if M <= 25:
+        fd = osgpr.elbo_grads_fd(X, y, Z, kind, 1.4, ls, 0.05)
+        for key in ("variance", "noise_variance", "lengthscales", "Z"):
+            a, b = np.asarray(g1[key], np.float64), np.asarray(fd[key], np.float64)
+            assert np.max(np.abs(a - b)) <= 1e-3 * max(np.max(np.abs(b)), 1.0), key
+
+
+def test_packed_gradient_inside_memory_limit():
+    """elbo_and_grads at a limit the dense tail cannot meet: the packed path
+    plans its peak (grad_peak_bytes), stays under the limit on the device
+    and returns the dense path's numbers."""
+    import torch
+    N, d, M = 30000, 3, 1500
+    X, y, Z, _ = synthetic.sgpr_data(N, d, M, seed=19, dtype=np.float32)
+    from paper_2206_14148_b200.sgpr import grad_memory_bytes
+    resident = (N * d + N + M * d) * 4
+    limit = resident + 2 * 8 * M * M // 2 + 24 * 10**6     # ~ two packed triangles + panels
+    assert grad_memory_bytes(M, d) + resident > limit          # the dense tail would not fit
+    Xd, yd, Zd = (torch.from_numpy(a).cuda() for a in (X, y, Z))
+    m = tb.SGPR(Xd, yd, Zd, "matern32", 1.0, 0.6, 0.02, memory_limit=limit)
+    planned = m.grad_peak_bytes()
+    assert planned <= limit
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated() - (Xd.numel() + yd.numel() + Zd.numel()) * 4
+    torch.cuda.reset_peak_memory_stats()
+    e, g = m.elbo_and_grads()
+    torch.cuda.synchronize()
+    peak = torch.cuda.max_memory_allocated() - base
+    assert peak <= limit, (peak, limit)
+    e2, g2 = tb.SGPR(X, y, Z, "matern32", 1.0, 0.6, 0.02, tail="dense").elbo_and_grads()
+    assert abs(e - e2) <= 1e-9 * abs(e2)
+    # Matern l = 0.6 with 1500 inducing points is ill-conditioned (cond(Kuu)
+    # ~ 1e5+): the two tails' explicit-inverse vs triangular-solve rounding
+    # differ at ~1e-5 of the largest dELBO/dZ entry
+    for key in ("variance", "noise_variance", "lengthscales", "Z"):
+        a, b = np.asarray(g[key], np.float64), np.asarray(g2[key], np.float64)
+        assert np.max(np.abs(a - b)) <= 1e-4 * max(np.max(np.abs(b)), 1.0), key
