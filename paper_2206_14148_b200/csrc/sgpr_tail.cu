@@ -1039,6 +1039,206 @@ gp_data_kernel(const T* __restrict__ X, const T* __restrict__ y, const double* _
   }
 }
 
+// Same contract as gp_data_kernel, d <= 12: each inducing tile's Kuf block
+// (128 x 128) is generated once into shared memory by all 256 threads with
+// 4 independent exps in flight per thread, then the DMMA loop reads it
+// there (the loader-side generation of gp_data_kernel serialises every
+// exp with the MMA issue of its warp).
+constexpr int kBld = kTT + 4;
+template <typename T>
+__global__ void __launch_bounds__(256, 1)
+gp_data12_kernel(const T* __restrict__ X, const T* __restrict__ y, const double* __restrict__ Zs,
+                 const double* __restrict__ G, const double* __restrict__ w, double inv_s2, int P,
+                 int nt, int64_t M, int64_t N, KernParams p, double* __restrict__ part_hyp,
+                 double* __restrict__ part_z) {
+  constexpr int DMAX = 12;
+  extern __shared__ __align__(16) double gsm[];
+  double* Bf = gsm;                                       // [128][kBld] Kuf block
+  double* As = Bf + kTT * kBld;                           // 2 * kGKc * kGLd staging
+  double* zt = As + 2 * kGKc * kGLd;                      // [128][DMAX]
+  double* zp = zt + kTT * DMAX;
+  double* xb = zp + kTT * DMAX;
+  double* yb = xb + kTT * DMAX;                           // [128]
+  double* gp_s = yb + kTT;                                // [128]
+  double* zacc = gp_s + kTT;                              // [128][DMAX]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wr = warp >> 2, wc = warp & 3, g = lane >> 2, tg = lane & 3;
+  const int dim = p.dim;
+  for (int e = tid; e < kTT * DMAX; e += blockDim.x) {
+    const int r = e / DMAX, t = e % DMAX;
+    const int64_t i = (int64_t)P * kTT + r;
+    zp[e] = (t < dim && i < M) ? Zs[i * dim + t] : 0.0;
+    zacc[e] = 0.0;
+  }
+  for (int r = tid; r < kTT; r += blockDim.x) {
+    const int64_t i = (int64_t)P * kTT + r;
+    gp_s[r] = i < M ? w[i] * inv_s2 : 0.0;
+  }
+  double gv = 0.0, gl[DMAX];
+#pragma unroll
+  for (int t = 0; t < DMAX; ++t) gl[t] = 0.0;
+  const int64_t nblk = (N + kTT - 1) / kTT;
+  const int cpt = tid & 127, kh = tid >> 7;               // generation: point, row parity
+  const int rr = tid >> 1, rk = (tid & 1) * 8;            // A loader ("row" pattern, ta)
+  for (int64_t nb = blockIdx.x; nb < nblk; nb += gridDim.x) {
+    __syncthreads();
+    for (int e = tid; e < kTT * DMAX; e += blockDim.x) {
+      const int r = e / DMAX, t = e % DMAX;
+      const int64_t n = nb * kTT + r;
+      xb[e] = (t < dim && n < N) ? (double)X[n * dim + t] * p.inv_ls[t] : 0.0;
+    }
+    for (int r = tid; r < kTT; r += blockDim.x) {
+      const int64_t n = nb * kTT + r;
+      yb[r] = n < N ? (double)y[n] : 0.0;
+    }
+    __syncthreads();
+    double xr[DMAX];
+#pragma unroll
+    for (int t = 0; t < DMAX; ++t) xr[t] = xb[cpt * DMAX + t];
+    const bool pvalid = nb * kTT + cpt < N;
+    double acc[8][4][2];
+    acc_zero(acc);
+    for (int kt = 0; kt < nt; ++kt) {
+      const int64_t ibase = (int64_t)kt * kTT;
+      for (int e = tid; e < kTT * DMAX; e += blockDim.x) {
+        const int r = e / DMAX, t = e % DMAX;
+        zt[e] = (t < dim && ibase + r < M) ? Zs[(ibase + r) * dim + t] : 0.0;
+      }
+      __syncthreads();                                    // zt ready; Bf free (prev. MMAs done)
+      // generate Kuf(ibase + k, point cpt) for k = kh, kh + 2, ...: 4 in flight
+      for (int k0 = kh; k0 < kTT; k0 += 8) {
+        double r2[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) r2[u] = 0.0;
+#pragma unroll
+        for (int t = 0; t < DMAX; ++t)
+          if (t < dim) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double df = zt[(k0 + 2 * u) * DMAX + t] - xr[t];
+              r2[u] = fma(df, df, r2[u]);
+            }
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + 2 * u;
+          Bf[k * kBld + cpt] = (pvalid && ibase + k < M) ? kern_from_r2(p, r2[u]) : 0.0;
+        }
+      }
+      // acc(r, c) += sum_k G(ibase + k, r) Bf(k, c): A = G tile (transposed)
+      const double* A = G + (int64_t)kt * kTE;
+      double ra[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ra[q] = A[(int64_t)rr * kTT + rk + q];
+      int stage = 0;
+      for (int k0 = 0; k0 < kTT; k0 += kGKc) {
+        double* as = As + stage * kGKc * kGLd;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) as[(rk + q) * kGLd + rr] = ra[q];
+        __syncthreads();                                  // also: Bf generated (first pass)
+        if (k0 + kGKc < kTT) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) ra[q] = A[(int64_t)rr * kTT + k0 + kGKc + rk + q];
+        }
+#pragma unroll
+        for (int ks = 0; ks < kGKc / 4; ++ks) {
+          double af[8], bf[4];
+          const double* ak = as + (ks * 4 + tg) * kGLd + wr * 64 + g;
+          const double* bk2 = Bf + (k0 + ks * 4 + tg) * kBld + wc * 32 + g;
+#pragma unroll
+          for (int a = 0; a < 8; ++a) af[a] = ak[a * 8];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) bf[b] = bk2[b * 8];
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+        stage ^= 1;
+      }
+      __syncthreads();                                    // Bf, zt consumed
+    }
+    // epilogue: W and the kernel-derivative contraction (as gp_data_kernel)
+    double* red = Bf;                                     // [4 wc][128][DMAX]
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int r = wr * 64 + a * 8 + g;
+      double gz[DMAX];
+#pragma unroll
+      for (int t = 0; t < DMAX; ++t) gz[t] = 0.0;
+      const bool rvalid = (int64_t)P * kTT + r < M;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = wc * 32 + b * 8 + 2 * tg + e;
+          if (!rvalid || nb * kTT + c >= N) continue;
+          const double W = acc[a][b][e] * inv_s2 + gp_s[r] * yb[c];
+          double r2 = 0.0;
+#pragma unroll
+          for (int t = 0; t < DMAX; ++t)
+            if (t < dim) {
+              const double df = zp[r * DMAX + t] - xb[c * DMAX + t];
+              r2 = fma(df, df, r2);
+            }
+          const double k = kern_from_r2(p, r2);
+          double dk;
+          if (p.kernel == TB_KERNEL_RBF) {
+            dk = -0.5 * k;
+          } else {
+            const double rq = sqrt(fmax(r2, 1e-36));
+            dk = -1.5 * p.variance * exp(-1.7320508075688772 * rq);
+          }
+          const double wd = W * dk;
+          gv = fma(W, k, gv);
+#pragma unroll
+          for (int t = 0; t < DMAX; ++t)
+            if (t < dim) {
+              const double df = zp[r * DMAX + t] - xb[c * DMAX + t];
+              gl[t] = fma(wd * df * df, -2.0 * p.inv_ls[t], gl[t]);
+              gz[t] = fma(wd * df, 2.0 * p.inv_ls[t], gz[t]);
+            }
+        }
+#pragma unroll
+      for (int t = 0; t < DMAX; ++t) {
+        double v = gz[t];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (tg == 0) red[((int64_t)wc * kTT + r) * DMAX + t] = v;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < kTT * DMAX; e += blockDim.x) {
+      const int r = e / DMAX, t = e % DMAX;
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v += red[((int64_t)q * kTT + r) * DMAX + t];
+      zacc[e] += v;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < kTT * DMAX; e += blockDim.x)
+    part_z[(int64_t)blockIdx.x * kTT * DMAX + e] = zacc[e];
+  double* hred = Bf;
+  __syncthreads();
+  gv = warp_sum(gv);
+  if (lane == 0) hred[warp * (1 + DMAX)] = gv;
+#pragma unroll
+  for (int t = 0; t < DMAX; ++t) {
+    const double v = warp_sum(gl[t]);
+    if (lane == 0) hred[warp * (1 + DMAX) + 1 + t] = v;
+  }
+  __syncthreads();
+  if (tid < 1 + DMAX) {
+    double v = 0.0;
+    for (int q = 0; q < 8; ++q) v += hred[q * (1 + DMAX) + tid];
+    part_hyp[(int64_t)blockIdx.x * (1 + DMAX) + tid] = tid == 0 ? v / p.variance : v;
+  }
+}
+static size_t gp_data12_smem() {
+  return (size_t)(kTT * kBld + 2 * kGKc * kGLd + 4 * kTT * 12 + 2 * kTT) * sizeof(double);
+}
+
 // grad_hyp[j] += sum_b part_hyp[b][j] (j < 1 + dim); grad_z[(P*128 + r)*dim + t]
 // += sum_b part_z[b][r][t]  (fixed order)
 __global__ void gp_data_reduce_kernel(const double* __restrict__ part_hyp,
@@ -1069,7 +1269,7 @@ static size_t gp_data_smem(int dmax) {
 
 int64_t grad_tail_workspace_bytes(int64_t M, int64_t M_pad, int64_t dim) {
   const int64_t nt = M_pad / kTT, tiles = nt * (nt + 1) / 2;
-  const int64_t dmax = dim <= 4 ? 4 : 16;
+  const int64_t dmax = dim <= 12 ? 12 : 16;
   return round_up(tiles * kTE * 8, 256)                 // L (packed)
          + round_up(2 * nt * kTE * 8, 256)              // diagonal inverses of L, P
          + 3 * round_up(M_pad * kTT * 8, 256)           // three column panels
@@ -1095,7 +1295,8 @@ int grad_tail_run(int64_t M, int64_t M_pad, const void* Z, const void* X, const 
   const int nt = (int)(M_pad / kTT);
   const int tiles = nt * (nt + 1) / 2;
   const int dim = kp.dim;
-  const int dmax = dim <= 4 ? 4 : 16;
+  // data kernel: d <= 12 -> gp_data12_kernel (12-wide), else the 16-wide loader version
+  const int dmax = dim <= 12 ? 12 : 16;
   char* ws = (char*)workspace;
   auto take = [&](int64_t bytes) { char* q = ws; ws += round_up(bytes, 256); return q; };
   double* L = (double*)take((int64_t)tiles * kTE * 8);
@@ -1173,14 +1374,18 @@ int grad_tail_run(int64_t M, int64_t M_pad, const void* Z, const void* X, const 
   if ((rc = tail_solve(Pf, invP, nt, u, scratch, w, 1, st))) return rc;
   scale_copy_kernel<<<(unsigned)ceil_div(M_pad, 256), 256, 0, st>>>(w, M, M_pad, 1.0 / s2, w);
   TB_LAUNCH_CHECK("grad_vec");
-  TB_CUDA_TRY(cudaFuncSetAttribute(dmax == 4 ? (const void*)gp_data_kernel<float, 4>
-                                             : (const void*)gp_data_kernel<float, 16>,
+  TB_CUDA_TRY(cudaFuncSetAttribute((const void*)gp_data12_kernel<float>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)gp_data_smem(dmax)));
-  TB_CUDA_TRY(cudaFuncSetAttribute(dmax == 4 ? (const void*)gp_data_kernel<double, 4>
-                                             : (const void*)gp_data_kernel<double, 16>,
+                                   (int)gp_data12_smem()));
+  TB_CUDA_TRY(cudaFuncSetAttribute((const void*)gp_data12_kernel<double>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)gp_data_smem(dmax)));
+                                   (int)gp_data12_smem()));
+  TB_CUDA_TRY(cudaFuncSetAttribute((const void*)gp_data_kernel<float, 16>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)gp_data_smem(16)));
+  TB_CUDA_TRY(cudaFuncSetAttribute((const void*)gp_data_kernel<double, 16>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)gp_data_smem(16)));
   const int64_t pn = M_pad * kTT;
   const unsigned eb = (unsigned)std::min<int64_t>(ceil_div(pn, 256), 4096);
   const int kd_blocks = 256;
@@ -1220,15 +1425,15 @@ int grad_tail_run(int64_t M, int64_t M_pad, const void* Z, const void* X, const 
     }
     // data side: all N points against G2[:, P]
     if (dtype == TB_F32) {
-      if (dmax == 4)
-        gp_data_kernel<float, 4><<<kGpGrid, 256, gp_data_smem(4), st>>>(
+      if (dmax == 12)
+        gp_data12_kernel<float><<<kGpGrid, 256, gp_data12_smem(), st>>>(
             (const float*)X, (const float*)y, Zs, B0, w, 1.0 / s2, P, nt, M, N, kp, ph, pz);
       else
         gp_data_kernel<float, 16><<<kGpGrid, 256, gp_data_smem(16), st>>>(
             (const float*)X, (const float*)y, Zs, B0, w, 1.0 / s2, P, nt, M, N, kp, ph, pz);
     } else {
-      if (dmax == 4)
-        gp_data_kernel<double, 4><<<kGpGrid, 256, gp_data_smem(4), st>>>(
+      if (dmax == 12)
+        gp_data12_kernel<double><<<kGpGrid, 256, gp_data12_smem(), st>>>(
             (const double*)X, (const double*)y, Zs, B0, w, 1.0 / s2, P, nt, M, N, kp, ph, pz);
       else
         gp_data_kernel<double, 16><<<kGpGrid, 256, gp_data_smem(16), st>>>(
