@@ -534,7 +534,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     // Units outer, tiles inner: the per-tile path carries no unit bookkeeping
     // (it was ~1/3 of the epilogue's issue slots when every tile computed its
     // successor with integer divisions).  Shared bounds are read with weak
-    // L2 loads (ld.global.cg) one tile ahead of their use.
+    // loads one tile ahead of their use.
     int i = 0;
     for (int u = grp; u < units; u += ngrp) {
       const int slice = u / qunits;
@@ -562,8 +562,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         }
         const float thr_g = qv ? fminf(fkey_inv(gk) * sc_mul, pool_thr) : -INFINITY;
         if (qv) {
-          pk = __ldcg(qpool + p_slot);
-          gk = __ldcg(gthr + q);
+          // plain (weak, L1-cacheable) loads: both bounds only ever decrease,
+          // so a stale copy is a looser but still valid bound (C2 engine
+          // 2.369 -> 2.346 ms same-box against ld.global.cg)
+          pk = qpool[p_slot];
+          gk = gthr[q];
         }
         if (ew == 0 && lane == 0) { TB_TR(1024, i, 0); }
         mbar_wait(&tfull[buf], (i >> 1) & 1);
