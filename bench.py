@@ -35,10 +35,11 @@ sys.path.insert(0, ROOT)
 # NCCL's communicator INIT lines go to a per-process log file (NCCL prints to
 # stdout otherwise, and stdout must stay the one JSON line); each rank
 # forwards them to its stderr when it finishes (_forward_nccl_log).
-if "NCCL_DEBUG" not in os.environ:
+if "NCCL_DEBUG_FILE" not in os.environ and \
+        os.environ.get("NCCL_DEBUG", "WARN").upper() in ("WARN", "VERSION", ""):
     os.environ["NCCL_DEBUG"] = "INFO"
-    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-    os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/tb_bench_nccl.%h.{os.getpid()}.log")
+    os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+    os.environ["NCCL_DEBUG_FILE"] = f"/tmp/tb_bench_nccl.%h.{os.getpid()}.log"
 
 N_DB, M_Q, DIM, K = 1_000_000, 10_000, 128, 10
 LIMIT = 10**9
