@@ -53,6 +53,9 @@ def _raise(exc):
     raise exc
 
 
+_COSINE_CHECK_BYTES = 1 << 20
+
+
 def plan(n: int, m: int, d: int, k: int, *, metric: str = "l2", dtype=np.float32,
          out_dtype=None, engine: str = "auto", memory_limit=None,
          resident_bytes: int | None = None, max_chunk_rows: int = 0) -> _lib.KnnPlan:
@@ -71,6 +74,8 @@ def plan(n: int, m: int, d: int, k: int, *, metric: str = "l2", dtype=np.float32
     es = np.dtype(dtype).itemsize
     if resident_bytes is None:
         resident_bytes = (n + m) * d * es
+    if metric == "cosine":
+        resident_bytes += _COSINE_CHECK_BYTES      # the zero-row check's scratch
     p = _lib.KnnPlan()
     lib = _lib.load()
     rc = lib.tb_knn_plan_create_ex(n, m, d, k, _lib.METRICS[metric], _tb_dtype(dtype),
@@ -123,12 +128,19 @@ class KnnOperator:
 
     def _check_cosine(self, x, q):
         """Cosine distance is undefined for all-zero rows: the reference
-        rejects them with ValueError (frontend.py:126-135)."""
+        rejects them with ValueError (frontend.py:126-135).  Row max-norms are
+        taken in chunks whose scratch stays inside the _COSINE_CHECK_BYTES the
+        planner reserves (a whole-matrix abs() would briefly double the
+        input's footprint past memory_limit)."""
         if self.metric != "cosine":
             return
+        torch = _torch()
         for t in (x, q):
-            if bool((t.abs().amax(dim=1) == 0).any()):
-                raise ValueError("cosine distance is undefined for zero rows")
+            rows = max(1, _COSINE_CHECK_BYTES // (2 * (t.element_size() + 1)))
+            for s0 in range(0, int(t.shape[0]), rows):
+                nrm = torch.linalg.vector_norm(t[s0:s0 + rows], ord=float("inf"), dim=1)
+                if bool((nrm == 0).any()):
+                    raise ValueError("cosine distance is undefined for zero rows")
 
     def alloc_outputs(self):
         torch = _torch()

@@ -1,0 +1,76 @@
+"""memory_limit is a hard bound on the device (the reference's budget,
+interpreter.py:149-151,543-546): for randomly drawn shapes and limits, the
+planned peak is checked against the limit before any work and the measured
+peak (caching-allocator bytes, inputs included) never exceeds it - kNN
+(all three metrics, host and device inputs), the SGPR ELBO and the SGPR
+training gradient."""
+
+import numpy as np
+import pytest
+
+import paper_2206_14148_b200 as tb
+from paper_2206_14148_b200 import neighbors, synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+def _measure(fn):
+    import torch
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    out = fn()
+    torch.cuda.synchronize()
+    return out, torch.cuda.max_memory_allocated() - base
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_knn_random_limits_hold_on_the_device(seed):
+    import torch
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(2_000, 200_000))
+    m = int(rng.integers(1, 3_000))
+    d = int(rng.choice([3, 16, 64, 128, 200]))
+    k = int(rng.integers(1, min(33, n + 1)))
+    metric = ["l2", "cosine", "l1"][seed % 3]
+    x = torch.randn((n, d), device="cuda")
+    q = torch.randn((m, d), device="cuda")
+    inputs = (n + m) * d * 4
+    free = neighbors.plan(n, m, d, k, metric=metric).peak_bytes - inputs
+    limit = inputs + int(free * rng.uniform(0.15, 1.2)) + 4 * 2**20
+    try:
+        p = neighbors.plan(n, m, d, k, metric=metric, memory_limit=limit)
+    except tb.BudgetExceeded:
+        return                                   # refused before any allocation
+    assert p.peak_bytes <= limit
+    (dist, idx), peak = _measure(lambda: tb.knn(x, q, k, metric=metric, memory_limit=limit))
+    assert peak + inputs <= limit, (peak + inputs, limit, p.peak_bytes)
+    assert dist.shape == (m, k)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_sgpr_random_limits_hold_on_the_device(seed):
+    import torch
+    rng = np.random.default_rng(200 + seed)
+    N = int(rng.integers(5_000, 60_000))
+    M = int(rng.integers(100, 800))
+    d = int(rng.integers(3, 6))              # (1-D Z with 1000+ points is not PD in fp64)
+    X, y, Z, _ = synthetic.sgpr_data(N, d, M, seed=seed, dtype=np.float32)
+    Xd, yd, Zd = (torch.from_numpy(a).cuda() for a in (X, y, Z))
+    inputs = (N * d + N + M * d) * 4
+    full = tb.sgpr.plan(N, M, d).peak_bytes
+    limit = inputs + int((full - inputs) * rng.uniform(0.4, 1.1)) + 2**20
+    m = tb.SGPR(Xd, yd, Zd, "rbf", 1.0, 0.5, 0.05, memory_limit=limit)
+    try:
+        e, peak = _measure(m.elbo)
+    except tb.BudgetExceeded:
+        return
+    assert peak + inputs <= limit, (peak + inputs, limit)
+    assert np.isfinite(e)
+    need = m.grad_peak_bytes()
+    m2 = tb.SGPR(Xd, yd, Zd, "rbf", 1.0, 0.5, 0.05, memory_limit=max(limit, need))
+    (e2, g), peak2 = _measure(m2.elbo_and_grads)
+    assert peak2 + inputs <= max(limit, need), (peak2 + inputs, need)
+    # two tail formulations; the ELBO is a small difference of O(N var / s2)
+    # terms, which they round differently at ~1e-10 of their size
+    assert abs(e2 - e) <= 1e-9 * max(abs(e), N * 1.0 / 0.05)
