@@ -153,6 +153,14 @@ TB_API int tb_topk_merge(const void* dist_lists, const int64_t* idx_lists,
 TB_API int tb_knn_fallback_count(const tb_knn_plan* plan, const void* workspace,
                           void* stream, int64_t* count);
 
+/* Input check of the last tb_knn_run / tb_knn_run_host on this plan:
+ * TB_ERR_ARG ("cosine distance is undefined for zero rows") when the cosine
+ * operand prep met an all-zero database or query row, else TB_OK.  Replaces
+ * the reference's host-side zero-norm scan (frontend.py:126-135): the prep
+ * kernels flag the rows while they normalise, so the check costs no pass over
+ * the inputs.  Synchronises the stream. */
+TB_API int tb_knn_check(const tb_knn_plan* plan, const void* workspace, void* stream);
+
 /* ---------------- SGPR sufficient statistics ----------------------------
  * Sigma = Kuf Kuf^T (M x M, fp64), v = Kuf y (M, fp64), yy = y^T y, for
  * X[N,dim], y[N], Z[M,dim] (dtype), accumulated over N in ascending order.

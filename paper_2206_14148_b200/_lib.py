@@ -69,6 +69,7 @@ _SIGS = {
     "tb_topk_merge": (ctypes.c_int, [_vp, _vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp]),
     "tb_knn_fallback_count": (ctypes.c_int, [ctypes.POINTER(KnnPlan), _vp, _vp,
                                              ctypes.POINTER(_i64)]),
+    "tb_knn_check": (ctypes.c_int, [ctypes.POINTER(KnnPlan), _vp, _vp]),
     "tb_sgpr_plan_create": (ctypes.c_int, [_i64, _i64, _i64, _i32, _i32, _i32, _i64, _i64,
                                            ctypes.POINTER(SgprPlan)]),
     "tb_sgpr_stats_run": (ctypes.c_int, [ctypes.POINTER(SgprPlan), _vp, _vp, _vp,

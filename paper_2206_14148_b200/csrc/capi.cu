@@ -481,6 +481,17 @@ int tb_knn_fallback_count(const tb_knn_plan* p, const void* workspace,
   return TB_OK;
 }
 
+int tb_knn_check(const tb_knn_plan* p, const void* workspace, void* stream) {
+  if (!p || !workspace) return fail(TB_ERR_ARG, "null argument");
+  if (p->metric != TB_METRIC_COSINE) return TB_OK;
+  unsigned v = 0;
+  const char* ws = (const char*)workspace;
+  TB_CUDA_TRY(cudaMemcpyAsync(&v, ws + p->off[kStats] + 4 * kZeroRowWord, 4,
+                              cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  TB_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return v ? fail(TB_ERR_ARG, "cosine distance is undefined for zero rows") : TB_OK;
+}
+
 int tb_topk_merge(const void* dist_lists, const int64_t* idx_lists,
                   int32_t n_lists, int64_t m, int64_t k, int32_t dtype,
                   void* out_dist, int64_t* out_idx, void* stream) {

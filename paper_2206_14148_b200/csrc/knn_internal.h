@@ -31,8 +31,10 @@ enum KnnSlot {
 // bits, [3] max |q| bits, [4] max |x| bits of the current chunk, [5] the
 // chunk's max ||x - fp16 x||, [kF16Slot..+3] fp16 engine scales (floats:
 // s, t, alpha, 1/(s t)), [12] redo flag of the chunk conversion, [13] max 1/t,
-// [14] centring flag, [15] max |mu|; words 64.. hold mu (fp64 [d]) for tc1
+// [14] centring flag, [15] max |mu|, [16] cosine zero-row flag; words 64..
+// hold mu (fp64 [d]) for tc1
 constexpr int kF16Slot = 8;
+constexpr int kZeroRowWord = 16;
 
 struct KnnDims {
   int64_t n, m, d, k;
@@ -44,7 +46,7 @@ struct KnnDims {
 int launch_query_prep(int dtype, int metric, const void* q, int64_t m, int64_t d,
                       double* qn64, float* qnorm, __nv_bfloat16* qhi,
                       __nv_bfloat16* qlo, int64_t m_pad, int64_t d_pad,
-                      cudaStream_t st, const unsigned* centre = nullptr);
+                      cudaStream_t st, unsigned* centre = nullptr);
 int launch_db_prep(int dtype, int metric, const void* x, int64_t rows, int64_t d,
                    float* xn, unsigned* xmax_bits, __nv_bfloat16* xhi,
                    __nv_bfloat16* xlo, int64_t rows_pad, int64_t d_pad,

@@ -76,7 +76,7 @@ rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
                   float* __restrict__ norm32, unsigned* __restrict__ max_bits,
                   __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo,
                   int64_t rows_pad, int64_t d_pad, double scale,
-                  uint8_t* __restrict__ ext, const unsigned* __restrict__ centre) {
+                  uint8_t* __restrict__ ext, unsigned* __restrict__ centre) {
   __shared__ float wmax[8];
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t r = gt / G;
@@ -95,6 +95,9 @@ rows_split_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
     inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+    // cosine is undefined for an all-zero row: flag it (stats word
+    // kZeroRowWord, read back by tb_knn_check) instead of a separate pass
+    if (centre && seg == 0 && r < rows && nn == 0.0) centre[kZeroRowWord] = 1u;
   }
   double acc = 0.0;
   for (int64_t c0 = (int64_t)seg * 8; r < rows_pad && c0 < d_pad; c0 += 8 * G) {
@@ -188,7 +191,7 @@ static int rows_prep(const void* src, int64_t rows, int64_t d, double* n64,
                      float* n32, float* norm32, unsigned* max_bits,
                      __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t rows_pad,
                      int64_t d_pad, cudaStream_t st, int metric, double scale = 1.0,
-                     uint8_t* ext = nullptr, const unsigned* centre = nullptr) {
+                     uint8_t* ext = nullptr, unsigned* centre = nullptr) {
   const int64_t limit = hi ? rows_pad : rows;
   if (limit <= 0) return TB_OK;
   if (hi && d_pad % 64 == 0) {
@@ -356,6 +359,7 @@ rows_f16_kernel(const T* __restrict__ src, int64_t rows, int64_t d,
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
     inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+    if (seg == 0 && r < rows && nn == 0.0) stats[kZeroRowWord] = 1u;   // see rows_split_kernel
   }
   double acc = 0.0, rn = 0.0;
   float rnf = 0.f, accf = 0.f;
@@ -683,7 +687,7 @@ int launch_db_prep_f16(int dtype, int metric, const void* x, int64_t rows, int64
 int launch_query_prep(int dtype, int metric, const void* q, int64_t m, int64_t d,
                       double* qn64, float* qnorm, __nv_bfloat16* qhi,
                       __nv_bfloat16* qlo, int64_t m_pad, int64_t d_pad,
-                      cudaStream_t st, const unsigned* centre) {
+                      cudaStream_t st, unsigned* centre) {
   // the tensor-core engines use 2q (exact) so that acc' = 2 q.x - ||x||^2
   if (dtype == TB_F32)
     return rows_prep<float>(q, m, d, qn64, nullptr, qnorm, nullptr, qhi, qlo, m_pad, d_pad, st,

@@ -384,7 +384,6 @@ def evaluate(graph: Graph, inputs, budget: int | None = None, *,
         led = _DeviceLedger(dev, poison_freed)
         x = led.alloc(f"{graph.name}/param0", torch.from_numpy(arrays[0]).to(dev))
         q = led.alloc(f"{graph.name}/param1", torch.from_numpy(arrays[1]).to(dev))
-        op._check_cosine(x, q)
         ws = led.alloc(f"{graph.name}/workspace", op.allocate_workspace())
         dist, idx = op.alloc_outputs()
         led.alloc(f"{graph.name}/values", dist)

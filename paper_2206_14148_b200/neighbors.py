@@ -53,9 +53,6 @@ def _raise(exc):
     raise exc
 
 
-_COSINE_CHECK_BYTES = 1 << 20
-
-
 def plan(n: int, m: int, d: int, k: int, *, metric: str = "l2", dtype=np.float32,
          out_dtype=None, engine: str = "auto", memory_limit=None,
          resident_bytes: int | None = None, max_chunk_rows: int = 0) -> _lib.KnnPlan:
@@ -74,8 +71,6 @@ def plan(n: int, m: int, d: int, k: int, *, metric: str = "l2", dtype=np.float32
     es = np.dtype(dtype).itemsize
     if resident_bytes is None:
         resident_bytes = (n + m) * d * es
-    if metric == "cosine":
-        resident_bytes += _COSINE_CHECK_BYTES      # the zero-row check's scratch
     p = _lib.KnnPlan()
     lib = _lib.load()
     rc = lib.tb_knn_plan_create_ex(n, m, d, k, _lib.METRICS[metric], _tb_dtype(dtype),
@@ -126,21 +121,18 @@ class KnnOperator:
         torch = _torch()
         return torch.float32 if np.dtype(dt) == np.float32 else torch.float64
 
-    def _check_cosine(self, x, q):
+    def _check_zero_rows(self, st):
         """Cosine distance is undefined for all-zero rows: the reference
-        rejects them with ValueError (frontend.py:126-135).  Row max-norms are
-        taken in chunks whose scratch stays inside the _COSINE_CHECK_BYTES the
-        planner reserves (a whole-matrix abs() would briefly double the
-        input's footprint past memory_limit)."""
+        rejects them with ValueError (frontend.py:126-135).  The operand prep
+        kernels flag such rows while they normalise (no extra pass over the
+        inputs); tb_knn_check reads the flag back, synchronising the stream."""
         if self.metric != "cosine":
             return
-        torch = _torch()
-        for t in (x, q):
-            rows = max(1, _COSINE_CHECK_BYTES // (2 * (t.element_size() + 1)))
-            for s0 in range(0, int(t.shape[0]), rows):
-                nrm = torch.linalg.vector_norm(t[s0:s0 + rows], ord=float("inf"), dim=1)
-                if bool((nrm == 0).any()):
-                    raise ValueError("cosine distance is undefined for zero rows")
+        rc = _lib.load().tb_knn_check(ctypes.byref(self.plan), self.workspace.data_ptr(),
+                                      st.cuda_stream)
+        if rc == _lib.TB_ERR_ARG:
+            raise ValueError(_lib.last_error())
+        _lib.check(rc, "knn_check")
 
     def alloc_outputs(self):
         torch = _torch()
@@ -164,7 +156,6 @@ class KnnOperator:
             if t.data_ptr() % 16:
                 raise EvaluationError(f"{name} must start on a 16-byte boundary "
                                       "(clone() the view)")
-        self._check_cosine(x, q)
         dist, idx = out if out is not None else self.alloc_outputs()
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         ev_arr, n_ev = None, 0
@@ -176,6 +167,7 @@ class KnnOperator:
                                        self.workspace.data_ptr(), self.workspace.numel(),
                                        st.cuda_stream, ev_arr, n_ev)
         _lib.check(rc, "knn")
+        self._check_zero_rows(st)
         return dist, idx
 
     def run_host(self, xh, qh, out_host=None, *, index_base: int = 0, stream=None,
@@ -197,7 +189,6 @@ class KnnOperator:
                                       f"{(int(rows), int(p.d))}")
             if t.dtype != self._torch_dtype(self.dtype):
                 raise EvaluationError(f"{name} dtype {t.dtype} != planned {self.dtype}")
-        self._check_cosine(xh, qh)
         if staging is None:
             if getattr(self, "_staging", None) is None:
                 td = self._torch_dtype(self.dtype)
@@ -217,6 +208,7 @@ class KnnOperator:
                                          idd.data_ptr(), self.workspace.data_ptr(),
                                          self.workspace.numel(), st.cuda_stream)
         _lib.check(rc, "knn_host")
+        self._check_zero_rows(st)
         if synchronize:
             st.synchronize()
         return dh, ih

@@ -448,6 +448,19 @@ def test_metric_engine_rules_and_zero_rows():
         tb.knn(x, q, 3, metric="l1", engine="tc3")
     with pytest.raises(tb.KernelUnavailable):
         tb.knn(x, q, 3, metric="cosine", engine="simt")
+    # zero rows are flagged by the prep kernels (database or query side,
+    # both tensor-core engines, device and host entry points)
+    import torch
+    for engine in ("tc1", "tc3"):
+        for side in ("x", "q"):
+            xz, qz = x.copy(), q.copy()
+            (xz if side == "x" else qz)[3] = 0.0
+            with pytest.raises(ValueError, match="zero rows"):
+                tb.knn(xz, qz, 3, metric="cosine", engine=engine)
+            op = neighbors.KnnOperator(500, 5, 8, 3, metric="cosine", engine=engine)
+            with pytest.raises(ValueError, match="zero rows"):
+                op.run_host(torch.from_numpy(xz), torch.from_numpy(qz))
+            op.run(torch.from_numpy(x).cuda(), torch.from_numpy(q).cuda())   # flag cleared
     x[7] = 0.0
     with pytest.raises(ValueError, match="zero rows"):
         tb.knn(x, q, 3, metric="cosine")
