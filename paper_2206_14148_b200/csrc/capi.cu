@@ -211,7 +211,7 @@ int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int32_t me
     plan->off[kCandI] = c.take(lists * m * cand * 4);
     plan->off[kRunS] = c.take(2 * m * cand * 4);
     plan->off[kRunI] = c.take(2 * m * cand * 4);
-    plan->off[kGThr] = c.take(m * 4 * (1 + (int64_t)cand));   // thresholds + K'-slot pools
+    plan->off[kGThr] = c.take(tc_gthr_words(m, cand) * 4);   // thresholds + insertion pools
     if (tc) {
       // tc1 (fp16 single pass) stages one plane per operand
       const int64_t lo = engine == TB_ENGINE_TC1 ? 0 : 1;
@@ -375,7 +375,7 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
   unsigned* gthr = (unsigned*)at(kGThr);
 
   TB_CUDA_TRY(cudaMemsetAsync(stats, 0, 256, st));
-  if (tc) TB_CUDA_TRY(cudaMemsetAsync(gthr, 0xFF, p->m * 4 * (1 + (int64_t)p->cand), st));
+  if (tc) TB_CUDA_TRY(cudaMemsetAsync(gthr, 0xFF, tc_gthr_words(p->m, p->cand) * 4, st));
   const bool f16 = p->engine == TB_ENGINE_TC1;
   float* qln = f16 ? (float*)at(kQln) : nullptr;
   const float* f16p = f16 ? reinterpret_cast<const float*>(stats + kF16Slot) : nullptr;

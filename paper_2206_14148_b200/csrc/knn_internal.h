@@ -34,6 +34,15 @@ enum KnnSlot {
 // [14] centring flag, [15] max |mu|, [16] cosine zero-row flag; words 64..
 // hold mu (fp64 [d]) for tc1
 constexpr int kF16Slot = 8;
+
+// kGThr region: per-query thresholds (u32[m], padded to 32 words) followed by
+// the per-query insertion pools of the tcgen05 engine (tc_pool_slots(K')
+// hashed slots per query; 2 K' for K' = 16, see knn_tc.cu)
+constexpr int tc_pool_slots(int cand) { return cand == 16 ? 32 : cand; }
+inline int64_t tc_thr_words(int64_t m) { return (m + 31) / 32 * 32; }
+inline int64_t tc_gthr_words(int64_t m, int cand) {
+  return tc_thr_words(m) + m * (int64_t)tc_pool_slots(cand);
+}
 constexpr int kZeroRowWord = 16;
 
 struct KnnDims {

@@ -126,7 +126,7 @@ __device__ __forceinline__ void insert_masked_acc(TopList<float, K>& L, const ui
       L.insert_after(v, base + j);
       // union bound: slot (index mod K') keeps the best score hashed to it;
       // K' finite slots = K' distinct elements at or below their maximum
-      if (pool) atomicMin(pool + ((base + j) & (K - 1)), fkey(v * sc_inv));
+      if (pool) atomicMin(pool + ((base + j) & (tc_pool_slots(K) - 1)), fkey(v * sc_inv));
     }
   }
 }
@@ -163,6 +163,18 @@ struct TcWork {
 // (debug bit 16 enables), read back with tb_debug_tc_trace (tools/tc_trace.py).
 #ifdef TB_TC_TRACE
 __device__ unsigned long long g_tc_trace[148 * 2048];
+// whole-launch timeline (tools/tc_timeline.py): per launch (0 seed, 1 main)
+// and CTA, %globaltimer at entry [0], at every 32nd tile of the MMA issuer
+// [1 + i/32], the issuer's tile count [126] and the CTA's exit [127]
+__device__ unsigned long long g_tc_tl[2 * 148 * 128];
+// insertion census per launch: [0] warp-level insertion-path entries,
+// [1] lanes with a candidate, [2] candidates offered (mask bits)
+__device__ unsigned long long g_tc_cnt[2 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define TB_TR(off, tile, k)                                                   \
   if (trace && (tile) >= tr0 && (tile) < tr0 + 64)                            \
   trace[(off) + ((tile) - tr0) * 8 + (k)] = (unsigned long long)clock64()
@@ -182,6 +194,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               unsigned* __restrict__ pool) {
   using Cfg = TcCfg<PASSES, SQ>;
   constexpr int S = Cfg::kStages;
+#ifdef TB_TC_TRACE
+  const unsigned long long t_entry = gtimer();
+#endif
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* a_base = smem;
@@ -247,6 +262,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   unsigned long long* trace =
       (work.drain_only & 16) && work.list0 == 2 ? g_tc_trace + (size_t)blockIdx.x * 2048 : nullptr;
   const int tr0 = work.drain_only >> 8;
+  unsigned long long* tl =
+      blockIdx.x < 148 ? g_tc_tl + ((work.list0 == 2 ? 148 : 0) + blockIdx.x) * 128 : nullptr;
+  if (tl && threadIdx.x == 0) tl[0] = t_entry;
 #endif
 
   if (warp == 0) {
@@ -407,6 +425,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       for (int t = t0; t < t1; ++t, ++i) {
         const int buf = i & 1;
         if (lane == 0) { TB_TR(0, i, 0); }
+#ifdef TB_TC_TRACE
+        if (tl && lane == 0 && (i & 31) == 0 && i < 32 * 125) tl[1 + (i >> 5)] = gtimer();
+#endif
         mbar_wait(&tempty[buf], ((i >> 1) & 1) ^ 1);
         if (lane == 0) { TB_TR(0, i, 1); }
         const uint32_t d = tmem + buf * kTcN;
@@ -523,6 +544,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         __syncwarp();
       }
     }
+#ifdef TB_TC_TRACE
+    if (tl && lane == 0) tl[126] = (unsigned long long)i;
+#endif
   } else {
     // ---------------------------------------------------------- epilogue
     const int ew = warp - 2;             // 0..7
@@ -541,31 +565,68 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       const int q = qtile_of(u) * kTcM + row;
       const int tb = work.t0 + slice * work.tps, te = min(work.T, tb + work.tps);
       const bool qv = q < m;
-      unsigned* const qpool = pool + (int64_t)(qv ? q : 0) * KC;
-      // per-query pool of K' hashed slots (see insert_masked_acc): its maximum
-      // bounds the K'-th best of everything inserted anywhere.  Read one slot
-      // per tile round-robin; after a full round the running max of the values
-      // read is valid (slots only decrease) and becomes pool_thr.
+      constexpr int kPool = tc_pool_slots(KC);
+      // refresh period, C2 engine ms against the round-robin max of 16 slots
+      // (2.370 same box): 16 -> 2.38, 32 -> 2.33, 64 -> 2.31, 128 -> 2.30;
+      // on another box 128 -> 2.272, 256 -> 2.29, unit start only -> 2.33
+      constexpr int kPoolEvery = 128;
+      unsigned* const qpool = pool + (int64_t)(qv ? q : 0) * kPool;
+      // Per-query pool of hashed slots, each the best score inserted anywhere
+      // with (index mod kPool) = slot (see insert_masked_acc): any K' slot
+      // values are K' distinct elements at or below their maximum, so that
+      // maximum bounds the K'-th best of the union of all lists.
+      //  * K' = 16: 32 slots, read whole (8 x 16 B) at the start of the unit's
+      //    first tile and every kPoolEvery-th (the two column halves half a
+      //    period apart) and reduced at its end to the 16th smallest slot
+      //    (two sorted halves + a half-cleaner): a bound ~2.4x tighter in rank
+      //    than the max of 16 slots, i.e. ~2.4x fewer insertions in the run;
+      //  * otherwise K' slots read round-robin, one per tile; after a full
+      //    round the running max is valid (slots only decrease).
       float p_max = -INFINITY, pool_thr = INFINITY;
       int p_slot = 0;
-      unsigned pk = qv ? __ldcg(qpool) : 0xFFFFFFFFu;
+      unsigned pv[kPool == 2 * KC ? 32 : 1];
+      if (kPool != 2 * KC && qv) {
+        unsigned mx = 0u;
+#pragma unroll
+        for (int p = 0; p < KC; ++p) mx = max(mx, __ldcg(qpool + p));
+        pool_thr = fkey_inv(mx) * sc_mul;
+      }
+      unsigned pk = qv && kPool != 2 * KC ? __ldcg(qpool) : 0xFFFFFFFFu;
       unsigned gk = qv ? __ldcg(gthr + q) : 0u;
       for (int t = tb; t < te; ++t, ++i) {
         const int buf = i & 1;
+        // refresh at the unit's first tile, then every kPoolEvery tiles, the
+        // two column halves (which share SMSPs) half a period apart
+        const int pt = t - tb + (half ? kPoolEvery / 2 : 0);
+        const bool refresh = kPool == 2 * KC && qv && (t == tb || (pt & (kPoolEvery - 1)) == 0);
+        if constexpr (kPool == 2 * KC) {
+          if (refresh) {
+            const uint4* p4 = reinterpret_cast<const uint4*>(qpool);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const uint4 w = __ldcg(p4 + v);
+              pv[4 * v] = w.x;
+              pv[4 * v + 1] = w.y;
+              pv[4 * v + 2] = w.z;
+              pv[4 * v + 3] = w.w;
+            }
+          }
+        } else {
+          p_max = fmaxf(p_max, fkey_inv(pk) * sc_mul);
+          if (++p_slot == KC) {
+            pool_thr = p_max;
+            p_max = -INFINITY;
+            p_slot = 0;
+          }
+        }
         // candidates must also beat the best K'-th score any list has
         // published for this query and the pool bound (both valid for the union)
-        p_max = fmaxf(p_max, fkey_inv(pk) * sc_mul);
-        if (++p_slot == KC) {
-          pool_thr = p_max;
-          p_max = -INFINITY;
-          p_slot = 0;
-        }
         const float thr_g = qv ? fminf(fkey_inv(gk) * sc_mul, pool_thr) : -INFINITY;
         if (qv) {
           // plain (weak, L1-cacheable) loads: both bounds only ever decrease,
           // so a stale copy is a looser but still valid bound (C2 engine
           // 2.369 -> 2.346 ms same-box against ld.global.cg)
-          pk = qpool[p_slot];
+          if (kPool != 2 * KC) pk = qpool[p_slot];
           gk = gthr[q];
         }
         if (ew == 0 && lane == 0) { TB_TR(1024, i, 0); }
@@ -602,6 +663,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
               uint32_t mask = 0;
 #pragma unroll
               for (int j = 0; j < 32; ++j) mask |= (__uint_as_float(r[j]) > nthr ? 1u : 0u) << j;
+#ifdef TB_TC_TRACE
+              {
+                unsigned long long* cn = g_tc_cnt + (work.list0 == 2 ? 4 : 0);
+                const unsigned act = __activemask();
+                if (lane == __ffs(act) - 1) atomicAdd(cn, 1ull);
+                if (mask) atomicAdd(cn + 1, 1ull);
+                atomicAdd(cn + 2, (unsigned long long)__popc(mask));
+              }
+#endif
               insert_masked_acc(L, r, mask, base + (c + h) * 32, thr_g, qpool, sc_inv);
             }
           }
@@ -610,6 +680,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         // and every other CTA on this query tighten their thresholds with it
         if (ew == 0 && lane == 0) { TB_TR(1024, i, 3); }
         if (qv && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst() * sc_inv));
+        if constexpr (kPool == 2 * KC) {
+          if (refresh) pool_thr = fminf(pool_thr, fkey_inv(kth_of_32(pv)) * sc_mul);
+        }
       }
       // unit done: publish this (slice, column half)'s candidates
       if (qv) {
@@ -628,6 +701,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
   if (MC) cluster_sync();           // no multicast or remote arrive targets an exited CTA
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, 512);
+#ifdef TB_TC_TRACE
+  if (tl && threadIdx.x == 0) tl[127] = gtimer();
+#endif
 }
 
 // ------------------------------------------------ CTA-pair variant (tc3) --
@@ -1094,12 +1170,13 @@ static int tc_launch(const CUtensorMap& qh, const CUtensorMap& ql, const CUtenso
     cfg.attrs = at;
     cfg.numAttrs = 1;
     TB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, qh, ql, xh, xl, xext, work, (int)m, nkb, idx_base,
-                                   cs, ci, gthr, f16p, gthr + m));
+                                   cs, ci, gthr, f16p, gthr + tc_thr_words(m)));
   } else {
     if (int rc = set_smem_once((const void*)knn_tc_kernel<PASSES, KC, SQ, F16, false>, (int)smem))
       return rc;
     knn_tc_kernel<PASSES, KC, SQ, F16, false><<<grid, kTcThreads, smem, st>>>(
-        qh, ql, xh, xl, xext, work, (int)m, nkb, idx_base, cs, ci, gthr, f16p, gthr + m);
+        qh, ql, xh, xl, xext, work, (int)m, nkb, idx_base, cs, ci, gthr, f16p,
+        gthr + tc_thr_words(m));
   }
   TB_LAUNCH_CHECK("knn_tc");
   return TB_OK;
@@ -1196,5 +1273,16 @@ int tc_dispatch(int passes, int cand, const CUtensorMap& mqh, const CUtensorMap&
 #ifdef TB_TC_TRACE
 extern "C" __attribute__((visibility("default"))) int tb_debug_tc_trace(void* out) {
   return (int)cudaMemcpyFromSymbol(out, tb::g_tc_trace, sizeof(tb::g_tc_trace));
+}
+extern "C" __attribute__((visibility("default"))) int tb_debug_tc_timeline(void* out) {
+  return (int)cudaMemcpyFromSymbol(out, tb::g_tc_tl, sizeof(tb::g_tc_tl));
+}
+extern "C" __attribute__((visibility("default"))) int tb_debug_tc_census(void* out, int reset) {
+  int rc = (int)cudaMemcpyFromSymbol(out, tb::g_tc_cnt, sizeof(tb::g_tc_cnt));
+  if (reset) {
+    unsigned long long z[8] = {};
+    rc |= (int)cudaMemcpyToSymbol(tb::g_tc_cnt, z, sizeof(z));
+  }
+  return rc;
 }
 #endif

@@ -49,6 +49,38 @@ __device__ __forceinline__ bool lex_less(S a, I ia, S b, I ib) {
   return (a < b) | ((a == b) & (ia < ib));
 }
 
+// 16th smallest of 32 keys: Batcher odd-even merge sort of each half
+// (63 comparators each), then the half-cleaner min(a_i, b_15-i) yields the 16
+// smallest, whose maximum is the answer (~290 integer min/max, registers only)
+template <int N>
+__host__ __device__ __forceinline__ void oem_sort(unsigned* a) {
+#pragma unroll
+  for (int p = 1; p < N; p <<= 1)
+#pragma unroll
+    for (int k = p; k >= 1; k >>= 1)
+#pragma unroll
+      for (int j = k % p; j + k < N; j += 2 * k)
+#pragma unroll
+        for (int i = 0; i < k && i + j + k < N; ++i)
+          if ((i + j) / (2 * p) == (i + j + k) / (2 * p)) {
+            const unsigned lo = a[i + j] < a[i + j + k] ? a[i + j] : a[i + j + k];
+            const unsigned hi = a[i + j] < a[i + j + k] ? a[i + j + k] : a[i + j];
+            a[i + j] = lo;
+            a[i + j + k] = hi;
+          }
+}
+__host__ __device__ __forceinline__ unsigned kth_of_32(unsigned (&v)[32]) {
+  oem_sort<16>(v);
+  oem_sort<16>(v + 16);
+  unsigned b = 0u;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const unsigned m = v[i] < v[31 - i] ? v[i] : v[31 - i];
+    b = b < m ? m : b;
+  }
+  return b;
+}
+
 // Sorted top-K list held in registers (fully unrolled -> no local memory).
 template <typename S, int K, typename I = int>
 struct TopList {
