@@ -595,6 +595,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       unsigned gk = qv ? __ldcg(gthr + q) : 0u;
       for (int t = tb; t < te; ++t, ++i) {
         const int buf = i & 1;
+        if (ew == 0 && lane == 0) { TB_TR(1024, i, 4); }
         // refresh at the unit's first tile, then every kPoolEvery tiles, the
         // two column halves (which share SMSPs) half a period apart
         const int pt = t - tb + (half ? kPoolEvery / 2 : 0);
@@ -683,6 +684,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         if constexpr (kPool == 2 * KC) {
           if (refresh) pool_thr = fminf(pool_thr, fkey_inv(kth_of_32(pv)) * sc_mul);
         }
+        if (ew == 0 && lane == 0) { TB_TR(1024, i, 5); }
       }
       // unit done: publish this (slice, column half)'s candidates
       if (qv) {

@@ -51,6 +51,9 @@ segs = [ee[..., 1] - ee[..., 0], ee[..., 2] - ee[..., 1], ee[..., 3] - ee[..., 2
         epi[:, 9:61, 0] - ee[..., 3]]
 for nm, sg in zip(names, segs):
     print(f"  {nm:18s} median {np.median(sg):7.0f}  mean {np.mean(sg):7.0f}")
+segs = [ee[..., 5] - ee[..., 3], epi[:, 9:61, 4] - ee[..., 5], ee[..., 0] - ee[..., 4]]
+for nm, sg in zip(["publish->end", "end->top(i+1)", "top->ready"], segs):
+    print(f"  {nm:18s} median {np.median(sg):7.0f}  mean {np.mean(sg):7.0f}")
 # latency from the issuer's commit of tile i to the epilogue seeing tfull
 lat = ee[..., 1] - mm[..., 7]
 print(f"  commit(i) -> epilogue sees tfull(i): median {np.median(lat):.0f}")
