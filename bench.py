@@ -189,6 +189,7 @@ def host_cores() -> int:
 
 
 SG_N, SG_D, SG_M = 2_000_000, 11, 10_000
+SG_NTEST = 200_000          # predictive-mean test points (10 % split)
 
 
 def sgpr_cpu_baseline(n_sample: int, threads: int):
@@ -299,9 +300,33 @@ def run_sgpr(args, dev, world, rank, dist):
                         "i8_issued_tops": 9.0 * achieved,
                         "frac_of_nominal": achieved / (4500.0 / 9.0),
                         "useful_flops": useful}}
+    # predictive mean (BASELINE configs[3] "ELBO + predictive mean") at a
+    # 10 % test split, each rank predicting its own shard of test points:
+    # mu(X*) = K(X*, Z) w, the fp64 kernel-MVM kernel at d = 11
+    nt0, nt1 = shard_range(SG_NTEST, rank, world)
+    g.manual_seed(91 + rank)
+    Xs = torch.randn((nt1 - nt0, SG_D), generator=g, device=dev)
+    m.predict_mean(Xs[:1024])
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
+    p0.record()
+    mu = m.predict_mean(Xs)
+    p1.record()
+    torch.cuda.synchronize()
+    pred_ms = p0.elapsed_time(p1)
+    if dist is not None:
+        t = torch.tensor([pred_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        pred_ms = float(t.item())
+    out["predict"] = {"n_test": SG_NTEST, "ms": pred_ms, "points_per_s": SG_NTEST / (pred_ms / 1e3),
+                      "kernel_evals_per_s": SG_NTEST * SG_M / (pred_ms / 1e3),
+                      "finite": bool(torch.isfinite(mu).all().item()),
+                      "kernel": "kernel_mvm_fixed_kernel<float,11,RBF> (fp64 arithmetic)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = sgpr_cpu_baseline(args.sgpr_cpu_n, host_cores())
-    del m, X, y, Z
+    del m, X, y, Z, Xs, mu
     return out
 
 
