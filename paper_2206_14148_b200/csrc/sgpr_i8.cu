@@ -75,7 +75,17 @@ constexpr size_t kI8Smem = 1024 + (size_t)kI8Stages * kI8StageBytes + 512;   // 
 // (no predicated-off dimensions issue).
 constexpr int kI8QuantThreads = 128;
 constexpr int kQRows = 32, kQPts = 128, kQLd = kQPts + 4;
-template <typename T, int DMAX, bool EXACT>
+template <int KERN>
+__device__ __forceinline__ double kern_r2_t(double variance, double r2) {
+  // kern_from_r2 with the kernel type fixed at compile time (same
+  // expressions, same order: identical results)
+  if (KERN == TB_KERNEL_RBF) return variance * exp(-0.5 * r2);
+  const double r = sqrt(fmax(r2, 1e-36));
+  const double s3 = 1.7320508075688772 * r;
+  return variance * (1.0 + s3) * exp(-s3);
+}
+
+template <typename T, int DMAX, bool EXACT, int KERN>
 __global__ void __launch_bounds__(kI8QuantThreads)
 kuf_quant_kernel(const T* __restrict__ X, const T* __restrict__ y, const T* __restrict__ Z,
                  int64_t n0, int64_t cur, int64_t M, int64_t M_pad, int64_t nc, KernParams p,
@@ -107,12 +117,17 @@ kuf_quant_kernel(const T* __restrict__ X, const T* __restrict__ y, const T* __re
     zr[t] = (row_ok && t < dim) ? (double)Z[i * p.dim + t] * p.inv_ls[t] : 0.0;
   __syncthreads();
   const double magic = 6755399441055744.0;            // 1.5 * 2^52
+  const int ncol = (int)(cur - c0 < kQPts ? cur - c0 : kQPts);   // valid points of this block
   double vacc = 0.0;
   // 4 points in flight per thread (independent r^2 / exp chains; per point
   // the r^2 / k expressions and their order are unchanged): 0.49 -> 0.46 ms
   // per C4 chunk.  (Generating the next chunk inside the Gram kernel with its
   // idle epilogue warps was tried: 8 warps per SM cannot hide the fp64
   // latencies, the Gram stretched from 2.45 to 4.7-5.0 ms; reverted.)
+  // Branch-free validity (selects) and the 4 points' digit bytes packed
+  // into one 32-bit shared store per plane (byte permutes): ncu had the
+  // kernel issue-bound (76 % of issue slots) with 110 instructions per
+  // evaluation, a third of them fp64.
   for (int k = 0; k < 32; k += 4) {
     double r2[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -130,22 +145,21 @@ kuf_quant_kernel(const T* __restrict__ X, const T* __restrict__ y, const T* __re
         }
       }
     }
-    double kv[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) kv[u] = kern_from_r2(p, r2[u]);
+    uint32_t q[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int pc = warp * 32 + k + u;
-      uint32_t q = 0;
-      if (row_ok && c0 + pc < cur) {
-        const double qm = fmin(kv[u] * qscale, 16777215.0) + magic;
-        q = (uint32_t)__double2loint(qm);
-        vacc = fma(qm - magic, ys[pc], vacc);           // exact q * y products
-      }
-      qb[0][lane][pc] = (uint8_t)(q & 255u);
-      qb[1][lane][pc] = (uint8_t)((q >> 8) & 255u);
-      qb[2][lane][pc] = (uint8_t)(q >> 16);
+      const bool ok = row_ok && pc < ncol;
+      const double qm = fmin(kern_r2_t<KERN>(p.variance, r2[u]) * qscale, 16777215.0) + magic;
+      q[u] = ok ? (uint32_t)__double2loint(qm) : 0u;
+      vacc = fma(ok ? qm - magic : 0.0, ys[pc], vacc);   // exact q * y products
     }
+    const uint32_t t01 = __byte_perm(q[0], q[1], 0x5140), t23 = __byte_perm(q[2], q[3], 0x5140);
+    const uint32_t u01 = __byte_perm(q[0], q[1], 0x0062), u23 = __byte_perm(q[2], q[3], 0x0062);
+    const int pc0 = warp * 32 + k;
+    *reinterpret_cast<uint32_t*>(&qb[0][lane][pc0]) = __byte_perm(t01, t23, 0x5410);
+    *reinterpret_cast<uint32_t*>(&qb[1][lane][pc0]) = __byte_perm(t01, t23, 0x7632);
+    *reinterpret_cast<uint32_t*>(&qb[2][lane][pc0]) = __byte_perm(u01, u23, 0x5410);
   }
   vred[warp][lane] = vacc;
   __syncthreads();
@@ -719,16 +733,21 @@ int i8_gen_chunk(const void* X, const void* y, const void* Z, int dtype, int64_t
   const int64_t ncur = round_up(cur, 128);           // columns written this chunk
   const double qscale = std::ldexp(1.0, kI8FracBits) / kp.variance;
   dim3 g((unsigned)(ncur / 128), (unsigned)(M_pad / 32));
-#define TB_KQ(T, D, EX)                                                                    \
+#define TB_KQK(T, D, EX, KK)                                                               \
   do {                                                                                     \
     const int xs_bytes = kQPts * ((D + 1) & ~1) * 8;                                       \
     if (xs_bytes > 32768)                                                                  \
-      TB_CUDA_TRY(cudaFuncSetAttribute(kuf_quant_kernel<T, D, EX>,                         \
+      TB_CUDA_TRY(cudaFuncSetAttribute(kuf_quant_kernel<T, D, EX, KK>,                     \
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                        xs_bytes));                                         \
-    kuf_quant_kernel<T, D, EX><<<g, kI8QuantThreads, xs_bytes, st>>>(                      \
+    kuf_quant_kernel<T, D, EX, KK><<<g, kI8QuantThreads, xs_bytes, st>>>(                  \
         (const T*)X, (const T*)y, (const T*)Z, n0, cur, M, M_pad, nc, kp, qscale, planes,  \
         vpart);                                                                            \
+  } while (0)
+#define TB_KQ(T, D, EX)                                                                    \
+  do {                                                                                     \
+    if (kp.kernel == TB_KERNEL_RBF) TB_KQK(T, D, EX, TB_KERNEL_RBF);                       \
+    else TB_KQK(T, D, EX, TB_KERNEL_MATERN32);                                             \
   } while (0)
 #define TB_KQ_DIM(T)                                                      \
   switch (kp.dim) {                                                       \
@@ -749,6 +768,7 @@ int i8_gen_chunk(const void* X, const void* y, const void* Z, int dtype, int64_t
   }
 #undef TB_KQ_DIM
 #undef TB_KQ
+#undef TB_KQK
   TB_LAUNCH_CHECK("kuf_quant");
   v_reduce_kernel<<<(unsigned)ceil_div(M, 256), 256, 0, st>>>(
       vpart, (int)(ncur / 128), M, M_pad, kp.variance * std::ldexp(1.0, -kI8FracBits), v);
