@@ -182,6 +182,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TB_TR(off, tile, k)
 #endif
 
+// The A/B timing modes (TcWork::drain_only, from TB_TC_DEBUG) exist only in
+// the study build (make trace: -DTB_TC_TRACE); in the product library the
+// bits are compile-time zero, so none of their branches sit in the tcgen05
+// loops (ncu had counted ~16 instructions per tile per epilogue warp on the
+// constant loads and tests of the debug word).
+#ifdef TB_TC_TRACE
+#define TB_DBG(w) ((w).drain_only)
+#else
+#define TB_DBG(w) 0
+#endif
+
 template <int PASSES, int KC, bool SQ, bool F16, bool MC>
 __global__ void __launch_bounds__(kTcThreads, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
@@ -279,7 +290,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       }
     }
     __syncwarp();
-    const bool loads_on = !(work.drain_only & 2);
+    const bool loads_on = !(TB_DBG(work) & 2);
     int s = 0, i = 0;
     uint32_t ph = 0, seg = 0;
     for (int u = grp; u < units; u += ngrp, ++seg) {
@@ -412,7 +423,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
     const uint64_t dext_b = desc_k_inter(smem_u32(bext), 128, 256);
     const uint64_t da = desc_k_sw128(smem_u32(a_base));
     const uint64_t db = desc_k_sw128(smem_u32(b_base));
-    const bool mma_on = !(work.drain_only & 4);
+    const bool mma_on = !(TB_DBG(work) & 4);
     int s = 0, i = 0;
     uint32_t ph = 0, seg = 0;
     for (int u = grp; u < units; u += ngrp, ++seg) {
@@ -650,7 +661,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             mbar_arrive(&tempty[buf]);
             if (ew == 0 && lane == 0) { TB_TR(1024, i, 2); }
           }
-          if (work.drain_only & 1) continue;
+          if (TB_DBG(work) & 1) continue;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint32_t(&r)[32] = h ? rb : ra;
@@ -659,7 +670,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             // compact loop so the hot path fits the I-cache
             const float thr = fminf(L.worst(), thr_g);
             const float hi = max_of_32(r);
-            if (-hi < thr && !(work.drain_only & 8)) {
+            if (-hi < thr && !(TB_DBG(work) & 8)) {
               const float nthr = -thr;                   // score < thr <=> acc > -thr
               uint32_t mask = 0;
 #pragma unroll
@@ -823,7 +834,7 @@ knn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_qhi,
 #pragma unroll
             for (int mat = 0; mat < 2; ++mat) {
               mbar_wait(&empty[s], ph ^ 1);
-              if (work.drain_only & 2) {
+              if (TB_DBG(work) & 2) {
                 if (rank == 0) mbar_arrive(&full[s]);
               } else {
                 if (rank == 0) mbar_expect_tx(&full[s], 2 * kPrHalf);
@@ -869,7 +880,7 @@ knn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_qhi,
 #pragma unroll
             for (int kk = 0; kk < kTcKB / 16; ++kk) {
               const uint32_t ko = kk * 32;
-              if (work.drain_only & 4) continue;
+              if (TB_DBG(work) & 4) continue;
               mma_bf16_2sm(d, desc_k_sw128(ahi + ko), desc_k_sw128(b0 + ko), idesc, 1);
               mma_bf16_2sm(d, desc_k_sw128(alo + ko), desc_k_sw128(b0 + ko), idesc, 1);
             }
@@ -883,7 +894,7 @@ knn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_qhi,
             b0 = smem_u32(b_base + (size_t)s * kPrHalf);
 #pragma unroll
             for (int kk = 0; kk < kTcKB / 16; ++kk)
-              if (!(work.drain_only & 4)) mma_bf16_2sm(d, desc_k_sw128(ahi + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, 1);
+              if (!(TB_DBG(work) & 4)) mma_bf16_2sm(d, desc_k_sw128(ahi + kk * 32), desc_k_sw128(b0 + kk * 32), idesc, 1);
             mma_commit_2sm(&empty[s], 3);
             if (++s == S) {
               s = 0;
@@ -936,13 +947,13 @@ knn_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           tmem_ld32(taddr + c * 32, ra);
           tmem_ld32(taddr + (c + 1) * 32, rb);
           tmem_ld_wait();
-          if (work.drain_only & 1) continue;
+          if (TB_DBG(work) & 1) continue;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint32_t(&r)[32] = h ? rb : ra;
             const float thr = fminf(L.worst(), thr_g);
             const float hi = max_of_32(r);
-            if (-hi < thr && !(work.drain_only & 8)) {
+            if (-hi < thr && !(TB_DBG(work) & 8)) {
               const float nthr = -thr;                   // score < thr <=> acc > -thr
               uint32_t mask = 0;
 #pragma unroll

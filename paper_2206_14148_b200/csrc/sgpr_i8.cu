@@ -221,6 +221,15 @@ __device__ __forceinline__ void tile_of_unit(int u, int nt, int& ta, int& tb) {
   ta = tb = 0;
 }
 
+// A/B timing modes (TB_I8_DEBUG) only in a study build (-DTB_I8_STUDY): in
+// the product library they are compile-time zero and leave no branches in
+// the tcgen05 loops.
+#ifdef TB_I8_STUDY
+#define TB_I8_DBG(x) (x)
+#else
+#define TB_I8_DBG(x) 0
+#endif
+
 __global__ void __launch_bounds__(kI8Threads, 1)
 sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, int m_pad,
                     double scale, double* __restrict__ sig, int dbg) {
@@ -276,7 +285,7 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
         for (int kb = 0; kb < nkb; kb += step) {
           mbar_wait(&empty[s], ph ^ 1);
           if (elect_one_sync()) {
-            if (dbg == 1) {
+            if (TB_I8_DBG(dbg) == 1) {
               mbar_arrive(&full[s]);
             } else {
               uint8_t* st = smem + (size_t)s * kI8StageBytes;
@@ -332,7 +341,7 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
         const uint64_t a1 = a2 + 2 * kTileD, b1 = a2 + 3 * kTileD;
         const uint64_t a0 = a2 + 4 * kTileD, b0 = a2 + 5 * kTileD;
         if (elect_one_sync()) {
-          if (dbg != 2) {
+          if (TB_I8_DBG(dbg) != 2) {
             const uint32_t acc = kb ? 1u : 0u;
             mma_i8(acc0, a2, b2, idesc, acc);
             mma_i8(acc1, a2, b1, idesc, acc);
@@ -369,7 +378,7 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
         const uint64_t a = d0 + (uint64_t)s * kStageD;
         const int nk = min(3, nkb - kb);
         if (elect_one_sync()) {
-          if (dbg != 2) {
+          if (TB_I8_DBG(dbg) != 2) {
             for (int j = 0; j < nk; ++j) {
               const uint64_t aj = a + 2 * j * kTileD, bj = aj + kTileD;
               mma_i8(acc0, aj, bj, idesc, (kb | j) ? 1u : 0u);
@@ -540,7 +549,7 @@ sgpr_gram_i8_pair_kernel(const __grid_constant__ CUtensorMap tma, const __grid_c
             const uint32_t fb = mapa_shared(&full[s], 0);     // the leader's barrier
             uint8_t* st = smem + (size_t)s * kP2Stage;
             const int nk = phase ? min(3, nkb - kb) : 1;
-            if (dbg == 1) {
+            if (TB_I8_DBG(dbg) == 1) {
               if (rank == 0) mbar_arrive(&full[s]);
             } else {
             // the leader arms its own barrier for both CTAs' bytes
@@ -587,7 +596,7 @@ sgpr_gram_i8_pair_kernel(const __grid_constant__ CUtensorMap tma, const __grid_c
           const uint64_t a1 = a2 + kPairD, b1 = a1 + kAD;
           const uint64_t a0 = a1 + kPairD, b0 = a0 + kAD;
           const uint32_t acc = kb ? 1u : 0u;
-          if (dbg != 2) {
+          if (TB_I8_DBG(dbg) != 2) {
           mma_i8_2sm(acc0, a2, b2, idesc, acc);
           mma_i8_2sm(acc1, a2, b1, idesc, acc);
           mma_i8_2sm(acc1, a1, b2, idesc, 1);
@@ -619,7 +628,7 @@ sgpr_gram_i8_pair_kernel(const __grid_constant__ CUtensorMap tma, const __grid_c
           tc_fence_after();
           const uint64_t a = d0 + (uint64_t)s * kStageD;
           const int nk = min(3, nkb - kb);
-          for (int j = 0; j < nk && dbg != 2; ++j) {
+          for (int j = 0; j < nk && TB_I8_DBG(dbg) != 2; ++j) {
             const uint64_t aj = a + j * kPairD, bj = aj + kAD;
             mma_i8_2sm(acc0, aj, bj, idesc, (kb | j) ? 1u : 0u);
             mma_i8_2sm(acc0, aj + 2, bj + 2, idesc, 1);

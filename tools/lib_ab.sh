@@ -1,6 +1,7 @@
 #!/bin/bash
 # Same-box A/B of two library builds (old = libtb_pairwise_old.so) on the
-# C2 tc1 engine, alternating, for each TB_TC_DEBUG mode given (default 0).
+# C2 tc1 engine, alternating, for each TB_TC_DEBUG mode given (default 0;
+# modes other than 0 act only in study builds: make trace, -DTB_TC_TRACE).
 modes="${@:-0}"
 for rep in 1 2 3; do
   for mode in $modes; do
