@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, int m_pad,
                     double scale, double* __restrict__ sig, int dbg) {
   // dbg (TB_I8_DEBUG, A/B timing only): 1 = producer skips the TMA loads
-  // (MMA-issue bound), 2 = issuer skips the MMAs (TMA-feed bound);
+  // (MMA-issue bound), 2 = issuer skips the MMAs (TMA-feed bound), 3 = no
+  // phase B (level 0);
   // results are garbage in both modes
   const int nt = m_pad / kI8Tile;
   constexpr int S = kI8Stages;
@@ -280,7 +281,7 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
       int ta, tb;
       tile_of_unit(u, nt, ta, tb);
       const int ra = ta * kI8Tile, rb = tb * kI8Tile;
-      for (int phase = 0; phase < 2; ++phase) {
+      for (int phase = 0; phase < (TB_I8_DBG(dbg) == 3 ? 1 : 2); ++phase) {
         const int step = phase ? 3 : 1;
         for (int kb = 0; kb < nkb; kb += step) {
           mbar_wait(&empty[s], ph ^ 1);
@@ -372,7 +373,7 @@ sgpr_gram_i8_kernel(const __grid_constant__ CUtensorMap tm, int units, int nkb, 
       __syncwarp();
       mbar_wait(acc0_free, i & 1);
       tc_fence_after();
-      for (int kb = 0; kb < nkb; kb += 3) {
+      for (int kb = 0; kb < (TB_I8_DBG(dbg) == 3 ? 0 : nkb); kb += 3) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint64_t a = d0 + (uint64_t)s * kStageD;
