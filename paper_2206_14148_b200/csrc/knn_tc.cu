@@ -577,6 +577,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       const int tb = work.t0 + slice * work.tps, te = min(work.T, tb + work.tps);
       const bool qv = q < m;
       constexpr int kPool = tc_pool_slots(KC);
+      constexpr bool kSel = kPool == 32 && KC <= 16;   // K'-th smallest of 32 slots
       // refresh period, C2 engine ms against the round-robin max of 16 slots
       // (2.370 same box): 16 -> 2.38, 32 -> 2.33, 64 -> 2.31, 128 -> 2.30;
       // on another box 128 -> 2.272, 256 -> 2.29, unit start only -> 2.33
@@ -586,23 +587,23 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       // with (index mod kPool) = slot (see insert_masked_acc): any K' slot
       // values are K' distinct elements at or below their maximum, so that
       // maximum bounds the K'-th best of the union of all lists.
-      //  * K' = 16: 32 slots, read whole (8 x 16 B) at the start of the unit's
+      //  * K' <= 16: 32 slots, read whole (8 x 16 B) at the start of the unit's
       //    first tile and every kPoolEvery-th (the two column halves half a
-      //    period apart) and reduced at its end to the 16th smallest slot
+      //    period apart) and reduced at its end to the K'-th smallest slot
       //    (two sorted halves + a half-cleaner): a bound ~2.4x tighter in rank
       //    than the max of 16 slots, i.e. ~2.4x fewer insertions in the run;
       //  * otherwise K' slots read round-robin, one per tile; after a full
       //    round the running max is valid (slots only decrease).
       float p_max = -INFINITY, pool_thr = INFINITY;
       int p_slot = 0;
-      unsigned pv[kPool == 2 * KC ? 32 : 1];
-      if (kPool != 2 * KC && qv) {
+      unsigned pv[kSel ? 32 : 1];
+      if (!kSel && qv) {
         unsigned mx = 0u;
 #pragma unroll
         for (int p = 0; p < KC; ++p) mx = max(mx, __ldcg(qpool + p));
         pool_thr = fkey_inv(mx) * sc_mul;
       }
-      unsigned pk = qv && kPool != 2 * KC ? __ldcg(qpool) : 0xFFFFFFFFu;
+      unsigned pk = qv && !kSel ? __ldcg(qpool) : 0xFFFFFFFFu;
       unsigned gk = qv ? __ldcg(gthr + q) : 0u;
       for (int t = tb; t < te; ++t, ++i) {
         const int buf = i & 1;
@@ -610,8 +611,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         // refresh at the unit's first tile, then every kPoolEvery tiles, the
         // two column halves (which share SMSPs) half a period apart
         const int pt = t - tb + (half ? kPoolEvery / 2 : 0);
-        const bool refresh = kPool == 2 * KC && qv && (t == tb || (pt & (kPoolEvery - 1)) == 0);
-        if constexpr (kPool == 2 * KC) {
+        const bool refresh = kSel && qv && (t == tb || (pt & (kPoolEvery - 1)) == 0);
+        if constexpr (kSel) {
           if (refresh) {
             const uint4* p4 = reinterpret_cast<const uint4*>(qpool);
 #pragma unroll
@@ -638,7 +639,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           // plain (weak, L1-cacheable) loads: both bounds only ever decrease,
           // so a stale copy is a looser but still valid bound (C2 engine
           // 2.369 -> 2.346 ms same-box against ld.global.cg)
-          if (kPool != 2 * KC) pk = qpool[p_slot];
+          if (!kSel) pk = qpool[p_slot];
           gk = gthr[q];
         }
         if (ew == 0 && lane == 0) { TB_TR(1024, i, 0); }
@@ -692,8 +693,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         // and every other CTA on this query tighten their thresholds with it
         if (ew == 0 && lane == 0) { TB_TR(1024, i, 3); }
         if (qv && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst() * sc_inv));
-        if constexpr (kPool == 2 * KC) {
-          if (refresh) pool_thr = fminf(pool_thr, fkey_inv(kth_of_32(pv)) * sc_mul);
+        if constexpr (kSel) {
+          if (refresh) pool_thr = fminf(pool_thr, fkey_inv(kth_of_32<KC>(pv)) * sc_mul);
         }
         if (ew == 0 && lane == 0) { TB_TR(1024, i, 5); }
       }

@@ -49,9 +49,9 @@ __device__ __forceinline__ bool lex_less(S a, I ia, S b, I ib) {
   return (a < b) | ((a == b) & (ia < ib));
 }
 
-// 16th smallest of 32 keys: Batcher odd-even merge sort of each half
-// (63 comparators each), then the half-cleaner min(a_i, b_15-i) yields the 16
-// smallest, whose maximum is the answer (~290 integer min/max, registers only)
+// K-th smallest (K <= 16) of 32 keys: Batcher odd-even merge sort of each
+// half (63 comparators each), then min over i of max(a[i-1], b[K-1-i]) for
+// the two sorted halves a, b (~290 integer min/max, registers only)
 template <int N>
 __host__ __device__ __forceinline__ void oem_sort(unsigned* a) {
 #pragma unroll
@@ -69,16 +69,18 @@ __host__ __device__ __forceinline__ void oem_sort(unsigned* a) {
             a[i + j + k] = hi;
           }
 }
+template <int K>
 __host__ __device__ __forceinline__ unsigned kth_of_32(unsigned (&v)[32]) {
+  static_assert(K >= 1 && K <= 16, "kth_of_32: K in [1, 16]");
   oem_sort<16>(v);
   oem_sort<16>(v + 16);
-  unsigned b = 0u;
+  unsigned best = v[16 + K - 1] < v[K - 1] ? v[16 + K - 1] : v[K - 1];   // i = 0 and i = K
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const unsigned m = v[i] < v[31 - i] ? v[i] : v[31 - i];
-    b = b < m ? m : b;
+  for (int i = 1; i < K; ++i) {
+    const unsigned m = v[i - 1] < v[16 + K - 1 - i] ? v[16 + K - 1 - i] : v[i - 1];
+    best = m < best ? m : best;
   }
-  return b;
+  return best;
 }
 
 // Sorted top-K list held in registers (fully unrolled -> no local memory).

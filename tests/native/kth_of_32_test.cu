@@ -1,5 +1,5 @@
 // Host check of the pool-bound selection network (tb_common.cuh kth_of_32):
-// the 16th smallest of 32 keys, against std::nth_element, on random,
+// the 16th and 12th smallest of 32 keys, against std::nth_element, on random,
 // duplicate-heavy and all-unset (0xFFFFFFFF) inputs.  Built and run by
 // tests/test_native_helpers.py with nvcc (host code only, no GPU needed).
 #include <algorithm>
@@ -24,10 +24,18 @@ int main() {
       if (mode == 3) x = 0xFFFFFFFFu;
       v[i] = w[i] = x;
     }
+    unsigned v2[32];
+    for (int i = 0; i < 32; ++i) v2[i] = v[i];
     std::nth_element(w, w + 15, w + 32);
-    const unsigned got = tb::kth_of_32(v);
+    const unsigned got = tb::kth_of_32<16>(v);
     if (got != w[15]) {
-      std::printf("FAIL trial %d: got %u want %u\n", trial, got, w[15]);
+      std::printf("FAIL K=16 trial %d: got %u want %u\n", trial, got, w[15]);
+      return 1;
+    }
+    std::nth_element(w, w + 11, w + 32);
+    const unsigned got12 = tb::kth_of_32<12>(v2);
+    if (got12 != w[11]) {
+      std::printf("FAIL K=12 trial %d: got %u want %u\n", trial, got12, w[11]);
       return 1;
     }
   }

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 @pytest.mark.skipif(shutil.which("nvcc") is None, reason="nvcc not on PATH")
 def test_kth_of_32_selection_network(tmp_path):
-    """The tc1 epilogue's pool bound (16th smallest of 32 slot keys) must
+    """The tc1 epilogue's pool bound (K'-th smallest of 32 slot keys) must
     never be below the true order statistic: a smaller bound would filter a
     true neighbour before any list saw it, which the re-rank cannot detect."""
     exe = tmp_path / "kth"
