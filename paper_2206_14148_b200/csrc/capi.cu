@@ -205,7 +205,7 @@ int tb_knn_plan_create_ex(int64_t n, int64_t m, int64_t d, int64_t k, int32_t me
     plan->off[kQnorm] = c.take(m * 4);
     // counters | tc1 centring mean [d] + per-block partials [64][d + 1]
     plan->off[kStats] = c.take(256 + 8 * (plan->d_pad + 64 * (plan->d_pad + 1)));
-    plan->off[kFbList] = c.take(m * 4);
+    plan->off[kFbList] = c.take(fb_region_bytes(m));
     plan->off[kXn] = c.take(chunk_pad * 4);
     plan->off[kCandS] = c.take(lists * m * cand * 4);
     plan->off[kCandI] = c.take(lists * m * cand * 4);

@@ -31,9 +31,19 @@ enum KnnSlot {
 // bits, [3] max |q| bits, [4] max |x| bits of the current chunk, [5] the
 // chunk's max ||x - fp16 x||, [kF16Slot..+3] fp16 engine scales (floats:
 // s, t, alpha, 1/(s t)), [12] redo flag of the chunk conversion, [13] max 1/t,
-// [14] centring flag, [15] max |mu|, [16] cosine zero-row flag; words 64..
+// [14] centring flag, [15] max |mu|, [16] cosine zero-row flag, [17] count
+// of queries the fallback's hit-buffer path hands on; words 64..
 // hold mu (fp64 [d]) for tc1
 constexpr int kF16Slot = 8;
+constexpr int kFbOverWord = 17;      // count of fallback queries the hit-buffer path hands on
+
+// kFbList region: int fb_list[m] (uncertified query rows), then (8-byte
+// aligned) double bounds[m]: the exact k-th candidate distance of each, an
+// upper bound on its true k-th distance (the fallback scans below it)
+inline int64_t fb_region_bytes(int64_t m) { return ((m * 4 + 7) & ~(int64_t)7) + m * 8; }
+__host__ __device__ __forceinline__ double* fb_bounds(int* fb, int64_t m) {
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(fb) + ((m * 4 + 7) & ~(int64_t)7));
+}
 
 // kGThr region: per-query thresholds (u32[m], padded to 32 words) followed by
 // the per-query insertion pools of the tcgen05 engine (tc_pool_slots(K')

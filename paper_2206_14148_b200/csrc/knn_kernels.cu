@@ -1127,6 +1127,7 @@ __global__ void knn_refine_kernel(const float* __restrict__ cs,
       if (!ok) {
         const int pos = atomicAdd(reinterpret_cast<int*>(&stats[1]), 1);
         fb_list[pos] = (int)r;
+        fb_bounds(fb_list, m)[pos] = kth;     // the true k-th distance is <= kth
       }
     }
   }
@@ -1202,7 +1203,7 @@ knn_fallback_partial_kernel(const T* __restrict__ x, const T* __restrict__ q, in
                             int* __restrict__ sc_i) {
   __shared__ double sd[8][KC];
   __shared__ int si[8][KC];
-  const int count = *reinterpret_cast<const volatile int*>(&stats[1]);
+  const int count = *reinterpret_cast<const volatile int*>(stats);
   if (count == 0) return;
   const int S = max(1, (int)gridDim.x / count);
   const int units = count * S;
@@ -1253,7 +1254,7 @@ knn_fallback_rows_kernel(const T* __restrict__ x, const T* __restrict__ q, int64
   __shared__ double qq_s;
   __shared__ double sd[8][KC];
   __shared__ int si[8][KC];
-  const int count = *reinterpret_cast<const volatile int*>(&stats[1]);
+  const int count = *reinterpret_cast<const volatile int*>(stats);
   if (count == 0) return;
   const int S = max(1, (int)gridDim.x / count);
   const int units = count * S;
@@ -1330,7 +1331,7 @@ __global__ void knn_fallback_merge_kernel(const unsigned* __restrict__ stats,
                                           const int* __restrict__ sc_i,
                                           OT* __restrict__ out_dist,
                                           int64_t* __restrict__ out_idx, int64_t index_base) {
-  const int count = *reinterpret_cast<const volatile int*>(&stats[1]);
+  const int count = *reinterpret_cast<const volatile int*>(stats);
   const int S = count ? max(1, G / count) : 1;
   const int lane = threadIdx.x & 31;
   for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < count;
@@ -1349,6 +1350,131 @@ __global__ void knn_fallback_merge_kernel(const unsigned* __restrict__ stats,
   }
 }
 
+// Bounded fallback (the first, fast stage).  The re-rank already holds, for
+// every uncertified query, the exact distance of its k-th candidate: an
+// upper bound on its true k-th distance.  Blocks take QB such queries (in
+// shared memory, fp64) against a slice of the database, one database row
+// per thread: each row is read once for the QB queries, QB fp64 distances
+// in registers (the re-rank's formulas, summed serially), and a row at or
+// below a query's bound is appended to that query's hit buffer - usually
+// just its k true neighbours, so no per-row top-K' work.  (The warp-per-row
+// brute force below took 0.33 ms per query at 1e6 x 128.)
+constexpr int kFbQB = 8;
+template <typename T, int MET>
+__global__ void __launch_bounds__(256)
+knn_fallback_tile_kernel(const T* __restrict__ x, const T* __restrict__ q, int64_t n,
+                         int64_t d, const unsigned* __restrict__ cntp,
+                         const int* __restrict__ fb_list, const double* __restrict__ fb_bnd,
+                         int* __restrict__ hit_cnt, double* __restrict__ hit_d,
+                         int* __restrict__ hit_i, int hcap) {
+  extern __shared__ __align__(16) double fq[];      // [kFbQB][d]
+  __shared__ double bnd[kFbQB], qq[kFbQB];
+  const int count = *reinterpret_cast<const volatile int*>(cntp);
+  if (count == 0) return;
+  const int groups = (count + kFbQB - 1) / kFbQB;
+  const int S = max(1, (int)gridDim.x / groups);
+  for (int u = blockIdx.x; u < groups * S; u += gridDim.x) {
+    const int g = u % groups, slice = u / groups;   // concurrent blocks share a slice (L2)
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < kFbQB * d; e += blockDim.x) {
+      const int qi = (int)(e / d);
+      const int p = g * kFbQB + qi;
+      fq[e] = p < count ? (double)q[(int64_t)fb_list[p] * d + (e - (int64_t)qi * d)] : 0.0;
+    }
+    if (threadIdx.x < kFbQB) {
+      const int p = g * kFbQB + threadIdx.x;
+      // slack for the summation order (<= 2 d 2^-53 relative for sums of
+      // non-negative terms; an absolute 1e-12 for the cosine's 1 - c)
+      const double b = p < count ? fb_bnd[p] : -INFINITY;
+      bnd[threadIdx.x] = b + 1e-12 * fabs(b) + (MET == TB_METRIC_COSINE ? 1e-12 : 0.0);
+    }
+    __syncthreads();
+    if (MET == TB_METRIC_COSINE && threadIdx.x < kFbQB) {
+      double a = 0.0;
+      for (int64_t c = 0; c < d; ++c) a = fma(fq[threadIdx.x * d + c], fq[threadIdx.x * d + c], a);
+      qq[threadIdx.x] = a;
+    }
+    __syncthreads();
+    const int64_t j0 = n * slice / S, j1 = n * (slice + 1) / S;
+    for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+      const T* xr = x + j * d;
+      double acc[kFbQB], xx = 0.0;
+#pragma unroll
+      for (int qi = 0; qi < kFbQB; ++qi) acc[qi] = 0.0;
+      auto term = [&](int64_t c, double b) {
+        if (MET == TB_METRIC_COSINE) xx = fma(b, b, xx);
+#pragma unroll
+        for (int qi = 0; qi < kFbQB; ++qi) {
+          const double a = fq[qi * d + c];
+          if (MET == TB_METRIC_COSINE) {
+            acc[qi] = fma(a, b, acc[qi]);
+          } else {
+            const double df = a - b;
+            acc[qi] = MET == TB_METRIC_L1 ? acc[qi] + fabs(df) : fma(df, df, acc[qi]);
+          }
+        }
+      };
+      if (sizeof(T) == 4 && (d & 3) == 0) {
+        for (int64_t c = 0; c < d; c += 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(xr + c));
+          term(c, v.x);
+          term(c + 1, v.y);
+          term(c + 2, v.z);
+          term(c + 3, v.w);
+        }
+      } else {
+        for (int64_t c = 0; c < d; ++c) term(c, (double)xr[c]);
+      }
+#pragma unroll
+      for (int qi = 0; qi < kFbQB; ++qi) {
+        const double dist =
+            MET == TB_METRIC_COSINE ? 1.0 - acc[qi] / (sqrt(qq[qi]) * sqrt(xx)) : acc[qi];
+        if (dist <= bnd[qi]) {
+          const int p = g * kFbQB + qi;
+          const int pos = atomicAdd(hit_cnt + p, 1);
+          if (pos < hcap) {
+            hit_d[(int64_t)p * hcap + pos] = dist;
+            hit_i[(int64_t)p * hcap + pos] = (int)j;
+          }
+        }
+      }
+    }
+  }
+}
+
+// The k best hits of each query (ties -> lower index); a query whose hits
+// overflowed the buffer (many rows tied at its bound) or came short goes on
+// to the exhaustive kernels through the overflow list.
+template <typename OT, int KC>
+__global__ void knn_fallback_hits_kernel(const unsigned* __restrict__ cntp,
+                                         const int* __restrict__ fb_list,
+                                         const int* __restrict__ hit_cnt,
+                                         const double* __restrict__ hit_d,
+                                         const int* __restrict__ hit_i, int hcap, int k,
+                                         unsigned* __restrict__ over_cnt,
+                                         int* __restrict__ over_list,
+                                         OT* __restrict__ out_dist,
+                                         int64_t* __restrict__ out_idx, int64_t index_base) {
+  const int count = *reinterpret_cast<const volatile int*>(cntp);
+  const int lane = threadIdx.x & 31;
+  for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < count;
+       p += gridDim.x * (blockDim.x >> 5)) {
+    const int64_t r = fb_list[p];
+    const int h = hit_cnt[p];
+    if (h > hcap || h < k) {
+      if (lane == 0) over_list[atomicAdd(reinterpret_cast<int*>(over_cnt), 1)] = (int)r;
+      continue;
+    }
+    TopList<double, KC> M;
+    M.init();
+    for (int t = lane; t < h; t += 32) M.offer(hit_d[(int64_t)p * hcap + t], hit_i[(int64_t)p * hcap + t]);
+    warp_drain(M, k, [&](int t, double v, int j) {
+      out_dist[r * k + t] = (OT)v;
+      out_idx[r * k + t] = (int64_t)j + index_base;
+    });
+  }
+}
+
 template <typename T, typename OT, int KC, int MET>
 static int fallback_launch(const void* x, const void* q, int64_t n, int64_t d, int64_t k,
                            const unsigned* stats, const int* fb, void* scratch,
@@ -1360,18 +1486,46 @@ static int fallback_launch(const void* x, const void* q, int64_t n, int64_t d, i
   // scratch holds max(G, count) lists of KC (double, int); count <= m
   const int64_t cap = scratch_bytes / (12 * KC);
   if (cap < m) return fail(TB_ERR_ARG, "fallback scratch too small");
+  const unsigned* list_cnt = stats + 1;
+  const int* list = fb;
+  // stage 1: bounded scan into per-query hit buffers (scratch: hit counts,
+  // then hcap (distance, row) slots per query); what it cannot settle goes
+  // on through stats[kFbOverWord] and the overflow list (the bounds' space,
+  // dead once the scan has run)
+  const int64_t hcap = std::min<int64_t>(64, (scratch_bytes / std::max<int64_t>(m, 1) - 8) / 12);
+  const size_t fq_bytes = (size_t)kFbQB * d * 8;
+  if (hcap >= k + 4 && fq_bytes <= 48 * 1024) {
+    int* hit_cnt = (int*)scratch;
+    double* hit_d = (double*)((char*)scratch + ((m * 4 + 7) & ~(int64_t)7));
+    int* hit_i = (int*)(hit_d + m * hcap);
+    TB_CUDA_TRY(cudaMemsetAsync(hit_cnt, 0, m * 4, st));
+    knn_fallback_tile_kernel<T, MET><<<4 * sms, 256, fq_bytes, st>>>(
+        (const T*)x, (const T*)q, n, d, list_cnt, fb, fb_bounds(const_cast<int*>(fb), m), hit_cnt,
+        hit_d, hit_i, (int)hcap);
+    TB_LAUNCH_CHECK("knn_fallback_tile");
+    unsigned* over_cnt = const_cast<unsigned*>(stats) + kFbOverWord;
+    int* over_list = reinterpret_cast<int*>(fb_bounds(const_cast<int*>(fb), m));
+    knn_fallback_hits_kernel<OT, KC><<<(unsigned)ceil_div(m, 8), 256, 0, st>>>(
+        list_cnt, fb, hit_cnt, hit_d, hit_i, (int)hcap, (int)k, over_cnt, over_list, (OT*)od, oi,
+        base);
+    TB_LAUNCH_CHECK("knn_fallback_hits");
+    list_cnt = over_cnt;
+    list = over_list;
+  }
+  // stage 2 (exhaustive; normally nothing left): per-block top-K' over
+  // database slices, then one merge
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(4 * sms, cap));
   double* sc_d = (double*)scratch;
   int* sc_i = (int*)(sc_d + cap * KC);
   if (d <= 64)
     knn_fallback_rows_kernel<T, KC, MET, 64><<<G, 256, 0, st>>>((const T*)x, (const T*)q, n, d,
-                                                                stats, fb, sc_d, sc_i);
+                                                                list_cnt, list, sc_d, sc_i);
   else
     knn_fallback_partial_kernel<T, KC, MET><<<G, 256, 0, st>>>((const T*)x, (const T*)q, n, d,
-                                                               stats, fb, sc_d, sc_i);
+                                                               list_cnt, list, sc_d, sc_i);
   TB_LAUNCH_CHECK("knn_fallback_partial");
   knn_fallback_merge_kernel<OT, KC><<<(unsigned)ceil_div(m, 8), 256, 0, st>>>(
-      stats, fb, G, (int)k, sc_d, sc_i, (OT*)od, oi, base);
+      list_cnt, list, G, (int)k, sc_d, sc_i, (OT*)od, oi, base);
   TB_LAUNCH_CHECK("knn_fallback_merge");
   return TB_OK;
 }
