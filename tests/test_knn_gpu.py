@@ -285,6 +285,27 @@ def test_fallback_path_is_exact(engines, monkeypatch):
     assert rel_err(res.dist, ref_d) < 1e-12
 
 
+@pytest.mark.parametrize("metric", ["l2", "cosine", "l1"])
+@pytest.mark.parametrize("d", [20, 128, 300])
+def test_fallback_stages_exact(metric, d, monkeypatch):
+    """Both fallback stages, every query forced through them: the bounded
+    hit-buffer scan (most queries) and, for queries with more rows tied at
+    the k-th distance than the hit buffer holds (90 exact duplicates of the
+    nearest row), the exhaustive kernels; ties -> lower index throughout."""
+    monkeypatch.setenv("TB_FORCE_FALLBACK", "1")
+    rng = np.random.default_rng(d)
+    x = rng.standard_normal((6000, d)).astype(np.float32)
+    q = rng.standard_normal((41, d)).astype(np.float32)
+    dup = rng.choice(6000, 90, replace=False)
+    x[dup] = q[3] + 0.01                      # query 3: 90 rows tied at its k nearest
+    engine = "simt" if metric == "l1" else "tc1"
+    ref_d, ref_i = oknn.exact(x, q, 10, metric=metric)
+    res = tb.knn(x, q, 10, metric=metric, engine=engine, return_result=True)
+    assert res.fallback_queries == 41
+    assert np.array_equal(res.idx[3], np.sort(dup)[:10])
+    mcheck(res.dist, res.idx, ref_d, ref_i, x, q, metric)
+
+
 def test_input_buffers_untouched(engines):
     torch = _torch()
     rng = np.random.default_rng(8)
