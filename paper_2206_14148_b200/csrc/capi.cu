@@ -460,10 +460,12 @@ static int knn_run_impl(const tb_knn_plan* p, const void* x, const void* q,
                          qn64, qnorm, qln, stats, p->n, p->m, p->d, p->k, c1, c2,
                          out_dist, out_idx, index_base, fb, st);
   if (rc) return rc;
-  // the per-chunk candidate lists (kCandS, kCandI) are dead after the last
-  // merge: the fallback uses them as scratch
+  // everything the planner placed from kXn on (norms, candidate and running
+  // lists, thresholds, operand and chunk staging) is dead once the re-rank
+  // has run: the fallback uses it as scratch (its hit buffers need room on
+  // clustered data, where a query's bound can enclose hundreds of rows)
   return launch_knn_fallback(p->dtype, p->out_dtype, p->metric, x, q, p->n, p->m, p->d, p->k, stats, fb,
-                             at(kCandS), p->off[kRunS] - p->off[kCandS], out_dist, out_idx,
+                             at(kXn), p->workspace_bytes - p->off[kXn], out_dist, out_idx,
                              index_base, st);
 }
 

@@ -1415,12 +1415,27 @@ knn_fallback_tile_kernel(const T* __restrict__ x, const T* __restrict__ q, int64
         }
       };
       if (sizeof(T) == 4 && (d & 3) == 0) {
+        // 4 row elements per step; each query's 4 values as two 16-byte
+        // shared loads (one load per two fp64 updates)
         for (int64_t c = 0; c < d; c += 4) {
           const float4 v = __ldg(reinterpret_cast<const float4*>(xr + c));
-          term(c, v.x);
-          term(c + 1, v.y);
-          term(c + 2, v.z);
-          term(c + 3, v.w);
+          const double b0 = v.x, b1 = v.y, b2 = v.z, b3 = v.w;
+          if (MET == TB_METRIC_COSINE) xx = fma(b3, b3, fma(b2, b2, fma(b1, b1, fma(b0, b0, xx))));
+#pragma unroll
+          for (int qi = 0; qi < kFbQB; ++qi) {
+            const double2 a01 = *reinterpret_cast<const double2*>(fq + qi * d + c);
+            const double2 a23 = *reinterpret_cast<const double2*>(fq + qi * d + c + 2);
+            double t = acc[qi];
+            if (MET == TB_METRIC_COSINE) {
+              t = fma(a23.y, b3, fma(a23.x, b2, fma(a01.y, b1, fma(a01.x, b0, t))));
+            } else if (MET == TB_METRIC_L1) {
+              t = (((t + fabs(a01.x - b0)) + fabs(a01.y - b1)) + fabs(a23.x - b2)) + fabs(a23.y - b3);
+            } else {
+              const double d0 = a01.x - b0, d1 = a01.y - b1, d2 = a23.x - b2, d3 = a23.y - b3;
+              t = fma(d3, d3, fma(d2, d2, fma(d1, d1, fma(d0, d0, t))));
+            }
+            acc[qi] = t;
+          }
         }
       } else {
         for (int64_t c = 0; c < d; ++c) term(c, (double)xr[c]);
@@ -1492,7 +1507,9 @@ static int fallback_launch(const void* x, const void* q, int64_t n, int64_t d, i
   // then hcap (distance, row) slots per query); what it cannot settle goes
   // on through stats[kFbOverWord] and the overflow list (the bounds' space,
   // dead once the scan has run)
-  const int64_t hcap = std::min<int64_t>(64, (scratch_bytes / std::max<int64_t>(m, 1) - 8) / 12);
+  // (up to 1024 slots: on clustered data the k-th candidate's distance can
+  // enclose hundreds of rows of the query's cluster)
+  const int64_t hcap = std::min<int64_t>(1024, (scratch_bytes / std::max<int64_t>(m, 1) - 8) / 12);
   const size_t fq_bytes = (size_t)kFbQB * d * 8;
   if (hcap >= k + 4 && fq_bytes <= 48 * 1024) {
     int* hit_cnt = (int*)scratch;
