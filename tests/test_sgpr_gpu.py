@@ -118,6 +118,23 @@ def test_kernel_mvm_ard(kind):
     assert rel_err(out, ref) < 1e-13
 
 
+@pytest.mark.parametrize("kind", ["rbf", "matern32"])
+@pytest.mark.parametrize("dim,n,M", [(1, 5003, 2503), (11, 3001, 1031), (16, 257, 5)])
+def test_kernel_mvm_ragged_tiles(kind, dim, n, M):
+    """The fixed-dimension MVM kernels over several Z tiles with a ragged
+    last tile, a ragged last row block, and M smaller than a tile: same
+    result as the fp64 oracle, and deterministic."""
+    rng = np.random.default_rng(dim + M)
+    X = rng.standard_normal((n, dim))
+    Z = rng.standard_normal((M, dim))
+    w = rng.standard_normal(M)
+    ls = list(np.linspace(0.7, 1.6, dim))
+    ref = omvm.kernel_mvm(X, Z, w, kind, 1.3, ls)
+    out = tb.kernel_mvm(X, Z, w, kind, 1.3, ls)
+    assert rel_err(out, ref) < 1e-13
+    assert np.array_equal(out, tb.kernel_mvm(X, Z, w, kind, 1.3, ls))
+
+
 @pytest.mark.parametrize("N,M", [(9000, 300), (777, 129)])
 def test_sgpr_i8_cta_pair_kernel_same_statistics(N, M, monkeypatch):
     """Opt-in CTA-pair Gram (tcgen05.mma.cta_group::2, TB_I8_PAIR=1) returns
