@@ -191,7 +191,24 @@ def compare(got_dist, got_idx, ref_dist, ref_idx, x, q,
             report["mismatches"] += 1
             report["first_bad"] = report["first_bad"] or (
                 "neighbour", r, gi.tolist(), ri.tolist())
-    report["dist_rel_err"] = rel_err(got_dist, ref_dist)
+    if metric == "cosine":
+        # cosine distances live in [0, 2]; exactly parallel rows have distance
+        # 0 computed as a few ulps of either sign, so the error is measured
+        # against the metric's scale, not against an all-~0 reference
+        report["dist_rel_err"] = float(np.max(np.abs(got_dist - ref_dist), initial=0.0)
+                                       / max(float(np.max(np.abs(ref_dist), initial=0.0)), 1.0))
+    else:
+        # the reference's expanded form ||q||^2 + ||x||^2 - 2 q.x leaves a few
+        # ulps of that sum where the true distance is 0 (duplicates); the
+        # error is measured against max(max |ref|, 1e-6 of the norms' scale)
+        x64 = np.asarray(x, dtype=np.float64)
+        q64 = np.asarray(q, dtype=np.float64)
+        sq = (float(np.max(np.einsum("ij,ij->i", x64, x64), initial=0.0))
+              + float(np.max(np.einsum("ij,ij->i", q64, q64), initial=0.0)))
+        floor = 1e-6 * sq if metric == "l2" else 0.0
+        den = max(float(np.max(np.abs(ref_dist), initial=0.0)), floor)
+        diff = float(np.max(np.abs(got_dist - ref_dist), initial=0.0))
+        report["dist_rel_err"] = diff / den if den > 0 else (0.0 if diff == 0 else np.inf)
     report["ok"] = (report["mismatches"] == 0 and report["bad_index"] == 0
                     and report["dist_rel_err"] <= dist_rtol)
     return report
