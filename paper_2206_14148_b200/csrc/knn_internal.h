@@ -39,10 +39,15 @@ constexpr int kFbOverWord = 17;      // count of fallback queries the hit-buffer
 
 // kFbList region: int fb_list[m] (uncertified query rows), then (8-byte
 // aligned) double bounds[m]: the exact k-th candidate distance of each, an
-// upper bound on its true k-th distance (the fallback scans below it)
-inline int64_t fb_region_bytes(int64_t m) { return ((m * 4 + 7) & ~(int64_t)7) + m * 8; }
+// upper bound on its true k-th distance (the fallback scans below it), then
+// int hits[m]: the fallback's hit counts (zeroed by the re-rank as it
+// appends a query, so the common no-fallback call needs no memset)
+inline int64_t fb_region_bytes(int64_t m) { return ((m * 4 + 7) & ~(int64_t)7) + m * 12; }
 __host__ __device__ __forceinline__ double* fb_bounds(int* fb, int64_t m) {
   return reinterpret_cast<double*>(reinterpret_cast<char*>(fb) + ((m * 4 + 7) & ~(int64_t)7));
+}
+__host__ __device__ __forceinline__ int* fb_hits(int* fb, int64_t m) {
+  return reinterpret_cast<int*>(fb_bounds(fb, m) + m);
 }
 
 // kGThr region: per-query thresholds (u32[m], padded to 32 words) followed by

@@ -1128,6 +1128,7 @@ __global__ void knn_refine_kernel(const float* __restrict__ cs,
         const int pos = atomicAdd(reinterpret_cast<int*>(&stats[1]), 1);
         fb_list[pos] = (int)r;
         fb_bounds(fb_list, m)[pos] = kth;     // the true k-th distance is <= kth
+        fb_hits(fb_list, m)[pos] = 0;
       }
     }
   }
@@ -1503,19 +1504,18 @@ static int fallback_launch(const void* x, const void* q, int64_t n, int64_t d, i
   if (cap < m) return fail(TB_ERR_ARG, "fallback scratch too small");
   const unsigned* list_cnt = stats + 1;
   const int* list = fb;
-  // stage 1: bounded scan into per-query hit buffers (scratch: hit counts,
-  // then hcap (distance, row) slots per query); what it cannot settle goes
+  // stage 1: bounded scan into per-query hit buffers (hcap (distance, row)
+  // slots per query in the scratch); what it cannot settle goes
   // on through stats[kFbOverWord] and the overflow list (the bounds' space,
   // dead once the scan has run)
   // (up to 1024 slots: on clustered data the k-th candidate's distance can
   // enclose hundreds of rows of the query's cluster)
-  const int64_t hcap = std::min<int64_t>(1024, (scratch_bytes / std::max<int64_t>(m, 1) - 8) / 12);
+  const int64_t hcap = std::min<int64_t>(1024, scratch_bytes / std::max<int64_t>(m, 1) / 12);
   const size_t fq_bytes = (size_t)kFbQB * d * 8;
   if (hcap >= k + 4 && fq_bytes <= 48 * 1024) {
-    int* hit_cnt = (int*)scratch;
-    double* hit_d = (double*)((char*)scratch + ((m * 4 + 7) & ~(int64_t)7));
+    int* hit_cnt = fb_hits(const_cast<int*>(fb), m);        // zeroed by the re-rank
+    double* hit_d = (double*)scratch;
     int* hit_i = (int*)(hit_d + m * hcap);
-    TB_CUDA_TRY(cudaMemsetAsync(hit_cnt, 0, m * 4, st));
     knn_fallback_tile_kernel<T, MET><<<4 * sms, 256, fq_bytes, st>>>(
         (const T*)x, (const T*)q, n, d, list_cnt, fb, fb_bounds(const_cast<int*>(fb), m), hit_cnt,
         hit_d, hit_i, (int)hcap);
