@@ -596,7 +596,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       //    round the running max is valid (slots only decrease).
       float p_max = -INFINITY, pool_thr = INFINITY;
       int p_slot = 0;
-      unsigned pv[kSel ? 32 : 1];
       if (!kSel && qv) {
         unsigned mx = 0u;
 #pragma unroll
@@ -612,19 +611,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         // two column halves (which share SMSPs) half a period apart
         const int pt = t - tb + (half ? kPoolEvery / 2 : 0);
         const bool refresh = kSel && qv && (t == tb || (pt & (kPoolEvery - 1)) == 0);
-        if constexpr (kSel) {
-          if (refresh) {
-            const uint4* p4 = reinterpret_cast<const uint4*>(qpool);
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              const uint4 w = __ldcg(p4 + v);
-              pv[4 * v] = w.x;
-              pv[4 * v + 1] = w.y;
-              pv[4 * v + 2] = w.z;
-              pv[4 * v + 3] = w.w;
-            }
-          }
-        } else {
+        if constexpr (!kSel) {
           p_max = fmaxf(p_max, fkey_inv(pk) * sc_mul);
           if (++p_slot == KC) {
             pool_thr = p_max;
@@ -694,7 +681,22 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         if (ew == 0 && lane == 0) { TB_TR(1024, i, 3); }
         if (qv && L.worst() < thr_g) atomicMin(gthr + q, fkey(L.worst() * sc_inv));
         if constexpr (kSel) {
-          if (refresh) pool_thr = fminf(pool_thr, fkey_inv(kth_of_32<KC>(pv)) * sc_mul);
+          // the pool snapshot is read here, after the tile, with the
+          // accumulator registers dead (its L2 latency is exposed once per
+          // kPoolEvery tiles instead of 32 registers held across every tile)
+          if (refresh) {
+            unsigned pv[32];
+            const uint4* p4 = reinterpret_cast<const uint4*>(qpool);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const uint4 w = __ldcg(p4 + v);
+              pv[4 * v] = w.x;
+              pv[4 * v + 1] = w.y;
+              pv[4 * v + 2] = w.z;
+              pv[4 * v + 3] = w.w;
+            }
+            pool_thr = fminf(pool_thr, fkey_inv(kth_of_32<KC>(pv)) * sc_mul);
+          }
         }
         if (ew == 0 && lane == 0) { TB_TR(1024, i, 5); }
       }
