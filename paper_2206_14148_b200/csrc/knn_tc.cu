@@ -636,23 +636,27 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
         const uint32_t taddr =
             tmem + ((uint32_t)(quad * 32) << 16) + buf * kTcN + half * (kTcN / 2);
         const int base = idx_base + t * kTcN + half * (kTcN / 2);
+        // 32-column chunks, software-pipelined by one: chunk c+1's TMEM load
+        // is in flight while chunk c is scanned (two 32-register buffers, as
+        // many as the load pairs used), so three of the four load latencies
+        // hide behind max trees instead of two being exposed per tile
+        uint32_t ra[32], rb[32];
+        tmem_ld32(taddr, ra);
+        tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < kTcN / 64; c += 2) {
-          uint32_t ra[32], rb[32];
-          tmem_ld32(taddr + c * 32, ra);
-          tmem_ld32(taddr + (c + 1) * 32, rb);
-          tmem_ld_wait();
-          if (c + 2 >= kTcN / 64) {
-            // last columns are in registers: release the accumulator now so
-            // the MMA of tile i+2 may overwrite it while they are processed
+        for (int c = 0; c < kTcN / 2 / 32; ++c) {
+          uint32_t(&r)[32] = (c & 1) ? rb : ra;
+          uint32_t(&nx)[32] = (c & 1) ? ra : rb;
+          if (c + 1 < kTcN / 2 / 32) {
+            tmem_ld32(taddr + (c + 1) * 32, nx);
+          } else {
+            // every column is in registers: release the accumulator now so
+            // the MMA of tile i+2 may overwrite it while the last is scanned
             tc_fence_before();
             mbar_arrive(&tempty[buf]);
             if (ew == 0 && lane == 0) { TB_TR(1024, i, 2); }
           }
-          if (TB_DBG(work) & 1) continue;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t(&r)[32] = h ? rb : ra;
+          if (!(TB_DBG(work) & 1)) {
             // common case: no column beats the threshold -> one max tree
             // over acc' (score = -acc'); the rare insertions run from one
             // compact loop so the hot path fits the I-cache
@@ -672,9 +676,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
                 atomicAdd(cn + 2, (unsigned long long)__popc(mask));
               }
 #endif
-              insert_masked_acc(L, r, mask, base + (c + h) * 32, thr_g, qpool, sc_inv);
+              insert_masked_acc(L, r, mask, base + c * 32, thr_g, qpool, sc_inv);
             }
           }
+          if (c + 1 < kTcN / 2 / 32) tmem_ld_wait();
         }
         // publish the running K'-th score every tile: the other column half
         // and every other CTA on this query tighten their thresholds with it
