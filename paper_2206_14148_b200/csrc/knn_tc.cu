@@ -607,6 +607,20 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
       for (int t = tb; t < te; ++t, ++i) {
         const int buf = i & 1;
         if (ew == 0 && lane == 0) { TB_TR(1024, i, 4); }
+        if (ew == 0 && lane == 0) { TB_TR(1024, i, 0); }
+        mbar_wait(&tfull[buf], (i >> 1) & 1);
+        if (ew == 0 && lane == 0) { TB_TR(1024, i, 1); }
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem + ((uint32_t)(quad * 32) << 16) + buf * kTcN + half * (kTcN / 2);
+        const int base = idx_base + t * kTcN + half * (kTcN / 2);
+        // 32-column chunks, software-pipelined by one: chunk c+1's TMEM load
+        // is in flight while chunk c is scanned (two 32-register buffers, as
+        // many as the load pairs used), so three of the four load latencies
+        // hide behind max trees instead of two being exposed per tile
+        uint32_t ra[32], rb[32];
+        tmem_ld32(taddr, ra);
+        // the per-tile bookkeeping runs while the first chunk is in flight
         // refresh at the unit's first tile, then every kPoolEvery tiles, the
         // two column halves (which share SMSPs) half a period apart
         const int pt = t - tb + (half ? kPoolEvery / 2 : 0);
@@ -629,19 +643,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tm_qhi,
           if (!kSel) pk = qpool[p_slot];
           gk = gthr[q];
         }
-        if (ew == 0 && lane == 0) { TB_TR(1024, i, 0); }
-        mbar_wait(&tfull[buf], (i >> 1) & 1);
-        if (ew == 0 && lane == 0) { TB_TR(1024, i, 1); }
-        tc_fence_after();
-        const uint32_t taddr =
-            tmem + ((uint32_t)(quad * 32) << 16) + buf * kTcN + half * (kTcN / 2);
-        const int base = idx_base + t * kTcN + half * (kTcN / 2);
-        // 32-column chunks, software-pipelined by one: chunk c+1's TMEM load
-        // is in flight while chunk c is scanned (two 32-register buffers, as
-        // many as the load pairs used), so three of the four load latencies
-        // hide behind max trees instead of two being exposed per tile
-        uint32_t ra[32], rb[32];
-        tmem_ld32(taddr, ra);
         tmem_ld_wait();
 #pragma unroll
         for (int c = 0; c < kTcN / 2 / 32; ++c) {
