@@ -110,8 +110,15 @@ def knn_sharded_host(xh_shard, qh, k: int, *, index_base: int, operator, group=N
                    torch.empty((int(p.m), int(p.d)), dtype=td, device=operator.device),
                    *operator.alloc_outputs())
     dd, idd = staging[2], staging[3]
-    dh_local = torch.empty(tuple(dd.shape), dtype=dd.dtype).pin_memory()
-    ih_local = torch.empty(tuple(idd.shape), dtype=torch.int64).pin_memory()
+    # the per-shard host copy of tb_knn_run_host is not used (the lists meet
+    # on the device); its pinned buffers are made once per operator, not per
+    # call (a pinned allocation costs far more than the copy)
+    cached = getattr(operator, "_shard_host_out", None)
+    if cached is None or tuple(cached[0].shape) != tuple(dd.shape) or cached[0].dtype != dd.dtype:
+        cached = (torch.empty(tuple(dd.shape), dtype=dd.dtype).pin_memory(),
+                  torch.empty(tuple(idd.shape), dtype=torch.int64).pin_memory())
+        operator._shard_host_out = cached
+    dh_local, ih_local = cached
 
     def local(_x, _q, _k, base):
         operator.run_host(xh_shard, qh, (dh_local, ih_local), index_base=base,
