@@ -190,8 +190,49 @@ class SGPR:
         s = self._stats if self._stats is not None and self._stats.Sigma is not None \
             else self.statistics()
         if s.plan.sigma_layout == _lib.TB_SIGMA_TILES and self.tail == "packed":
-            return self._tail_packed(s)
+            try:
+                return self._tail_packed(s)
+            except EvaluationError as ex:
+                # The packed tail factors A = Kuu + Sigma/s2 itself, whose
+                # condition number is about cond(Kuu) cond(B); the dense tail
+                # factors GPflow's B = I + L^-1 Sigma L^-T / s2 (>= I).  With
+                # cond(A) ~ 1e14 (long lengthscales, dense inducing points)
+                # the blocked packed factorisation can meet a negative pivot
+                # where LAPACK-style cuSOLVER on B does not: recompute the
+                # statistics (the packed tail consumed them) and take the
+                # dense tail when it fits the limit, else re-raise.
+                if "not positive definite" not in str(ex) or not self._dense_tail_fits():
+                    raise
+                self._refit_ill_conditioned()
+                s = self.statistics()
         return self._tail_dense(s)
+
+    def _refit_ill_conditioned(self):
+        """After the packed factorisation failed: drop the consumed
+        statistics and, for engine "auto", recompute them in fp64 (at cond(A)
+        ~ 1e14 the 24-bit fixed-point rounding of Kuf, exact as it is, moves
+        the ELBO by ~1e-4); an explicitly chosen engine is kept."""
+        self._stats = None
+        if self.engine == "auto":
+            self.engine = "f64"
+
+    def _dense_tail_fits(self) -> bool:
+        """Whether the dense tail (full Sigma + ~5 M x M fp64 work matrices
+        beside the packed statistics and the inputs) fits memory_limit."""
+        if self.memory_limit is None:
+            return True
+        from .sizes import as_limit
+        limit = as_limit(self.memory_limit)
+        M = int(self.Z.shape[0])
+        engine = "f64" if self.engine == "auto" else self.engine     # as _refit_ill_conditioned
+        inputs = sum(int(t.numel()) * t.element_size() for t in (self.X, self.y, self.Z))
+        try:
+            stats = int(plan(int(self.X.shape[0]), M, self.dim, kernel=self.kernel,
+                             memory_limit=self.memory_limit, resident_bytes=inputs,
+                             engine=engine).sigma_bytes)
+        except BudgetExceeded:
+            return False
+        return inputs + stats + 6 * 8 * M * M + (8 << 20) <= limit
 
     def _tail_packed(self, s):
         """In place on the packed tiles (tb_sgpr_tail_run): the evaluation
@@ -301,7 +342,16 @@ class SGPR:
         torch = _torch()
         M, dim = int(self.Z.shape[0]), self.dim
         if self.tail == "packed" and dim <= 16 and self.grad_peak_bytes() >= 0:
-            return self._elbo_and_grads_packed()
+            try:
+                return self._elbo_and_grads_packed()
+            except EvaluationError as ex:
+                # as in _tail: a negative pivot of the packed factorisation
+                # of A on a very ill-conditioned problem -> the dense path
+                # below (GPflow's formulation), if it fits; the packed path
+                # consumed the statistics, which are recomputed
+                if "not positive definite" not in str(ex):
+                    raise
+                self._refit_ill_conditioned()
         if self.memory_limit is not None:
             limit = as_limit(self.memory_limit)
             resident = (self.X.numel() + self.y.numel() + self.Z.numel()) * self.X.element_size()

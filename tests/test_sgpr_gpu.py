@@ -365,3 +365,21 @@ def test_packed_gradient_inside_memory_limit():
     for key in ("variance", "noise_variance", "lengthscales", "Z"):
         a, b = np.asarray(g[key], np.float64), np.asarray(g2[key], np.float64)
         assert np.max(np.abs(a - b)) <= 1e-4 * max(np.max(np.abs(b)), 1.0), key
+
+
+def test_packed_tail_falls_back_when_A_is_too_ill_conditioned():
+    """cond(Kuu + Sigma/s2) ~ 1e14 (2-D inputs, long lengthscales, dense
+    inducing points, jitter 1e-6): the packed in-place factorisation of A
+    meets a negative pivot, so the ELBO and the gradient take GPflow's dense
+    formulation (Cholesky of B = I + L^-1 Sigma L^-T / s2) - same answer as
+    the fp64 oracle, no error."""
+    X, y, Z, Xs = synthetic.sgpr_data(15364, 2, 432, seed=70, n_test=64, dtype=np.float32)
+    var, ls, noise = 1.8588339123918893, [2.4, 1.35], 0.05396516393244166
+    ref, w = osgpr.elbo(X, y, Z, "rbf", var, ls, noise)
+    m = tb.SGPR(X, y, Z, "rbf", var, ls, noise)
+    e = m.elbo()
+    assert abs(e - ref) <= 1e-4 * abs(ref)
+    assert rel_err(m.predict_mean(Xs), osgpr.predict_mean(Xs, Z, w, "rbf", var, ls)) <= 1e-4
+    e2, g = tb.SGPR(X, y, Z, "rbf", var, ls, noise).elbo_and_grads()
+    assert abs(e2 - ref) <= 1e-4 * abs(ref)
+    assert np.all(np.isfinite(np.asarray(g["Z"])))

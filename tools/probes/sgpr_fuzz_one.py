@@ -1,0 +1,39 @@
+import sys, os
+sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
+import numpy as np
+import paper_2206_14148_b200 as tb
+from oracle import sgpr as osgpr
+from paper_2206_14148_b200 import synthetic
+from conftest import rel_err
+seed = int(sys.argv[1])
+rng = np.random.default_rng(5000 + seed)
+N = int(rng.integers(500, 20_000)); d = int(rng.choice([2, 3, 5, 8, 11, 16])); M = int(rng.integers(8, min(600, N // 2)))
+kind = ["rbf", "matern32"][seed % 2]
+dtype = np.float32 if rng.random() < 0.7 else np.float64
+var = float(rng.uniform(0.5, 2.0)); ls = [float(v) for v in rng.uniform(0.8, 2.5, d)]; noise = float(rng.uniform(0.01, 0.2))
+engine = "auto" if rng.random() < 0.7 else "f64"
+X, y, Z, Xs = synthetic.sgpr_data(N, d, M, seed=seed, n_test=64, dtype=dtype)
+limit = None
+if rng.random() < 0.5:
+    inputs = (N * d + N + M * d) * np.dtype(dtype).itemsize
+    full = tb.sgpr.plan(N, M, d, kernel=kind).peak_bytes
+    limit = inputs + int((full - inputs) * rng.uniform(0.5, 1.0)) + 2**20
+print("N", N, "d", d, "M", M, kind, dtype, "var", var, "noise", noise, "engine", engine, "limit", limit, "ls", np.round(ls, 2))
+ref, w = osgpr.elbo(X, y, Z, kind, var, ls, noise)
+mu_ref = osgpr.predict_mean(Xs, Z, w, kind, var, ls)
+K = osgpr.kuu(Z, kind, var, ls, 1e-6)
+print("cond(Kuu) %.3e" % np.linalg.cond(K))
+for eng, tail in (("i8", "packed"), ("i8", "dense"), ("f64", "dense"), ("f64", "packed")):
+    try:
+        m = tb.SGPR(X, y, Z, kind, var, ls, noise, engine=eng, tail=tail)
+        e = m.elbo(); mu = m.predict_mean(Xs)
+        print(eng, tail, "elbo rel %.2e" % (abs(e - ref) / abs(ref)), "mean rel_err %.2e" % rel_err(mu, mu_ref))
+    except Exception as ex:
+        print(eng, tail, "ERR", repr(ex)[:100])
+# oracle's own sensitivity: GPflow order
+try:
+    ref2, w2 = osgpr.elbo_afirst(X, y, Z, kind, var, ls, noise)
+    mu2 = osgpr.predict_mean(Xs, Z, w2, kind, var, ls)
+    print("oracle A-first vs Sigma-first: elbo rel %.2e mean rel_err %.2e" % (abs(ref2 - ref) / abs(ref), rel_err(mu2, mu_ref)))
+except Exception as ex:
+    print("afirst err", repr(ex)[:100])
