@@ -225,8 +225,9 @@ TB_API int tb_sgpr_sigma_unpack(const tb_sgpr_plan* plan, const double* Sigma,
  * The O(M^3) part of the ELBO on a TB_SIGMA_TILES Sigma, in place, so the
  * whole evaluation fits memory_limit (two packed M x M matrices):
  *   Kuu = L L^T,  Kuu + Sigma/s2 = P P^T (P overwrites Sigma),  X = L^-1 P
- * out4 = {sum log diag L, sum log diag P, |P^-1 v|^2, ||X||_F^2} (device
- * doubles) and w_out[M] = P^-T P^-1 v / s2 (the predictive-mean weights).
+ * out4 = {sum log diag L, sum log diag P, |P^-1 v|^2, ||X||_F^2,
+ *         min diag(L)^2, max diag(L)^2} (6 device doubles: the last two
+ *         bound cond(Kuu) from below, a conditioning indicator) and w_out[M] = P^-T P^-1 v / s2 (the predictive-mean weights).
  * Then (GPflow SGPR.elbo): sum log diag LB = out4[1] - out4[0],
  * c^T c = out4[2] / s2^2, tr(AAT) = out4[3] - M_pad.  Synchronises `stream`
  * (reports a failed Cholesky as TB_ERR_ARG). */

@@ -443,6 +443,34 @@ tail_reduce_kernel(const double* __restrict__ base, int mode, double* __restrict
   }
 }
 
+// min and max of diag(L)^2 over the M real rows (padding rows are identity):
+// cond(Kuu) >= max/min, the conditioning indicator the Python layer uses to
+// move engine "auto" to fp64 statistics (one block, 128 threads)
+__global__ void tail_diag_range_kernel(const double* __restrict__ L, int nt, int64_t M,
+                                       double* __restrict__ out2) {
+  __shared__ double smin[kTT], smax[kTT];
+  double lo = INFINITY, hi = 0.0;
+  for (int a = 0; a < nt; ++a) {
+    const int64_t row = (int64_t)a * kTT + threadIdx.x;
+    if (row < M) {
+      const double d = L[tslot(a, a) * kTE + (int64_t)threadIdx.x * kTT + threadIdx.x];
+      lo = fmin(lo, d * d);
+      hi = fmax(hi, d * d);
+    }
+  }
+  smin[threadIdx.x] = lo;
+  smax[threadIdx.x] = hi;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 1; t < kTT; ++t) {
+      lo = fmin(lo, smin[t]);
+      hi = fmax(hi, smax[t]);
+    }
+    out2[0] = lo;
+    out2[1] = hi;
+  }
+}
+
 __global__ void sum_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
   // fixed order: lane-strided partial sums, then a fixed shuffle tree
   double s = 0.0;
@@ -544,7 +572,8 @@ int tail_run(int64_t M, int64_t M_pad, const void* Z, int dtype, const KernParam
   double* scratch = vv + M_pad;
   ws += round_up(4 * M_pad * 8, 256);
   double* part = (double*)ws;
-  double* scal = part + tiles;            // [0] logdet L, [1] logdet P, [2] |u|^2, [3] ||X||^2
+  double* scal = part + tiles;            // [0] logdet L, [1] logdet P, [2] |u|^2, [3] ||X||^2,
+                                          // [4] min diag(L)^2, [5] max diag(L)^2
   int* info = (int*)(scal + 6);
   TB_CUDA_TRY(cudaFuncSetAttribute(tail_potrf_inv_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -586,6 +615,7 @@ int tail_run(int64_t M, int64_t M_pad, const void* Z, int dtype, const KernParam
   // log dets
   tail_reduce_kernel<<<tiles, 256, 0, st>>>(L, 0, part);
   sum_kernel<<<1, 32, 0, st>>>(part, tiles, scal + 0);
+  tail_diag_range_kernel<<<1, kTT, 0, st>>>(L, nt, M, scal + 4);
   tail_reduce_kernel<<<tiles, 256, 0, st>>>(sigma, 0, part);
   sum_kernel<<<1, 32, 0, st>>>(part, tiles, scal + 1);
   TB_LAUNCH_CHECK("tail_logdet");
@@ -609,7 +639,7 @@ int tail_run(int64_t M, int64_t M_pad, const void* Z, int dtype, const KernParam
   tail_reduce_kernel<<<tiles, 256, 0, st>>>(sigma, 1, part);
   sum_kernel<<<1, 32, 0, st>>>(part, tiles, scal + 3);
   TB_LAUNCH_CHECK("tail_frob");
-  TB_CUDA_TRY(cudaMemcpyAsync(out4, scal, 4 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  TB_CUDA_TRY(cudaMemcpyAsync(out4, scal, 6 * sizeof(double), cudaMemcpyDeviceToDevice, st));
   int h_info = 0;
   TB_CUDA_TRY(cudaMemcpyAsync(&h_info, info, sizeof(int), cudaMemcpyDeviceToHost, st));
   TB_CUDA_TRY(cudaStreamSynchronize(st));

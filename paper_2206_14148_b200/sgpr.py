@@ -48,6 +48,14 @@ def _dev_tensor(a, device):
     return a.to(device).contiguous()
 
 
+# cond(Kuu) lower bound (max/min of the packed tail's diag(L)^2) above which
+# engine "auto" recomputes the statistics in fp64 when the dense tail fits
+# the limit: the fixed-point statistics move the predictive mean by ~cond(Kuu)
+# x 2e-12 (5e-4 seen at cond 2.8e8), and the diag bound under-reads cond(Kuu)
+# by up to ~250x on smooth kernels (fuzz: 8.6e5 for 2.1e8)
+COND_FP64 = 1e5
+
+
 def plan(N: int, M: int, dim: int, *, kernel: str = "rbf", dtype=np.float32,
          memory_limit=None, resident_bytes: int | None = None,
          engine: str = "auto") -> _lib.SgprPlan:
@@ -153,6 +161,7 @@ class SGPR:
         self.tail = tail          # packed: in place on the fixed-point engine's tiles
         self._stats = None
         self._w = None
+        self.cond_kuu_lb = None   # set by the packed tail: max/min diag(L)^2
 
     # -- hot path -----------------------------------------------------------
     def statistics(self, stream=None) -> SgprStats:
@@ -191,7 +200,16 @@ class SGPR:
             else self.statistics()
         if s.plan.sigma_layout == _lib.TB_SIGMA_TILES and self.tail == "packed":
             try:
-                return self._tail_packed(s)
+                bound = self._tail_packed(s)
+                # well conditioned (the usual case): done.  Otherwise the 2^-25
+                # rounding of Kuf, amplified by cond(A), can move the
+                # predictive weights past 1e-4: engine "auto" redoes the
+                # statistics in fp64 when the dense tail fits the limit
+                if not (self.engine == "auto" and self.cond_kuu_lb > COND_FP64
+                        and self._dense_tail_fits()):
+                    return bound
+                self._refit_ill_conditioned()
+                s = self.statistics()
             except EvaluationError as ex:
                 # The packed tail factors A = Kuu + Sigma/s2 itself, whose
                 # condition number is about cond(Kuu) cond(B); the dense tail
@@ -245,7 +263,7 @@ class SGPR:
         ws = torch.empty(max(int(lib.tb_sgpr_tail_workspace(ctypes.byref(p))), 1),
                          dtype=torch.uint8, device=self.device)
         w = torch.empty(M, dtype=torch.float64, device=self.device)
-        out = torch.empty(4, dtype=torch.float64, device=self.device)
+        out = torch.empty(6, dtype=torch.float64, device=self.device)
         st = torch.cuda.current_stream(self.device)
         rc = lib.tb_sgpr_tail_run(ctypes.byref(p), self.Z.data_ptr(), self.variance,
                                   self.lengthscales.ctypes.data_as(ctypes.c_void_p), self.jitter,
@@ -255,7 +273,9 @@ class SGPR:
         s.Sigma = None                     # overwritten by the in-place factorisation
         _lib.check(rc, "sgpr_tail")
         del ws
-        logdet_l, logdet_p, uu, xx = (float(t) for t in out.tolist())
+        logdet_l, logdet_p, uu, xx, dmin, dmax = (float(t) for t in out.tolist())
+        # max/min of diag(L)^2 bounds cond(Kuu) from below
+        self.cond_kuu_lb = dmax / dmin if dmin > 0 else math.inf
         s2, N = self.noise_variance, s.N
         bound = (-0.5 * N * LOG2PI - (logdet_p - logdet_l) - 0.5 * N * math.log(s2)
                  - 0.5 * s.yy / s2 + 0.5 * uu / (s2 * s2) - 0.5 * N * self.variance / s2

@@ -6,10 +6,11 @@ terms, since it is a small difference of large ones).
 
 The default engine rounds Kuf once to 24-bit fixed point (relative 2^-25 of
 the variance per entry).  The ELBO absorbs that at any conditioning; the
-predictive mean w = A^-1 v / s2 amplifies it by cond(A): with cond(Kuu)
-above ~1e7 (dense inducing points, long lengthscales) the i8 mean can miss
-1e-4 (seen: 5e-4 at cond(Kuu) = 2.8e8), and engine="f64" is the documented
-choice there - the test then holds the f64 engine to 1e-4 instead."""
+predictive mean w = A^-1 v / s2 amplifies it by cond(A) (5e-4 seen at
+cond(Kuu) = 2.8e8 with engine "i8"), so engine "auto" recomputes the
+statistics in fp64 when the packed tail's diag(L) shows an ill-conditioned
+Kuu and the dense tail fits memory_limit; only when it does not fit is the
+mean held to the looser bound the fixed-point statistics give there."""
 
 import os
 
@@ -52,8 +53,10 @@ def test_sgpr_random_cases_match_oracle(seed):
     assert abs(e - ref) <= 1e-4 * abs(ref) or abs(e - ref) <= 1e-9 * scale, (seed, e, ref)
     mu = m.predict_mean(Xs)
     mu_ref = osgpr.predict_mean(Xs, Z, w, kind, var, ls)
-    if engine != "f64" and np.linalg.cond(osgpr.kuu(Z, kind, var, ls, 1e-6)) > 1e7:
-        mf = tb.SGPR(X, y, Z, kind, var, ls, noise, engine="f64")
-        mf.elbo()
-        mu = mf.predict_mean(Xs)
-    assert rel_err(mu, mu_ref) <= 1e-4, (seed, rel_err(mu, mu_ref))
+    tol = 1e-4
+    if m.engine != "f64" and m.cond_kuu_lb is not None and m.cond_kuu_lb > tb.sgpr.COND_FP64:
+        # ill-conditioned and the fp64 refit did not fit memory_limit: the
+        # fixed-point mean is off by ~cond(Kuu) x 2e-12
+        assert not m._dense_tail_fits()
+        tol = 2e-3
+    assert rel_err(mu, mu_ref) <= tol, (seed, rel_err(mu, mu_ref), m.cond_kuu_lb)
