@@ -247,7 +247,8 @@ TB_API int tb_sgpr_tail_run(const tb_sgpr_plan* plan, const void* Z, double vari
  * footprint is two packed M x M triangles + 3 column panels.
  * out8: [0] sum log diag L, [1] sum log diag P, [2] |P^-1 v|^2,
  * [3] tr(Kuu^-1 A), [4] tr(A^-1 Kuu), [5] w^T Kuu w (A = Kuu + Sigma/s2,
- * w = A^-1 v / s2).  grad_hyp[2 (1 + dim)]: data-side (variance,
+ * w = A^-1 v / s2), [6] min diag(L)^2, [7] max diag(L)^2 (a lower bound on
+ * cond(Kuu)).  grad_hyp[2 (1 + dim)]: data-side (variance,
  * lengthscales) then Kuu-side sums (the latter doubled: halve them);
  * grad_Z[2 M dim]: data side then Kuu side.  Both are accumulated into
  * (zero them first).  dim <= 16.  No reference counterpart. */

@@ -1343,6 +1343,7 @@ int grad_tail_run(int64_t M, int64_t M_pad, const void* Z, const void* X, const 
   double* scratch = vv + M_pad;
   double* part = (double*)take((int64_t)(tiles + 16 + 3 * nt + 2 * 1024) * 8);
   double* scal = part + tiles;            // [0] logdet L [1] logdet P [2] |u|^2 [3..5] traces
+                                          // [6] min diag(L)^2 [7] max diag(L)^2
   int* info = (int*)(scal + 8);
   double* tr_part = scal + 16;            // [nt] trace blocks of A Kuu^-1
   double* ak_part = tr_part + nt;         // [nt] blocks of tr(A^-1 Kuu)
@@ -1394,6 +1395,7 @@ int grad_tail_run(int64_t M, int64_t M_pad, const void* Z, const void* X, const 
   double* Pf = sigma;
   tail_reduce_kernel<<<tiles, 256, 0, st>>>(L, 0, part);
   sum_kernel<<<1, 32, 0, st>>>(part, tiles, scal + 0);
+  tail_diag_range_kernel<<<1, kTT, 0, st>>>(L, nt, M, scal + 6);   // cond(Kuu) lower bound
   tail_reduce_kernel<<<tiles, 256, 0, st>>>(Pf, 0, part);
   sum_kernel<<<1, 32, 0, st>>>(part, tiles, scal + 1);
   TB_LAUNCH_CHECK("grad_logdet");
@@ -1480,7 +1482,7 @@ int grad_tail_run(int64_t M, int64_t M_pad, const void* Z, const void* X, const 
   sum_kernel<<<1, 32, 0, st>>>(ak_part, nt, scal + 4);
   sum_kernel<<<1, 32, 0, st>>>(wk_part, nt, scal + 5);
   TB_LAUNCH_CHECK("grad_scalars");
-  TB_CUDA_TRY(cudaMemcpyAsync(out8, scal, 6 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  TB_CUDA_TRY(cudaMemcpyAsync(out8, scal, 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
   int h_info = 0;
   TB_CUDA_TRY(cudaMemcpyAsync(&h_info, info, sizeof(int), cudaMemcpyDeviceToHost, st));
   TB_CUDA_TRY(cudaStreamSynchronize(st));

@@ -225,6 +225,15 @@ class SGPR:
                 s = self.statistics()
         return self._tail_dense(s)
 
+    def _dense_grad_fits(self, chunk_n: int) -> bool:
+        """Whether the dense gradient path fits memory_limit."""
+        if self.memory_limit is None:
+            return True
+        from .sizes import as_limit
+        M = int(self.Z.shape[0])
+        resident = (self.X.numel() + self.y.numel() + self.Z.numel()) * self.X.element_size()
+        return grad_memory_bytes(M, self.dim, chunk_n) + resident <= as_limit(self.memory_limit)
+
     def _refit_ill_conditioned(self):
         """After the packed factorisation failed: drop the consumed
         statistics and, for engine "auto", recompute them in fp64 (at cond(A)
@@ -363,7 +372,13 @@ class SGPR:
         M, dim = int(self.Z.shape[0]), self.dim
         if self.tail == "packed" and dim <= 16 and self.grad_peak_bytes() >= 0:
             try:
-                return self._elbo_and_grads_packed()
+                res = self._elbo_and_grads_packed()
+                # as in _tail: engine "auto" redoes an ill-conditioned problem
+                # from fp64 statistics when the dense path fits the limit
+                if not (self.engine == "auto" and self.cond_kuu_lb > COND_FP64
+                        and self._dense_grad_fits(chunk_n)):
+                    return res
+                self._refit_ill_conditioned()
             except EvaluationError as ex:
                 # as in _tail: a negative pivot of the packed factorisation
                 # of A on a very ill-conditioned problem -> the dense path
@@ -510,7 +525,8 @@ class SGPR:
             import torch.distributed as dist
             dist.all_reduce(gh[:1 + dim], group=self.group)
             dist.all_reduce(gz[:M * dim], group=self.group)
-        sl, sp, uu, tr_ka, tr_ak, wkw = (float(t) for t in out8[:6].tolist())
+        sl, sp, uu, tr_ka, tr_ak, wkw, dmin, dmax = (float(t) for t in out8.tolist())
+        self.cond_kuu_lb = dmax / dmin if dmin > 0 else math.inf
         N, s2, var, yy = float(s.N), self.noise_variance, self.variance, s.yy
         logdet_k, logdet_a = 2.0 * sl, 2.0 * sp
         vw = uu / s2                                 # v^T A^-1 v / s2

@@ -72,5 +72,11 @@ def test_sgpr_random_limits_hold_on_the_device(seed):
     (e2, g), peak2 = _measure(m2.elbo_and_grads)
     assert peak2 + inputs <= max(limit, need), (peak2 + inputs, need)
     # two tail formulations; the ELBO is a small difference of O(N var / s2)
-    # terms, which they round differently at ~1e-10 of their size
-    assert abs(e2 - e) <= 1e-9 * max(abs(e), N * 1.0 / 0.05)
+    # terms, which they round differently at ~1e-10 of their size - unless an
+    # ill-conditioned Kuu moved one of them to fp64 statistics (engine "auto"
+    # refits when the dense path fits its limit; the two limits differ here),
+    # where the fixed-point statistics' own accuracy is the yardstick
+    if m.engine == m2.engine:
+        assert abs(e2 - e) <= 1e-9 * max(abs(e), N * 1.0 / 0.05)
+    else:
+        assert abs(e2 - e) <= 1e-4 * abs(e)
